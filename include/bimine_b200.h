@@ -1,0 +1,201 @@
+/*
+ * bimine_b200.h -- C ABI of the B200 (sm_100a) sentence-alignment hot path.
+ *
+ * This is the drop-in boundary for the reference package `bimine`
+ * (arXiv 1512.01641 reimplementation, /root/reference/pkg).  The
+ * reference has exactly one native FFI, the Cython module `_nwcore`
+ * that `bimine.kernels` binds at import time (kernels.py:17-31):
+ *
+ *   nw_fill(double[:, ::1] dp, const double[:, ::1] sim,
+ *           double mismatch, double bonus, double gap)            _nwcore.pyx:19-36
+ *   nw_fill_wavefront(dp, sim, mismatch, bonus, gap, int workers)  _nwcore.pyx:45-70
+ *
+ * `bimine_nw_fill` / `bimine_nw_fill_wavefront` below replace those two
+ * entry points one for one (host pointers, caller-initialised boundary,
+ * interior written in place).  The remaining entry points move the rest
+ * of the north-star path -- the Python loops of align.py:102-129
+ * (build_score_matrix), align.py:132-163 (_traceback) and
+ * align.py:323-332 (filter_by_threshold) -- behind the same boundary as
+ * batched device calls, so the Python host only tokenises and packs.
+ *
+ * Conventions
+ *  - every function returns 0 on success or a negative BIMINE_E* code;
+ *    nothing throws across the ABI; bimine_last_error() returns a
+ *    thread-local message for the last failure on the calling thread.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Calls are stream ordered; *_host calls synchronise the
+ *    stream before returning.
+ *  - "dev" pointers are CUDA device pointers, "host" pointers are plain
+ *    host memory (pinned memory makes the copies asynchronous-fast).
+ *  - all floating point is IEEE binary64, round-to-nearest, with no
+ *    contraction, reproducing CPython float arithmetic bit for bit.
+ */
+#ifndef BIMINE_B200_H
+#define BIMINE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BIMINE_OK 0
+#define BIMINE_E_ARG (-1)      /* invalid argument (shape, NULL, range)            */
+#define BIMINE_E_CUDA (-2)     /* CUDA runtime error                                */
+#define BIMINE_E_LIMIT (-3)    /* input exceeds a documented kernel capacity        */
+#define BIMINE_E_NOMEM (-4)    /* allocation failed                                 */
+
+/* Model layout: the 21 doubles of SimilarityModel (classifier.py:115-124)
+ * in this order: weights[6], bias, sigmoid_a, sigmoid_b,
+ * feature_means[6], feature_scales[6]. */
+#define BIMINE_MODEL_DOUBLES 21
+
+/* Packed batch of document pairs.  Sentences are tokenised on the host
+ * (text.py:97-104) into joint-vocabulary ids; every source and target
+ * token string maps to one id space, so `t in target.token_set`
+ * (classifier.py:78) and `token_set & token_set` (classifier.py:94) are
+ * integer equality.  Per sentence the host supplies len(tokens),
+ * len(set(tokens)) and len(text) (SentenceProfile, classifier.py:34-47). */
+typedef struct bimine_batch {
+  int64_t n_pairs;
+  int64_t n_sentences;
+  int64_t n_tokens;
+  const int32_t *tokens;       /* [n_tokens] ids, sentences back to back          */
+  const int64_t *sent_tok_off; /* [n_sentences] first token of each sentence      */
+  const int32_t *sent_len;     /* [n_sentences] token count (>= 1)                */
+  const int32_t *sent_uniq;    /* [n_sentences] distinct token count              */
+  const int32_t *sent_chars;   /* [n_sentences] code points of the raw sentence   */
+  const int64_t *pair_src;     /* [n_pairs] index of the pair's first source sent */
+  const int32_t *pair_n;       /* [n_pairs] source sentence count N (>= 1)        */
+  const int64_t *pair_tgt;     /* [n_pairs] index of the first target sentence    */
+  const int32_t *pair_m;       /* [n_pairs] target sentence count M (>= 1)        */
+  const int64_t *pair_sim_off; /* [n_pairs] offset of the row-major N x M block   */
+} bimine_batch;
+
+/* Bilingual dictionary in CSR form over source ids (Lexicon,
+ * lexicon.py:22-59).  Only entries with p > 0 are kept: the reference
+ * reads them only through `p > best` with best >= 0 (classifier.py:78)
+ * and `p > 0.0` (classifier.py:58). */
+typedef struct bimine_dict_view {
+  int64_t n_rows;          /* source ids >= n_rows have no translations */
+  int64_t n_entries;
+  const int64_t *row_ptr;  /* [n_rows + 1]                               */
+  const int32_t *tgt;      /* [n_entries] target ids                     */
+  const double *prob;      /* [n_entries] probabilities, all > 0         */
+} bimine_dict_view;
+
+/* One mined match, filter_by_threshold's (float(sim[i, j]), i, j)
+ * (align.py:323-332). */
+typedef struct bimine_match {
+  double score;
+  int32_t i;
+  int32_t j;
+} bimine_match;
+
+/* Opaque device-resident dictionary (one per device). */
+typedef struct bimine_dict bimine_dict;
+
+const char *bimine_last_error(void);
+const char *bimine_version(void);
+
+/* ---- B1: reference FFI replacement (_nwcore.pyx:19-36, :45-70) -------
+ * dp:  host, (n+1) x (m+1) row-major, row 0 and column 0 initialised by
+ *      the caller (kernels.py:42-48); the interior is written in place.
+ * sim: host, n x m row-major, the already reversed matrix
+ *      (kernels.py:55,70; align.py:166-167).
+ * Bit-identical to the reference fill.  `workers` is accepted for
+ * signature compatibility; the anti-diagonal split is the GPU's. */
+int bimine_nw_fill(double *dp, const double *sim, int64_t n, int64_t m,
+                   double mismatch, double bonus, double gap, void *stream);
+int bimine_nw_fill_wavefront(double *dp, const double *sim, int64_t n,
+                             int64_t m, double mismatch, double bonus,
+                             double gap, int workers, void *stream);
+
+/* ---- dictionary -----------------------------------------------------
+ * COO host arrays (src, tgt, prob) in lexicon iteration order.  Entries
+ * with !(p > 0) are dropped; a repeated (src, tgt) keeps the last value
+ * (read_lexicon, lexicon.py:177).  Builds a CSR on the host and uploads
+ * it to the current device. */
+int bimine_dict_create(const int32_t *src, const int32_t *tgt,
+                       const double *prob, int64_t n_entries,
+                       bimine_dict **out);
+int bimine_dict_destroy(bimine_dict *dict);
+int bimine_dict_view_get(const bimine_dict *dict, bimine_dict_view *view_dev);
+int64_t bimine_dict_entries(const bimine_dict *dict);
+
+/* ---- score matrix (align.py:102-129) -------------------------------
+ * batch_dev: every pointer in the struct is a device pointer.
+ * model: host array of BIMINE_MODEL_DOUBLES.
+ * max_n / max_m: max over pairs of N and M (grid extents).
+ * sim_dev: output, written once, row-major per pair at pair_sim_off. */
+int bimine_score_batch(const bimine_dict *dict, const double *model,
+                       const bimine_batch *batch_dev, int32_t max_n,
+                       int32_t max_m, double *sim_dev, void *stream);
+
+/* ---- NW + traceback + threshold filter --------------------------------
+ * Problem p = pair * n_settings + s aligns pair `pair` under setting s
+ * (gap[s], threshold[s]); mismatch/bonus are shared (MiningConfig,
+ * align.py:73-90).  Fill on the reversed matrix (align.py:170-181),
+ * traceback with the diag > source-gap > target-gap tie order
+ * (align.py:132-163), emit Match steps with sim >= threshold
+ * (align.py:323-332).
+ *   out_off_dev[p]   : slot offset of problem p in matches_dev (capacity
+ *                      min(N, M) slots per problem)
+ *   counts_dev[p]    : number of matches emitted for problem p
+ *   score_dev[p]     : dp_rev[N, M] (Alignment.score), may be NULL
+ * All arrays are device pointers; gap/threshold are device arrays of
+ * n_settings doubles. */
+int bimine_nw_mine_batch(const double *sim_dev, const int64_t *pair_sim_off,
+                         const int32_t *pair_n, const int32_t *pair_m,
+                         int64_t n_pairs, int32_t n_settings,
+                         const double *gap_dev, const double *threshold_dev,
+                         double mismatch, double bonus,
+                         const int64_t *out_off_dev, bimine_match *matches_dev,
+                         int32_t *counts_dev, double *score_dev, void *stream);
+
+/* Full step lists for nw_align / nw_align_wavefront (Alignment.steps):
+ * step codes 0 = Match, 1 = GapSource, 2 = GapTarget in forward order,
+ * capacity N + M per pair at step_off_dev[p]; n_steps_dev[p] = count. */
+int bimine_nw_steps_batch(const double *sim_dev, const int64_t *pair_sim_off,
+                          const int32_t *pair_n, const int32_t *pair_m,
+                          int64_t n_pairs, const double *gap_dev,
+                          double mismatch, double bonus,
+                          const int64_t *step_off_dev, uint8_t *steps_dev,
+                          int32_t *n_steps_dev, double *score_dev,
+                          void *stream);
+
+/* Order-preserving compaction of per-problem match slots:
+ * match_base_dev[p] = exclusive prefix sum of counts; compact_dev
+ * receives the matches of problem 0, 1, ... back to back;
+ * total_dev[0] = sum of counts. */
+int bimine_compact_matches(const bimine_match *matches_dev,
+                           const int64_t *out_off_dev,
+                           const int32_t *counts_dev, int64_t n_problems,
+                           int64_t *match_base_dev, bimine_match *compact_dev,
+                           int64_t *total_dev, void *stream);
+
+/* ---- end to end from host buffers (the e2e call) ----------------------
+ * batch_host: host pointers.  Copies the packed batch to the device,
+ * scores, aligns under one setting, filters, compacts and copies back.
+ *   counts_host[n_pairs]        matches per pair
+ *   matches_host[capacity]      compacted matches in pair order
+ *   capacity >= sum over pairs of min(N, M)
+ *   sim_host (optional, may be NULL): the score matrices. */
+int bimine_mine_host(const bimine_dict *dict, const double *model,
+                     const bimine_batch *batch_host, double gap,
+                     double threshold, double mismatch, double bonus,
+                     int32_t *counts_host, bimine_match *matches_host,
+                     int64_t capacity, int64_t *total_host, double *sim_host,
+                     void *stream);
+
+/* ---- test hook -------------------------------------------------------
+ * Device evaluation of the score_from_margin logistic's exp
+ * (classifier.py:145-147, glibc __exp_fma restated) over n host doubles;
+ * used by the parity tests to pin the device exp against host math.exp. */
+int bimine_exp_device(const double *x_host, double *y_host, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BIMINE_B200_H */

@@ -1,0 +1,245 @@
+"""Host side of the boundary: tokenise, map to joint-vocabulary ids, pack.
+
+The reference profiles every sentence inside build_score_matrix
+(align.py:112-122 -> classifier.profile_sentence, classifier.py:43-47 ->
+tokenize, text.py:97-104) and then compares token *strings*.  Here the
+host does exactly that tokenisation once, maps every token string to an
+integer in one joint vocabulary shared by both languages and by the
+dictionary, and packs the result into the flat arrays of
+``bimine_batch`` (include/bimine_b200.h).  Equality of ids is equality
+of strings, so the device computes the same set memberships.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from .text import tokenize
+
+
+class Vocabulary:
+    """str -> int32 id, grown on demand; one instance per Lexicon."""
+
+    __slots__ = ("ids", "words")
+
+    def __init__(self) -> None:
+        self.ids: dict[str, int] = {}
+        self.words: list[str] = []
+
+    def __len__(self) -> int:
+        return len(self.words)
+
+    def get(self, word: str) -> int:
+        i = self.ids.get(word)
+        if i is None:
+            i = len(self.words)
+            self.ids[word] = i
+            self.words.append(word)
+        return i
+
+
+@dataclass
+class PackedBatch:
+    tokens: np.ndarray  # int32 [T]
+    sent_tok_off: np.ndarray  # int64 [S]
+    sent_len: np.ndarray  # int32 [S]
+    sent_uniq: np.ndarray  # int32 [S]
+    sent_chars: np.ndarray  # int32 [S]
+    pair_src: np.ndarray  # int64 [P]
+    pair_n: np.ndarray  # int32 [P]
+    pair_tgt: np.ndarray  # int64 [P]
+    pair_m: np.ndarray  # int32 [P]
+    pair_sim_off: np.ndarray  # int64 [P]
+
+    @property
+    def n_pairs(self) -> int:
+        return int(self.pair_n.shape[0])
+
+    @property
+    def n_sentences(self) -> int:
+        return int(self.sent_len.shape[0])
+
+    @property
+    def n_tokens(self) -> int:
+        return int(self.tokens.shape[0])
+
+    @property
+    def n_cells(self) -> int:
+        return int(self.pair_sim_off[-1] + int(self.pair_n[-1]) * int(self.pair_m[-1])) if self.n_pairs else 0
+
+    def match_capacity(self) -> np.ndarray:
+        """Per-pair slot offsets for matches (capacity min(N, M) each) and total."""
+        cap = np.minimum(self.pair_n, self.pair_m).astype(np.int64)
+        off = np.zeros(self.n_pairs + 1, dtype=np.int64)
+        np.cumsum(cap, out=off[1:])
+        return off
+
+    def nbytes(self) -> int:
+        return sum(
+            a.nbytes
+            for a in (
+                self.tokens, self.sent_tok_off, self.sent_len, self.sent_uniq,
+                self.sent_chars, self.pair_src, self.pair_n, self.pair_tgt,
+                self.pair_m, self.pair_sim_off,
+            )
+        )
+
+    @staticmethod
+    def from_token_lengths(
+        tokens: np.ndarray,
+        sent_len: np.ndarray,
+        sent_chars: np.ndarray,
+        pair_src: np.ndarray,
+        pair_n: np.ndarray,
+        pair_tgt: np.ndarray,
+        pair_m: np.ndarray,
+        sent_uniq: np.ndarray | None = None,
+    ) -> "PackedBatch":
+        tokens = np.ascontiguousarray(tokens, dtype=np.int32)
+        sent_len = np.ascontiguousarray(sent_len, dtype=np.int32)
+        off = np.zeros(sent_len.shape[0], dtype=np.int64)
+        if sent_len.shape[0] > 1:
+            np.cumsum(sent_len[:-1], out=off[1:])
+        if sent_uniq is None:
+            sent_uniq = unique_counts(tokens, sent_len)
+        pair_n = np.ascontiguousarray(pair_n, dtype=np.int32)
+        pair_m = np.ascontiguousarray(pair_m, dtype=np.int32)
+        cells = pair_n.astype(np.int64) * pair_m.astype(np.int64)
+        sim_off = np.zeros(pair_n.shape[0], dtype=np.int64)
+        if pair_n.shape[0] > 1:
+            np.cumsum(cells[:-1], out=sim_off[1:])
+        return PackedBatch(
+            tokens=tokens,
+            sent_tok_off=off,
+            sent_len=sent_len,
+            sent_uniq=np.ascontiguousarray(sent_uniq, dtype=np.int32),
+            sent_chars=np.ascontiguousarray(sent_chars, dtype=np.int32),
+            pair_src=np.ascontiguousarray(pair_src, dtype=np.int64),
+            pair_n=pair_n,
+            pair_tgt=np.ascontiguousarray(pair_tgt, dtype=np.int64),
+            pair_m=pair_m,
+            pair_sim_off=sim_off,
+        )
+
+    def select(self, pairs: Sequence[int] | np.ndarray) -> "PackedBatch":
+        """Sub-batch of the given pairs (order kept), re-packed contiguously."""
+        pairs = np.asarray(pairs, dtype=np.int64)
+        sent_idx = []
+        for p in pairs.tolist():
+            sent_idx.append(np.arange(self.pair_src[p], self.pair_src[p] + self.pair_n[p]))
+            sent_idx.append(np.arange(self.pair_tgt[p], self.pair_tgt[p] + self.pair_m[p]))
+        sent_idx = np.concatenate(sent_idx) if sent_idx else np.zeros(0, np.int64)
+        lens = self.sent_len[sent_idx]
+        tok_idx = np.concatenate(
+            [np.arange(self.sent_tok_off[s], self.sent_tok_off[s] + self.sent_len[s]) for s in sent_idx.tolist()]
+        ) if sent_idx.size else np.zeros(0, np.int64)
+        pn = self.pair_n[pairs].astype(np.int64)
+        pm = self.pair_m[pairs].astype(np.int64)
+        starts = np.zeros(pairs.shape[0], dtype=np.int64)
+        if pairs.shape[0] > 1:
+            np.cumsum((pn + pm)[:-1], out=starts[1:])
+        return PackedBatch.from_token_lengths(
+            self.tokens[tok_idx], lens, self.sent_chars[sent_idx],
+            starts, pn, starts + pn, pm, sent_uniq=self.sent_uniq[sent_idx],
+        )
+
+
+def unique_counts(tokens: np.ndarray, sent_len: np.ndarray) -> np.ndarray:
+    """len(set(tokens)) per sentence, vectorised."""
+    n_sent = sent_len.shape[0]
+    if tokens.shape[0] == 0:
+        return np.zeros(n_sent, dtype=np.int32)
+    sent_of = np.repeat(np.arange(n_sent, dtype=np.int64), sent_len)
+    key = sent_of << 32 | tokens.astype(np.int64) & 0xFFFFFFFF
+    key.sort()
+    first = np.ones(key.shape[0], dtype=bool)
+    first[1:] = key[1:] != key[:-1]
+    return np.bincount(key[first] >> 32, minlength=n_sent).astype(np.int32)
+
+
+class SentenceError(ValueError):
+    """An untokenizable sentence, with the side/index prefix the reference
+    adds in build_score_matrix (align.py:112-119)."""
+
+
+def profile_ids(sentence: str, vocab: Vocabulary) -> list[int]:
+    """profile_sentence (classifier.py:43-47) down to token ids."""
+    tokens = tokenize(sentence)
+    if not tokens:
+        raise ValueError(f"untokenizable sentence: {sentence!r}")
+    get = vocab.get
+    return [get(t) for t in tokens]
+
+
+class BatchBuilder:
+    """Accumulates document pairs (as sentence strings) into a PackedBatch."""
+
+    def __init__(self, vocab: Vocabulary) -> None:
+        self.vocab = vocab
+        self.tokens: list[int] = []
+        self.sent_len: list[int] = []
+        self.sent_uniq: list[int] = []
+        self.sent_chars: list[int] = []
+        self.pair_src: list[int] = []
+        self.pair_n: list[int] = []
+        self.pair_tgt: list[int] = []
+        self.pair_m: list[int] = []
+
+    def _profiles(self, sentences: Sequence[str], side: str) -> list[list[int]]:
+        out = []
+        for index, sentence in enumerate(sentences):
+            try:
+                out.append(profile_ids(sentence, self.vocab))
+            except ValueError as exc:
+                raise SentenceError(f"{side} sentence {index}: {exc}") from None
+        return out
+
+    def add_pair(self, source: Sequence[str], target: Sequence[str]) -> int:
+        """Tokenise and append one pair; raises ValueError with the
+        reference's messages (align.py:109-119) and leaves the builder
+        unchanged on error.  Returns the pair's index in the batch."""
+        if not source or not target:
+            raise ValueError("both sentence sequences must be non-empty")
+        src = self._profiles(source, "source")
+        tgt = self._profiles(target, "target")
+        first = len(self.sent_len)
+        for ids, text in zip(src + tgt, list(source) + list(target)):
+            self.tokens.extend(ids)
+            self.sent_len.append(len(ids))
+            self.sent_uniq.append(len(set(ids)))
+            self.sent_chars.append(len(text))
+        self.pair_src.append(first)
+        self.pair_n.append(len(src))
+        self.pair_tgt.append(first + len(src))
+        self.pair_m.append(len(tgt))
+        return len(self.pair_n) - 1
+
+    def build(self) -> PackedBatch:
+        return PackedBatch.from_token_lengths(
+            np.asarray(self.tokens, dtype=np.int32),
+            np.asarray(self.sent_len, dtype=np.int32),
+            np.asarray(self.sent_chars, dtype=np.int32),
+            np.asarray(self.pair_src, dtype=np.int64),
+            np.asarray(self.pair_n, dtype=np.int32),
+            np.asarray(self.pair_tgt, dtype=np.int64),
+            np.asarray(self.pair_m, dtype=np.int32),
+            sent_uniq=np.asarray(self.sent_uniq, dtype=np.int32),
+        )
+
+
+def lexicon_arrays(entries: Iterable[tuple[str, str, float]], vocab: Vocabulary):
+    """COO (src, tgt, prob) arrays of a lexicon in its iteration order."""
+    src, tgt, prob = [], [], []
+    get = vocab.get
+    for s, t, p in entries:
+        src.append(get(s))
+        tgt.append(get(t))
+        prob.append(float(p))
+    return (
+        np.asarray(src, dtype=np.int32),
+        np.asarray(tgt, dtype=np.int32),
+        np.asarray(prob, dtype=np.float64),
+    )
