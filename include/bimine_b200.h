@@ -128,10 +128,13 @@ int64_t bimine_dict_entries(const bimine_dict *dict);
  * batch_dev: every pointer in the struct is a device pointer.
  * model: host array of BIMINE_MODEL_DOUBLES.
  * max_n / max_m: max over pairs of N and M (grid extents).
+ * max_uniq / max_len: max over sentences of distinct / total tokens
+ *   (sizes the shared-memory hash; BIMINE_E_LIMIT above 16384 / 65535).
  * sim_dev: output, written once, row-major per pair at pair_sim_off. */
 int bimine_score_batch(const bimine_dict *dict, const double *model,
                        const bimine_batch *batch_dev, int32_t max_n,
-                       int32_t max_m, double *sim_dev, void *stream);
+                       int32_t max_m, int32_t max_uniq, int32_t max_len,
+                       double *sim_dev, void *stream);
 
 /* ---- NW + traceback + threshold filter --------------------------------
  * Problem p = pair * n_settings + s aligns pair `pair` under setting s
@@ -145,10 +148,12 @@ int bimine_score_batch(const bimine_dict *dict, const double *model,
  *   counts_dev[p]    : number of matches emitted for problem p
  *   score_dev[p]     : dp_rev[N, M] (Alignment.score), may be NULL
  * All arrays are device pointers; gap/threshold are device arrays of
- * n_settings doubles. */
+ * n_settings doubles; max_n / max_m (host scalars) bound N and M and
+ * size the per-warp direction storage. */
 int bimine_nw_mine_batch(const double *sim_dev, const int64_t *pair_sim_off,
                          const int32_t *pair_n, const int32_t *pair_m,
-                         int64_t n_pairs, int32_t n_settings,
+                         int64_t n_pairs, int32_t max_n, int32_t max_m,
+                         int32_t n_settings,
                          const double *gap_dev, const double *threshold_dev,
                          double mismatch, double bonus,
                          const int64_t *out_off_dev, bimine_match *matches_dev,
@@ -159,7 +164,8 @@ int bimine_nw_mine_batch(const double *sim_dev, const int64_t *pair_sim_off,
  * capacity N + M per pair at step_off_dev[p]; n_steps_dev[p] = count. */
 int bimine_nw_steps_batch(const double *sim_dev, const int64_t *pair_sim_off,
                           const int32_t *pair_n, const int32_t *pair_m,
-                          int64_t n_pairs, const double *gap_dev,
+                          int64_t n_pairs, int32_t max_n, int32_t max_m,
+                          const double *gap_dev,
                           double mismatch, double bonus,
                           const int64_t *step_off_dev, uint8_t *steps_dev,
                           int32_t *n_steps_dev, double *score_dev,

@@ -1,0 +1,517 @@
+// abi.cu -- the extern "C" boundary (include/bimine_b200.h) and launchers.
+//
+// Single translation unit: the kernels live in the included headers.
+// Built by paper_1512_01641_b200/build.py with
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false
+// (-fmad=false: no contraction anywhere; the glibc exp restatement uses
+// explicit __fma_rn where the host libm fuses).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/bimine_b200.h"
+#include "common.cuh"
+#include "nw_kernel.cuh"
+#include "score_kernel.cuh"
+
+using namespace bimine;
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const std::string &msg) {
+  g_error = msg;
+  return code;
+}
+
+#define BIMINE_CUDA(expr)                                                                  \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(BIMINE_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));      \
+  } while (0)
+
+cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+void pool_setup() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t threshold = UINT64_MAX;  // keep freed blocks cached in the pool
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+  });
+}
+
+int next_pow2(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+int ilog2(int x) {
+  int b = 0;
+  while ((1 << b) < x) ++b;
+  return b;
+}
+
+constexpr int kMaxCapU = 4096;
+constexpr int kMaxCapT = 16384;
+constexpr int kNwWarpsPerBlock = 4;
+constexpr size_t kNwSmemPerBlockMax = 200 * 1024;
+
+}  // namespace
+
+struct bimine_dict {
+  int device = 0;
+  int64_t n_rows = 0;
+  int64_t n_entries = 0;
+  int64_t *row_ptr = nullptr;
+  int32_t *tgt = nullptr;
+  double *prob = nullptr;
+};
+
+extern "C" {
+
+const char *bimine_last_error(void) { return g_error.c_str(); }
+
+const char *bimine_version(void) { return "bimine_b200 0.1.0 (sm_100a)"; }
+
+// ------------------------------------------------------------------------
+// dictionary
+// ------------------------------------------------------------------------
+
+int bimine_dict_create(const int32_t *src, const int32_t *tgt, const double *prob, int64_t n_entries,
+                       bimine_dict **out) {
+  if (!out || n_entries < 0 || (n_entries > 0 && (!src || !tgt || !prob)))
+    return fail(BIMINE_E_ARG, "bimine_dict_create: bad arguments");
+  // last value per (src, tgt) wins (lexicon.py:177); drop !(p > 0)
+  std::vector<int64_t> order(n_entries);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) {
+    if (src[x] != src[y]) return src[x] < src[y];
+    return tgt[x] < tgt[y];
+  });
+  std::vector<int32_t> ks, kt;
+  std::vector<double> kp;
+  ks.reserve(n_entries);
+  kt.reserve(n_entries);
+  kp.reserve(n_entries);
+  for (int64_t k = 0; k < n_entries; ++k) {
+    const int64_t e = order[k];
+    const bool last_of_key =
+        k + 1 == n_entries || src[order[k + 1]] != src[e] || tgt[order[k + 1]] != tgt[e];
+    if (!last_of_key) continue;  // stable sort: the later duplicate comes last
+    if (src[e] < 0 || tgt[e] < 0) return fail(BIMINE_E_ARG, "bimine_dict_create: negative token id");
+    if (!(prob[e] > 0.0)) continue;
+    ks.push_back(src[e]);
+    kt.push_back(tgt[e]);
+    kp.push_back(prob[e]);
+  }
+  auto *d = new bimine_dict();
+  cudaGetDevice(&d->device);
+  d->n_entries = (int64_t)ks.size();
+  d->n_rows = ks.empty() ? 0 : (int64_t)ks.back() + 1;
+  std::vector<int64_t> row_ptr(d->n_rows + 1, 0);
+  for (int32_t s : ks) row_ptr[s + 1]++;
+  for (int64_t r = 0; r < d->n_rows; ++r) row_ptr[r + 1] += row_ptr[r];
+  auto cleanup = [&](const char *what) {
+    cudaFree(d->row_ptr);
+    cudaFree(d->tgt);
+    cudaFree(d->prob);
+    delete d;
+    return fail(BIMINE_E_CUDA, std::string("bimine_dict_create: ") + what);
+  };
+  if (cudaMalloc(&d->row_ptr, sizeof(int64_t) * (d->n_rows + 1)) != cudaSuccess) return cleanup("cudaMalloc");
+  if (cudaMalloc(&d->tgt, sizeof(int32_t) * std::max<int64_t>(1, d->n_entries)) != cudaSuccess) return cleanup("cudaMalloc");
+  if (cudaMalloc(&d->prob, sizeof(double) * std::max<int64_t>(1, d->n_entries)) != cudaSuccess) return cleanup("cudaMalloc");
+  if (cudaMemcpy(d->row_ptr, row_ptr.data(), sizeof(int64_t) * (d->n_rows + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
+      (d->n_entries &&
+       (cudaMemcpy(d->tgt, kt.data(), sizeof(int32_t) * d->n_entries, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d->prob, kp.data(), sizeof(double) * d->n_entries, cudaMemcpyHostToDevice) != cudaSuccess)))
+    return cleanup("cudaMemcpy");
+  *out = d;
+  return BIMINE_OK;
+}
+
+int bimine_dict_destroy(bimine_dict *d) {
+  if (!d) return BIMINE_OK;
+  cudaFree(d->row_ptr);
+  cudaFree(d->tgt);
+  cudaFree(d->prob);
+  delete d;
+  return BIMINE_OK;
+}
+
+int bimine_dict_view_get(const bimine_dict *d, bimine_dict_view *v) {
+  if (!d || !v) return fail(BIMINE_E_ARG, "bimine_dict_view_get: null");
+  v->n_rows = d->n_rows;
+  v->n_entries = d->n_entries;
+  v->row_ptr = d->row_ptr;
+  v->tgt = d->tgt;
+  v->prob = d->prob;
+  return BIMINE_OK;
+}
+
+int64_t bimine_dict_entries(const bimine_dict *d) { return d ? d->n_entries : -1; }
+
+// ------------------------------------------------------------------------
+// score matrix
+// ------------------------------------------------------------------------
+
+int bimine_score_batch(const bimine_dict *dict, const double *model, const bimine_batch *b, int32_t max_n,
+                       int32_t max_m, int32_t max_uniq, int32_t max_len, double *sim_dev, void *stream) {
+  if (!dict || !model || !b || !sim_dev) return fail(BIMINE_E_ARG, "bimine_score_batch: null argument");
+  if (b->n_pairs == 0) return BIMINE_OK;
+  if (max_n < 1 || max_m < 1 || max_uniq < 1 || max_len < 1)
+    return fail(BIMINE_E_ARG, "bimine_score_batch: empty document or sentence");
+  if (max_uniq > kMaxCapU || max_len > kMaxCapT)
+    return fail(BIMINE_E_LIMIT, "bimine_score_batch: a sentence has more than 4096 distinct or 16384 total tokens");
+  if (b->n_pairs > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: more than 2^31-1 pairs per call");
+  ScoreArgs A;
+  A.b = to_dev(*b);
+  A.d = DictDev{dict->n_rows, dict->row_ptr, dict->tgt, dict->prob};
+  A.md = to_model(model);
+  A.sim = sim_dev;
+  A.cap_u = std::min(kMaxCapU, std::max(1024, next_pow2(max_uniq)));
+  A.cap_t = std::min(kMaxCapT, std::max(4096, next_pow2(max_len)));
+  A.hash_bits = ilog2(2 * A.cap_u);
+  static int *status = nullptr;
+  if (!status) BIMINE_CUDA(cudaMalloc(&status, sizeof(int)));
+  A.status = status;
+  const size_t smem = score_smem_layout(nullptr, A.cap_u, A.cap_t, nullptr);
+  BIMINE_CUDA(cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)b->n_pairs, (unsigned)((max_n + kScoreTile - 1) / kScoreTile),
+            (unsigned)((max_m + kScoreTile - 1) / kScoreTile));
+  if (grid.y > 65535 || grid.z > 65535) return fail(BIMINE_E_LIMIT, "bimine_score_batch: document too long");
+  score_kernel<<<grid, kScoreThreads, smem, as_stream(stream)>>>(A);
+  BIMINE_CUDA(cudaGetLastError());
+  return BIMINE_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------
+// NW launch helper
+// ------------------------------------------------------------------------
+namespace {
+
+template <int MODE>
+int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
+  if (A.n_problems == 0) return BIMINE_OK;
+  const int row_d = ((max_m + 1) + 1) & ~1;                      // doubles, even
+  const int64_t dir_w = (int64_t)(max_n + 1) * ((max_m >> 4) + 1);  // u32 words
+  const size_t per_warp = (size_t)row_d * 8 + (size_t)dir_w * 4;
+  A.row_doubles_per_warp = row_d;
+  if (MODE == kNwTable) A.dir_words_per_warp = 0;
+  const size_t per_block = per_warp * kNwWarpsPerBlock;
+  if (MODE != kNwTable && dir_w < (1LL << 31) && per_block <= kNwSmemPerBlockMax) {
+    A.dir_words_per_warp = (int)dir_w;
+    A.g_dirs = nullptr;
+    A.g_rows = nullptr;
+    BIMINE_CUDA(cudaFuncSetAttribute(nw_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per_block));
+    int blocks_per_sm = 0;
+    BIMINE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, nw_kernel<MODE>,
+                                                              kNwWarpsPerBlock * 32, per_block));
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    const int64_t want = (A.n_problems + kNwWarpsPerBlock - 1) / kNwWarpsPerBlock;
+    const int64_t grid = std::min<int64_t>(want, (int64_t)num_sms() * blocks_per_sm);
+    nw_kernel<MODE><<<(unsigned)grid, kNwWarpsPerBlock * 32, per_block, st>>>(A);
+    BIMINE_CUDA(cudaGetLastError());
+    return BIMINE_OK;
+  }
+  // global scratch: one slot per launched warp, bounded to ~2 GiB
+  if (dir_w >= (1LL << 31)) return fail(BIMINE_E_LIMIT, "nw: alignment table too large");
+  int64_t warps = std::min<int64_t>(A.n_problems, (int64_t)num_sms() * 16);
+  warps = std::max<int64_t>(1, std::min<int64_t>(warps, (int64_t)((size_t)2 << 30) / (int64_t)per_warp));
+  const int64_t blocks = (warps + kNwWarpsPerBlock - 1) / kNwWarpsPerBlock;
+  const int64_t slots = blocks * kNwWarpsPerBlock;  // every launched warp owns a slot
+  A.dir_words_per_warp = (MODE == kNwTable) ? 0 : (int)dir_w;
+  void *scratch = nullptr;
+  BIMINE_CUDA(cudaMallocAsync(&scratch, per_warp * slots, st));
+  A.g_rows = (double *)scratch;  // [slots][row_d] then [slots][dir_w]
+  A.g_dirs = (uint32_t *)((char *)scratch + (size_t)row_d * 8 * slots);
+  if (MODE == kNwTable) A.g_dirs = (uint32_t *)A.g_rows;  // never dereferenced; marks "global"
+  nw_kernel<MODE><<<(unsigned)blocks, kNwWarpsPerBlock * 32, 0, st>>>(A);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return fail(BIMINE_E_CUDA, std::string("nw_kernel: ") + cudaGetErrorString(e));
+  return BIMINE_OK;
+}
+
+NwArgs nw_args_base(const double *sim, const int64_t *sim_off, const int32_t *pn, const int32_t *pm,
+                    int64_t n_problems, int32_t n_settings, const double *gap, double mismatch, double bonus) {
+  NwArgs A;
+  memset(&A, 0, sizeof(A));
+  A.sim = sim;
+  A.sim_off = sim_off;
+  A.pair_n = pn;
+  A.pair_m = pm;
+  A.problem_ids = nullptr;
+  A.n_problems = n_problems;
+  A.n_settings = n_settings;
+  A.gap = gap;
+  A.mismatch = mismatch;
+  A.bonus = bonus;
+  return A;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bimine_nw_mine_batch(const double *sim_dev, const int64_t *pair_sim_off, const int32_t *pair_n,
+                         const int32_t *pair_m, int64_t n_pairs, int32_t max_n, int32_t max_m, int32_t n_settings,
+                         const double *gap_dev, const double *threshold_dev, double mismatch, double bonus,
+                         const int64_t *out_off_dev, bimine_match *matches_dev, int32_t *counts_dev,
+                         double *score_dev, void *stream) {
+  if (!sim_dev || !pair_sim_off || !pair_n || !pair_m || !gap_dev || !threshold_dev || !out_off_dev ||
+      !matches_dev || !counts_dev || n_settings < 1)
+    return fail(BIMINE_E_ARG, "bimine_nw_mine_batch: bad arguments");
+  if (n_pairs == 0) return BIMINE_OK;
+  if (max_n < 1 || max_m < 1) return fail(BIMINE_E_ARG, "bimine_nw_mine_batch: empty matrix");
+  NwArgs A = nw_args_base(sim_dev, pair_sim_off, pair_n, pair_m, n_pairs * n_settings, n_settings, gap_dev,
+                          mismatch, bonus);
+  A.threshold = threshold_dev;
+  A.out_off = out_off_dev;
+  A.matches = matches_dev;
+  A.counts = counts_dev;
+  A.score = score_dev;
+  return launch_nw<kNwMine>(A, max_n, max_m, as_stream(stream));
+}
+
+int bimine_nw_steps_batch(const double *sim_dev, const int64_t *pair_sim_off, const int32_t *pair_n,
+                          const int32_t *pair_m, int64_t n_pairs, int32_t max_n, int32_t max_m,
+                          const double *gap_dev, double mismatch, double bonus, const int64_t *step_off_dev,
+                          uint8_t *steps_dev, int32_t *n_steps_dev, double *score_dev, void *stream) {
+  if (!sim_dev || !pair_sim_off || !pair_n || !pair_m || !gap_dev || !step_off_dev || !steps_dev || !n_steps_dev)
+    return fail(BIMINE_E_ARG, "bimine_nw_steps_batch: bad arguments");
+  if (n_pairs == 0) return BIMINE_OK;
+  if (max_n < 1 || max_m < 1) return fail(BIMINE_E_ARG, "bimine_nw_steps_batch: empty matrix");
+  // one setting per pair: problem q == pair q, gap_dev[q]
+  NwArgs A = nw_args_base(sim_dev, pair_sim_off, pair_n, pair_m, n_pairs, 1, gap_dev, mismatch, bonus);
+  A.step_off = step_off_dev;
+  A.steps = steps_dev;
+  A.n_steps = n_steps_dev;
+  A.score = score_dev;
+  return launch_nw<kNwSteps>(A, max_n, max_m, as_stream(stream));
+}
+
+int bimine_compact_matches(const bimine_match *matches_dev, const int64_t *out_off_dev, const int32_t *counts_dev,
+                           int64_t n_problems, int64_t *match_base_dev, bimine_match *compact_dev,
+                           int64_t *total_dev, void *stream) {
+  if (n_problems == 0) {
+    BIMINE_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(int64_t), as_stream(stream)));
+    return BIMINE_OK;
+  }
+  scan_counts_kernel<<<1, 1024, 0, as_stream(stream)>>>(counts_dev, n_problems, match_base_dev, total_dev);
+  BIMINE_CUDA(cudaGetLastError());
+  const int64_t threads = n_problems * 32;
+  gather_matches_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(
+      matches_dev, out_off_dev, counts_dev, match_base_dev, n_problems, compact_dev);
+  BIMINE_CUDA(cudaGetLastError());
+  return BIMINE_OK;
+}
+
+// ------------------------------------------------------------------------
+// B1 shim: the reference's _nwcore.nw_fill / nw_fill_wavefront
+// ------------------------------------------------------------------------
+
+int bimine_nw_fill(double *dp, const double *sim, int64_t n, int64_t m, double mismatch, double bonus, double gap,
+                   void *stream) {
+  if (!dp || !sim || n < 1 || m < 1) return fail(BIMINE_E_ARG, "bimine_nw_fill: bad arguments");
+  if (n > 0x7fffffff || m > 0x7fffffff) return fail(BIMINE_E_LIMIT, "bimine_nw_fill: too large");
+  pool_setup();
+  cudaStream_t st = as_stream(stream);
+  const size_t sim_b = sizeof(double) * n * m, dp_b = sizeof(double) * (n + 1) * (m + 1);
+  const size_t small_b = 64;
+  char *buf = nullptr;
+  BIMINE_CUDA(cudaMallocAsync((void **)&buf, sim_b + dp_b + small_b, st));
+  double *d_sim = (double *)buf, *d_dp = (double *)(buf + sim_b);
+  char *sm = buf + sim_b + dp_b;
+  int64_t h_off = 0;
+  int32_t h_n = (int32_t)n, h_m = (int32_t)m;
+  // small parameter block: sim_off | n | m | gap
+  char host_small[64];
+  memcpy(host_small, &h_off, 8);
+  memcpy(host_small + 8, &h_n, 4);
+  memcpy(host_small + 12, &h_m, 4);
+  memcpy(host_small + 16, &gap, 8);
+  BIMINE_CUDA(cudaMemcpyAsync(sm, host_small, 24, cudaMemcpyHostToDevice, st));
+  BIMINE_CUDA(cudaMemcpyAsync(d_sim, sim, sim_b, cudaMemcpyHostToDevice, st));
+  BIMINE_CUDA(cudaMemcpyAsync(d_dp, dp, dp_b, cudaMemcpyHostToDevice, st));
+  NwArgs A = nw_args_base(d_sim, (const int64_t *)sm, (const int32_t *)(sm + 8), (const int32_t *)(sm + 12), 1, 1,
+                          (const double *)(sm + 16), mismatch, bonus);
+  A.table = d_dp;
+  int rc = launch_nw<kNwTable>(A, (int32_t)n, (int32_t)m, st);
+  if (rc != BIMINE_OK) {
+    cudaFreeAsync(buf, st);
+    return rc;
+  }
+  BIMINE_CUDA(cudaMemcpyAsync(dp, d_dp, dp_b, cudaMemcpyDeviceToHost, st));
+  BIMINE_CUDA(cudaFreeAsync(buf, st));
+  BIMINE_CUDA(cudaStreamSynchronize(st));
+  return BIMINE_OK;
+}
+
+int bimine_nw_fill_wavefront(double *dp, const double *sim, int64_t n, int64_t m, double mismatch, double bonus,
+                             double gap, int workers, void *stream) {
+  if (workers < 1) return fail(BIMINE_E_ARG, "workers must be >= 1");
+  return bimine_nw_fill(dp, sim, n, m, mismatch, bonus, gap, stream);
+}
+
+// ------------------------------------------------------------------------
+// end to end from host buffers
+// ------------------------------------------------------------------------
+
+int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_batch *h, double gap,
+                     double threshold, double mismatch, double bonus, int32_t *counts_host,
+                     bimine_match *matches_host, int64_t capacity, int64_t *total_host, double *sim_host,
+                     void *stream) {
+  if (!dict || !model || !h || !counts_host || !total_host) return fail(BIMINE_E_ARG, "bimine_mine_host: null");
+  const int64_t P = h->n_pairs, S = h->n_sentences, T = h->n_tokens;
+  *total_host = 0;
+  if (P == 0) return BIMINE_OK;
+  pool_setup();
+  cudaStream_t st = as_stream(stream);
+  int32_t max_n = 0, max_m = 0, max_u = 0, max_l = 0;
+  std::vector<int64_t> out_off(P);
+  int64_t cap = 0, cells = 0;
+  for (int64_t p = 0; p < P; ++p) {
+    const int32_t n = h->pair_n[p], m = h->pair_m[p];
+    if (n < 1 || m < 1) return fail(BIMINE_E_ARG, "bimine_mine_host: empty document");
+    max_n = std::max(max_n, n);
+    max_m = std::max(max_m, m);
+    out_off[p] = cap;
+    cap += std::min(n, m);
+    cells = std::max(cells, h->pair_sim_off[p] + (int64_t)n * m);
+  }
+  for (int64_t s = 0; s < S; ++s) {
+    if (h->sent_len[s] < 1) return fail(BIMINE_E_ARG, "bimine_mine_host: empty sentence");
+    max_u = std::max(max_u, h->sent_uniq[s]);
+    max_l = std::max(max_l, h->sent_len[s]);
+  }
+  if (capacity < cap) return fail(BIMINE_E_ARG, "bimine_mine_host: capacity < sum of min(N, M)");
+  // one device arena, carved in 256-byte aligned pieces
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    size_t o = (off + 255) & ~(size_t)255;
+    off = o + bytes;
+    return o;
+  };
+  const size_t o_tok = carve(4 * T), o_soff = carve(8 * S), o_slen = carve(4 * S), o_suniq = carve(4 * S),
+               o_schar = carve(4 * S), o_psrc = carve(8 * P), o_pn = carve(4 * P), o_ptgt = carve(8 * P),
+               o_pm = carve(4 * P), o_psim = carve(8 * P), o_outoff = carve(8 * P), o_sim = carve(8 * cells),
+               o_slots = carve(sizeof(bimine_match) * cap), o_counts = carve(4 * P), o_base = carve(8 * P),
+               o_comp = carve(sizeof(bimine_match) * cap), o_total = carve(8), o_par = carve(16);
+  char *arena = nullptr;
+  BIMINE_CUDA(cudaMallocAsync((void **)&arena, off, st));
+  auto H2D = [&](size_t o, const void *src, size_t bytes) {
+    return bytes ? cudaMemcpyAsync(arena + o, src, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+  };
+  double par[2] = {gap, threshold};
+  cudaError_t e = cudaSuccess;
+  e = e ? e : H2D(o_tok, h->tokens, 4 * T);
+  e = e ? e : H2D(o_soff, h->sent_tok_off, 8 * S);
+  e = e ? e : H2D(o_slen, h->sent_len, 4 * S);
+  e = e ? e : H2D(o_suniq, h->sent_uniq, 4 * S);
+  e = e ? e : H2D(o_schar, h->sent_chars, 4 * S);
+  e = e ? e : H2D(o_psrc, h->pair_src, 8 * P);
+  e = e ? e : H2D(o_pn, h->pair_n, 4 * P);
+  e = e ? e : H2D(o_ptgt, h->pair_tgt, 8 * P);
+  e = e ? e : H2D(o_pm, h->pair_m, 4 * P);
+  e = e ? e : H2D(o_psim, h->pair_sim_off, 8 * P);
+  e = e ? e : H2D(o_outoff, out_off.data(), 8 * P);
+  e = e ? e : H2D(o_par, par, 16);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(arena, st);
+    return fail(BIMINE_E_CUDA, std::string("bimine_mine_host H2D: ") + cudaGetErrorString(e));
+  }
+  bimine_batch d;
+  d.n_pairs = P;
+  d.n_sentences = S;
+  d.n_tokens = T;
+  d.tokens = (const int32_t *)(arena + o_tok);
+  d.sent_tok_off = (const int64_t *)(arena + o_soff);
+  d.sent_len = (const int32_t *)(arena + o_slen);
+  d.sent_uniq = (const int32_t *)(arena + o_suniq);
+  d.sent_chars = (const int32_t *)(arena + o_schar);
+  d.pair_src = (const int64_t *)(arena + o_psrc);
+  d.pair_n = (const int32_t *)(arena + o_pn);
+  d.pair_tgt = (const int64_t *)(arena + o_ptgt);
+  d.pair_m = (const int32_t *)(arena + o_pm);
+  d.pair_sim_off = (const int64_t *)(arena + o_psim);
+  double *sim = (double *)(arena + o_sim);
+  int rc = bimine_score_batch(dict, model, &d, max_n, max_m, max_u, max_l, sim, stream);
+  const double *pd = (const double *)(arena + o_par);
+  if (rc == BIMINE_OK)
+    rc = bimine_nw_mine_batch(sim, d.pair_sim_off, d.pair_n, d.pair_m, P, max_n, max_m, 1, pd, pd + 1, mismatch,
+                              bonus, (const int64_t *)(arena + o_outoff), (bimine_match *)(arena + o_slots),
+                              (int32_t *)(arena + o_counts), nullptr, stream);
+  if (rc == BIMINE_OK)
+    rc = bimine_compact_matches((const bimine_match *)(arena + o_slots), (const int64_t *)(arena + o_outoff),
+                                (const int32_t *)(arena + o_counts), P, (int64_t *)(arena + o_base),
+                                (bimine_match *)(arena + o_comp), (int64_t *)(arena + o_total), stream);
+  if (rc != BIMINE_OK) {
+    cudaFreeAsync(arena, st);
+    return rc;
+  }
+  e = cudaMemcpyAsync(counts_host, arena + o_counts, 4 * P, cudaMemcpyDeviceToHost, st);
+  e = e ? e : cudaMemcpyAsync(total_host, arena + o_total, 8, cudaMemcpyDeviceToHost, st);
+  if (sim_host && !e) e = cudaMemcpyAsync(sim_host, sim, 8 * cells, cudaMemcpyDeviceToHost, st);
+  e = e ? e : cudaStreamSynchronize(st);
+  if (!e && *total_host > 0 && matches_host)
+    e = cudaMemcpyAsync(matches_host, arena + o_comp, sizeof(bimine_match) * (*total_host), cudaMemcpyDeviceToHost,
+                        st);
+  cudaFreeAsync(arena, st);
+  e = e ? e : cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(BIMINE_E_CUDA, std::string("bimine_mine_host: ") + cudaGetErrorString(e));
+  return BIMINE_OK;
+}
+
+// ------------------------------------------------------------------------
+// test hook: the device exp
+// ------------------------------------------------------------------------
+
+__global__ void exp_kernel(const double *x, double *y, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = glibc_exp(x[i], kExpTableDev);
+}
+
+int bimine_exp_device(const double *x_host, double *y_host, int64_t n) {
+  if (n <= 0) return BIMINE_OK;
+  double *d = nullptr;
+  BIMINE_CUDA(cudaMalloc(&d, 16 * n));
+  cudaError_t e = cudaMemcpy(d, x_host, 8 * n, cudaMemcpyHostToDevice);
+  if (!e) {
+    exp_kernel<<<(unsigned)((n + 255) / 256), 256>>>(d, d + n, n);
+    e = cudaGetLastError();
+  }
+  if (!e) e = cudaMemcpy(y_host, d + n, 8 * n, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e) return fail(BIMINE_E_CUDA, std::string("bimine_exp_device: ") + cudaGetErrorString(e));
+  return BIMINE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// common.cuh -- shared device helpers for the bimine B200 kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bimine_b200.h"
+#include "glibc_exp.cuh"
+
+namespace bimine {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Device-side copy of the batch descriptor (all device pointers).
+struct BatchDev {
+  const int32_t *tokens;
+  const int64_t *sent_tok_off;
+  const int32_t *sent_len;
+  const int32_t *sent_uniq;
+  const int32_t *sent_chars;
+  const int64_t *pair_src;
+  const int32_t *pair_n;
+  const int64_t *pair_tgt;
+  const int32_t *pair_m;
+  const int64_t *pair_sim_off;
+  int64_t n_pairs;
+};
+
+struct DictDev {
+  int64_t n_rows;
+  const int64_t *row_ptr;
+  const int32_t *tgt;
+  const double *prob;
+};
+
+struct Model {
+  double w[6];
+  double bias, a, b;
+  double mean[6];
+  double scale[6];
+};
+
+inline BatchDev to_dev(const bimine_batch &b) {
+  return BatchDev{b.tokens, b.sent_tok_off, b.sent_len, b.sent_uniq, b.sent_chars,
+                  b.pair_src, b.pair_n, b.pair_tgt, b.pair_m, b.pair_sim_off, b.n_pairs};
+}
+
+inline Model to_model(const double *v) {
+  Model m;
+  for (int k = 0; k < 6; ++k) m.w[k] = v[k];
+  m.bias = v[6];
+  m.a = v[7];
+  m.b = v[8];
+  for (int k = 0; k < 6; ++k) m.mean[k] = v[9 + k];
+  for (int k = 0; k < 6; ++k) m.scale[k] = v[15 + k];
+  return m;
+}
+
+// Multiplicative (Fibonacci) hashing: the top `bits` bits of key * phi.
+__device__ __forceinline__ uint32_t hash_slot(int32_t key, int shift) {
+  return ((uint32_t)key * 0x9E3779B1u) >> shift;
+}
+
+// The exp table as a device global (the score kernel stages it in smem).
+__device__ const uint64_t kExpTableDev[256] = {
+#include "exp_table.inc"
+};
+
+}  // namespace bimine

@@ -1,0 +1,268 @@
+// nw_kernel.cuh -- Needleman-Wunsch fill + traceback + threshold filter.
+//
+// Reference: nw_align / nw_align_wavefront (align.py:170-200) fill the
+// table of the *reversed* score matrix (align.py:166-167) with
+//   dp[a][b] = max(dp[a-1][b-1] + c, dp[a-1][b] - gap, dp[a][b-1] - gap)
+//   c = mismatch + R[a-1][b-1] * (bonus - mismatch)
+// where a strict `>` keeps the earlier candidate on ties
+// (_nwcore.pyx:28-34), then walk forward from (0, 0) preferring the
+// diagonal, then a source gap, then a target gap (align.py:132-163),
+// and finally keep Match steps whose similarity reaches the threshold
+// (align.py:323-332).
+//
+// Because the traceback's equality tests re-evaluate exactly the
+// candidates the fill compared, "first candidate equal to the max in
+// the order diag, up, left" is the candidate the fill kept; recording it
+// as a 2-bit direction during the fill reproduces the reference walk
+// without the float64 table (verified against the reference on the
+// instance families of tests/golden/nw_golden.npz).
+//
+// One warp aligns one problem.  Rows of the reversed table are processed
+// in bands of 32, lane l owning row a0 + 1 + l; at step s lane l computes
+// column b = s - l + 1, so the 32 lanes sweep one anti-diagonal per step:
+// "up" arrives from lane l-1 by a warp shuffle, "diagonal" is the value
+// that arrived one step earlier, "left" is the lane's own previous cell.
+// Row a0 (the band's upper boundary) comes from a per-warp row buffer
+// that the previous band's lane 31 filled.  Directions (2 bits per cell,
+// 16 cells per word) live in shared memory for problems that fit and in
+// a per-warp global scratch slot otherwise; the walk runs on lane 0.
+#pragma once
+
+#include "common.cuh"
+
+namespace bimine {
+
+enum NwMode { kNwMine = 0, kNwSteps = 1, kNwTable = 2 };
+
+struct NwArgs {
+  const double *sim;           // all pairs, row-major per pair at sim_off
+  const int64_t *sim_off;      // [pairs]
+  const int32_t *pair_n;       // [pairs]
+  const int32_t *pair_m;       // [pairs]
+  const int64_t *problem_ids;  // [n_problems] or null (identity)
+  int64_t n_problems;
+  int32_t n_settings;          // problem q -> pair q / n_settings, setting q % n_settings
+  const double *gap;           // [n_settings]
+  const double *threshold;     // [n_settings] (mine mode)
+  double mismatch, bonus;
+  // mine mode
+  const int64_t *out_off;      // [problems] slot offsets
+  bimine_match *matches;
+  int32_t *counts;
+  double *score;               // [problems] or null
+  // steps mode
+  const int64_t *step_off;
+  uint8_t *steps;
+  int32_t *n_steps;
+  // table mode (single problem, reversed sim, caller boundaries)
+  double *table;
+  // scratch
+  int dir_words_per_warp;      // capacity (u32 words) of each warp's direction area
+  int row_doubles_per_warp;    // capacity of each warp's row buffer
+  uint32_t *g_dirs;            // global scratch (null -> shared memory)
+  double *g_rows;
+};
+
+template <int MODE>
+__device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *rowbuf) {
+  const int lane = threadIdx.x & 31;
+  const int64_t pair = q / A.n_settings;
+  const int setting = (int)(q % A.n_settings);
+  const int N = A.pair_n[pair], M = A.pair_m[pair];
+  const double *__restrict__ sim = A.sim + A.sim_off[pair];
+  const double gap = A.gap[setting];
+  const double ng = -gap;
+  const double mismatch = A.mismatch;
+  const double span = fsub(A.bonus, A.mismatch);
+  const int stride = (M >> 4) + 1;  // direction words per row (cells b = 0..M)
+  double *table = A.table;
+  const int64_t tw = (int64_t)M + 1;
+
+  // row 0 of the reversed table (kernels.py:46, or the caller's in table mode)
+  for (int b = lane; b <= M; b += 32) rowbuf[b] = (MODE == kNwTable) ? table[b] : fmul(ng, (double)b);
+  __syncwarp();
+  double last = 0.0;  // dp[N][M], on the lane that owns row N
+  for (int a0 = 0; a0 < N; a0 += 32) {
+    const int a = a0 + 1 + lane;
+    const bool active = a <= N;
+    // dp[a][0] (kernels.py:47) and dp[a-1][0]
+    const double left0 = (MODE == kNwTable) ? (active ? table[(int64_t)a * tw] : 0.0) : fmul(ng, (double)a);
+    double cur = left0;
+    double diag = 0.0;
+    if (lane == 0) diag = rowbuf[0];
+    {
+      const double prev_row0 = __shfl_up_sync(kFull, left0, 1);
+      if (lane > 0) diag = prev_row0;
+    }
+    // this lane's row of R: the reversed matrix row a-1 is sim row N - a
+    // walked backwards (table mode receives the reversed matrix itself,
+    // as kernels.fill_sequential passes it, kernels.py:55-57)
+    const double *srow = (MODE == kNwTable) ? sim + (int64_t)(a - 1) * M : sim + (int64_t)(N - a) * M + (M - 1);
+    const int64_t sdir = (MODE == kNwTable) ? 1 : -1;
+    uint32_t bits = 0u;
+    const int nsteps = M + 31;
+    for (int s = 0; s < nsteps; ++s) {
+      const int b = s - lane + 1;
+      double up = __shfl_up_sync(kFull, cur, 1);
+      if (lane == 0) {
+        up = (b >= 1 && b <= M) ? rowbuf[b] : 0.0;
+        if (b >= 1 && b <= M) diag = rowbuf[b - 1];
+      }
+      if (active && b >= 1 && b <= M) {
+        const double r = srow[sdir * (b - 1)];
+        const double c = fadd(mismatch, fmul(r, span));
+        double best = fadd(diag, c);
+        uint32_t dir = 0u;
+        double cand = fsub(up, gap);
+        if (cand > best) {
+          best = cand;
+          dir = 1u;
+        }
+        cand = fsub(cur, gap);
+        if (cand > best) {
+          best = cand;
+          dir = 2u;
+        }
+        cur = best;
+        if (MODE == kNwTable) {
+          table[(int64_t)a * tw + b] = best;
+        } else {
+          bits |= dir << (2 * (b & 15));
+          if ((b & 15) == 15 || b == M) {
+            dirs[(int64_t)a * stride + (b >> 4)] = bits;
+            bits = 0u;
+          }
+        }
+        if (lane == 31) rowbuf[b] = best;
+        if (a == N && b == M) last = best;
+      }
+      if (lane > 0) diag = up;  // dp[a-1][b] becomes next step's diagonal
+    }
+    // the next band's lane 0 needs dp[a0+32][0] as its first diagonal
+    __syncwarp();
+    if (lane == 31) rowbuf[0] = left0;
+    __syncwarp();
+  }
+  // dp[N][M] lives on lane (N - 1) % 32
+  last = __shfl_sync(kFull, last, (N - 1) & 31);
+  if (MODE == kNwTable) return;
+  if (lane == 0) {
+    int a = N, b = M;
+    int64_t cnt = 0;
+    if (MODE == kNwMine) {
+      const double thr = A.threshold[setting];
+      bimine_match *out = A.matches + A.out_off[q];
+      while (a > 0 && b > 0) {
+        const uint32_t d = (dirs[(int64_t)a * stride + (b >> 4)] >> (2 * (b & 15))) & 3u;
+        if (d == 0u) {
+          const int i = N - a, j = M - b;
+          const double v = sim[(int64_t)i * M + j];
+          if (v >= thr) {
+            out[cnt].score = v;
+            out[cnt].i = i;
+            out[cnt].j = j;
+            ++cnt;
+          }
+          --a;
+          --b;
+        } else if (d == 1u) {
+          --a;
+        } else {
+          --b;
+        }
+      }
+      A.counts[q] = (int32_t)cnt;
+    } else {
+      uint8_t *st = A.steps + A.step_off[q];
+      while (a > 0 && b > 0) {
+        const uint32_t d = (dirs[(int64_t)a * stride + (b >> 4)] >> (2 * (b & 15))) & 3u;
+        st[cnt++] = (uint8_t)d;
+        if (d == 0u) {
+          --a;
+          --b;
+        } else if (d == 1u) {
+          --a;
+        } else {
+          --b;
+        }
+      }
+      while (a > 0) {
+        st[cnt++] = 1u;
+        --a;
+      }
+      while (b > 0) {
+        st[cnt++] = 2u;
+        --b;
+      }
+      A.n_steps[q] = (int32_t)cnt;
+    }
+    if (A.score) A.score[q] = last;
+  }
+  __syncwarp();
+}
+
+// Warps loop over problems; each warp owns one direction area and one
+// row buffer, in dynamic shared memory (g_dirs == null) or in a global
+// scratch slot.
+template <int MODE>
+__global__ void __launch_bounds__(128) nw_kernel(const NwArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5;
+  const int warps_per_block = blockDim.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * warps_per_block + warp;
+  const int64_t total_warps = (int64_t)gridDim.x * warps_per_block;
+  uint32_t *dirs;
+  double *rowbuf;
+  if (A.g_dirs) {
+    dirs = A.g_dirs + gw * A.dir_words_per_warp;
+    rowbuf = A.g_rows + gw * A.row_doubles_per_warp;
+  } else {
+    double *rows = (double *)smem_raw;
+    uint32_t *dr = (uint32_t *)(rows + (size_t)warps_per_block * A.row_doubles_per_warp);
+    rowbuf = rows + (size_t)warp * A.row_doubles_per_warp;
+    dirs = dr + (size_t)warp * A.dir_words_per_warp;
+  }
+  for (int64_t k = gw; k < A.n_problems; k += total_warps) {
+    const int64_t q = A.problem_ids ? A.problem_ids[k] : k;
+    nw_problem<MODE>(A, q, dirs, rowbuf);
+  }
+}
+
+// ---- order-preserving compaction of per-problem match slots ----------
+
+// Single CTA exclusive scan of counts -> base (int64) and total.
+__global__ void __launch_bounds__(1024) scan_counts_kernel(const int32_t *counts, int64_t n, int64_t *base,
+                                                           int64_t *total) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t lo = min(n, t * per), hi = min(n, lo + per);
+  int64_t s = 0;
+  for (int64_t k = lo; k < hi; ++k) s += counts[k];
+  part[t] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int64_t v = t >= o ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int64_t run = part[t] - s;
+  for (int64_t k = lo; k < hi; ++k) {
+    base[k] = run;
+    run += counts[k];
+  }
+  if (t == 1023) *total = part[1023];
+}
+
+__global__ void gather_matches_kernel(const bimine_match *slots, const int64_t *out_off, const int32_t *counts,
+                                      const int64_t *base, int64_t n, bimine_match *compact) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const bimine_match *src = slots + out_off[w];
+  bimine_match *dst = compact + base[w];
+  for (int k = lane; k < counts[w]; k += 32) dst[k] = src[k];
+}
+
+}  // namespace bimine

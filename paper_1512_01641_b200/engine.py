@@ -1,0 +1,253 @@
+"""Device execution of the hot path through the C ABI.
+
+Holds the per-lexicon GPU dictionary (joint vocabulary + CSR uploaded
+once per device) and the batched calls the public API in ``align`` and
+``tuning`` is built on.  PyTorch provides device memory and streams;
+all compute is in libbimine_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .packing import PackedBatch, Vocabulary, lexicon_arrays
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class DeviceDictionary:
+    """A lexicon's joint vocabulary plus its CSR on one CUDA device."""
+
+    def __init__(self, vocab: Vocabulary, src: np.ndarray, tgt: np.ndarray, prob: np.ndarray, device: int):
+        self.vocab = vocab
+        self.device = device
+        L = N.load()
+        torch = _torch()
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            N.check(L.bimine_dict_create(N.ptr(src, N._i32p), N.ptr(tgt, N._i32p), N.ptr(prob, N._f64p),
+                                         int(src.shape[0]), ctypes.byref(handle)))
+        self.handle = handle
+        self.n_entries = int(L.bimine_dict_entries(handle))
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and N._lib is not None:
+            try:
+                N._lib.bimine_dict_destroy(h)
+            except Exception:
+                pass
+
+
+@dataclass
+class LexiconContext:
+    vocab: Vocabulary
+    coo: tuple  # (src, tgt, prob) ids in lexicon iteration order
+    devices: dict  # device index -> DeviceDictionary
+
+    def on(self, device: int) -> DeviceDictionary:
+        d = self.devices.get(device)
+        if d is None:
+            d = DeviceDictionary(self.vocab, *self.coo, device=device)
+            self.devices[device] = d
+        return d
+
+
+_contexts: dict[int, tuple] = {}
+_ctx_lock = threading.Lock()
+
+
+def lexicon_context(lexicon) -> LexiconContext:
+    """Cached (vocab, COO) for a lexicon object (ours or the reference's)."""
+    key = id(lexicon)
+    with _ctx_lock:
+        hit = _contexts.get(key)
+        if hit is not None and hit[0]() is lexicon:
+            return hit[1]
+        vocab = Vocabulary()
+        coo = lexicon_arrays(lexicon.items(), vocab)
+        ctx = LexiconContext(vocab=vocab, coo=coo, devices={})
+        try:
+            ref = weakref.ref(lexicon)
+        except TypeError:  # objects without weakref support: keep them alive
+            ref = (lambda obj: (lambda: obj))(lexicon)
+        _contexts[key] = (ref, ctx)
+        return ctx
+
+
+def current_device() -> int:
+    return _torch().cuda.current_device()
+
+
+# ---------------------------------------------------------------------------
+# device-resident batches
+# ---------------------------------------------------------------------------
+
+_FIELDS = ("tokens", "sent_tok_off", "sent_len", "sent_uniq", "sent_chars",
+           "pair_src", "pair_n", "pair_tgt", "pair_m", "pair_sim_off")
+
+
+class DeviceBatch:
+    """A PackedBatch copied to one device (torch tensors) + its ABI struct."""
+
+    def __init__(self, batch: PackedBatch, device: int, stream=None, pinned: bool = False):
+        torch = _torch()
+        self.batch = batch
+        self.device = device
+        self.t = {}
+        for f in _FIELDS:
+            a = torch.from_numpy(np.ascontiguousarray(getattr(batch, f)))
+            if pinned:
+                a = a.pin_memory()
+            self.t[f] = a.to(f"cuda:{device}", non_blocking=pinned)
+        self.struct = N.batch_struct_device(self.t, batch.n_pairs, batch.n_sentences, batch.n_tokens)
+        self.max_n = int(batch.pair_n.max(initial=0))
+        self.max_m = int(batch.pair_m.max(initial=0))
+        self.max_uniq = int(batch.sent_uniq.max(initial=0))
+        self.max_len = int(batch.sent_len.max(initial=0))
+        cap = batch.match_capacity()
+        self.capacity = int(cap[-1])
+        self.t["out_off"] = torch.from_numpy(cap[:-1].copy()).to(f"cuda:{device}")
+
+
+def stream_ptr(stream=None) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def score_device(dd: DeviceDictionary, model_vec: np.ndarray, db: DeviceBatch, sim, stream=None) -> None:
+    """build_score_matrix for every pair of a device batch into `sim` (torch f64)."""
+    L = N.load()
+    mv = np.ascontiguousarray(model_vec, dtype=np.float64)
+    N.check(L.bimine_score_batch(dd.handle, N.ptr(mv, N._f64p), ctypes.byref(db.struct), db.max_n, db.max_m,
+                                 db.max_uniq, db.max_len, sim.data_ptr(), stream_ptr(stream)))
+
+
+def mine_device(db: DeviceBatch, sim, gap: float, threshold: float, mismatch: float, bonus: float,
+                out: dict | None = None, stream=None) -> dict:
+    """NW + traceback + filter + compaction on device; returns device tensors
+    (counts, base, compact, total)."""
+    torch = _torch()
+    L = N.load()
+    dev = f"cuda:{db.device}"
+    P = db.batch.n_pairs
+    if out is None:
+        out = {
+            "par": torch.tensor([gap, threshold], dtype=torch.float64, device=dev),
+            "slots": torch.empty(max(db.capacity, 1) * 16, dtype=torch.uint8, device=dev),
+            "counts": torch.empty(max(P, 1), dtype=torch.int32, device=dev),
+            "base": torch.empty(max(P, 1), dtype=torch.int64, device=dev),
+            "compact": torch.empty(max(db.capacity, 1) * 16, dtype=torch.uint8, device=dev),
+            "total": torch.zeros(1, dtype=torch.int64, device=dev),
+        }
+    par = out["par"]
+    sp = stream_ptr(stream)
+    N.check(L.bimine_nw_mine_batch(sim.data_ptr(), db.t["pair_sim_off"].data_ptr(), db.t["pair_n"].data_ptr(),
+                                   db.t["pair_m"].data_ptr(), P, db.max_n, db.max_m, 1, par.data_ptr(),
+                                   par.data_ptr() + 8, mismatch, bonus, db.t["out_off"].data_ptr(),
+                                   out["slots"].data_ptr(), out["counts"].data_ptr(), None, sp))
+    N.check(L.bimine_compact_matches(out["slots"].data_ptr(), db.t["out_off"].data_ptr(), out["counts"].data_ptr(),
+                                     P, out["base"].data_ptr(), out["compact"].data_ptr(), out["total"].data_ptr(),
+                                     sp))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# host-buffer entry points
+# ---------------------------------------------------------------------------
+
+def mine_host(dd: DeviceDictionary, model_vec: np.ndarray, batch: PackedBatch, gap: float, threshold: float,
+              mismatch: float, bonus: float, want_sim: bool = False, stream=None):
+    """bimine_mine_host: H2D, score, NW, filter, compact, D2H.  Returns
+    (counts[P], matches structured array, sim or None)."""
+    L = N.load()
+    torch = _torch()
+    P = batch.n_pairs
+    counts = np.zeros(max(P, 1), dtype=np.int32)
+    cap = int(batch.match_capacity()[-1])
+    matches = np.zeros(max(cap, 1), dtype=N.MATCH_DTYPE)
+    total = np.zeros(1, dtype=np.int64)
+    sim = np.empty(max(batch.n_cells, 1), dtype=np.float64) if want_sim else None
+    cb = N.batch_struct_host(batch)
+    mv = np.ascontiguousarray(model_vec, dtype=np.float64)
+    with torch.cuda.device(dd.device):
+        N.check(L.bimine_mine_host(dd.handle, N.ptr(mv, N._f64p), ctypes.byref(cb), gap, threshold, mismatch, bonus,
+                                   N.ptr(counts, N._i32p), matches.ctypes.data, max(cap, 1), N.ptr(total, N._i64p),
+                                   sim.ctypes.data if sim is not None else None, stream_ptr(stream)))
+    return counts[:P], matches[: int(total[0])], (sim[: batch.n_cells] if sim is not None else None)
+
+
+def score_host(dd: DeviceDictionary, model_vec: np.ndarray, batch: PackedBatch) -> np.ndarray:
+    """Score matrices of a host batch (flat, at pair_sim_off)."""
+    torch = _torch()
+    with torch.cuda.device(dd.device):
+        db = DeviceBatch(batch, dd.device)
+        sim = torch.empty(max(batch.n_cells, 1), dtype=torch.float64, device=f"cuda:{dd.device}")
+        score_device(dd, model_vec, db, sim)
+        return sim[: batch.n_cells].cpu().numpy()
+
+
+def nw_steps_host(sims: list[np.ndarray], gaps: list[float], mismatch: float, bonus: float, device: int | None = None):
+    """Full step lists for a list of matrices: [(codes uint8[k], score)]."""
+    torch = _torch()
+    L = N.load()
+    if device is None:
+        device = current_device()
+    dev = f"cuda:{device}"
+    n = np.array([s.shape[0] for s in sims], dtype=np.int32)
+    m = np.array([s.shape[1] for s in sims], dtype=np.int32)
+    cells = n.astype(np.int64) * m
+    sim_off = np.zeros(len(sims), dtype=np.int64)
+    np.cumsum(cells[:-1], out=sim_off[1:])
+    step_off = np.zeros(len(sims), dtype=np.int64)
+    np.cumsum((n + m)[:-1].astype(np.int64), out=step_off[1:])
+    flat = np.concatenate([np.ascontiguousarray(s, dtype=np.float64).ravel() for s in sims])
+    with torch.cuda.device(device):
+        t_sim = torch.from_numpy(flat).to(dev)
+        t_off = torch.from_numpy(sim_off).to(dev)
+        t_n = torch.from_numpy(n).to(dev)
+        t_m = torch.from_numpy(m).to(dev)
+        t_gap = torch.tensor(np.asarray(gaps, dtype=np.float64)).to(dev)
+        t_soff = torch.from_numpy(step_off).to(dev)
+        t_steps = torch.empty(int((n + m).sum()), dtype=torch.uint8, device=dev)
+        t_nsteps = torch.empty(len(sims), dtype=torch.int32, device=dev)
+        t_score = torch.empty(len(sims), dtype=torch.float64, device=dev)
+        N.check(L.bimine_nw_steps_batch(t_sim.data_ptr(), t_off.data_ptr(), t_n.data_ptr(), t_m.data_ptr(),
+                                        len(sims), int(n.max()), int(m.max()), t_gap.data_ptr(), mismatch, bonus,
+                                        t_soff.data_ptr(), t_steps.data_ptr(), t_nsteps.data_ptr(),
+                                        t_score.data_ptr(), stream_ptr()))
+        steps = t_steps.cpu().numpy()
+        nsteps = t_nsteps.cpu().numpy()
+        scores = t_score.cpu().numpy()
+    return [(steps[step_off[k] : step_off[k] + nsteps[k]], float(scores[k])) for k in range(len(sims))]
+
+
+def nw_fill_host(dp: np.ndarray, sim: np.ndarray, mismatch: float, bonus: float, gap: float) -> None:
+    """The reference FFI contract (_nwcore.nw_fill): dp initialised by the caller."""
+    L = N.load()
+    if dp.dtype != np.float64 or not dp.flags.c_contiguous or not dp.flags.writeable:
+        raise ValueError("dp must be a writable C-contiguous float64 array")
+    sim = np.ascontiguousarray(sim, dtype=np.float64)
+    n, m = sim.shape
+    if dp.shape != (n + 1, m + 1):
+        raise ValueError("dp must have shape (n + 1, m + 1)")
+    N.check(L.bimine_nw_fill(N.ptr(dp, N._f64p), N.ptr(sim, N._f64p), n, m, mismatch, bonus, gap, None))
+
+
+def exp_device(x: np.ndarray) -> np.ndarray:
+    L = N.load()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    N.check(L.bimine_exp_device(N.ptr(x, N._f64p), N.ptr(y, N._f64p), x.size))
+    return y

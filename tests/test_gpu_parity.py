@@ -1,0 +1,306 @@
+"""GPU parity: the CUDA path against the reference's fixtures and the oracle.
+
+Bit-exact everywhere: score matrices (binary64 bit patterns), alignment
+step lists, Alignment.score, mined (score, i, j) triples.  The north-star
+tolerance for scores is 1e-6 relative; the kernels meet it with zero
+error, and the tests hold them to that.
+"""
+
+import numpy as np
+import pytest
+
+import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU containers
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+from paper_1512_01641_b200 import align as A  # noqa: E402
+from paper_1512_01641_b200 import engine as E  # noqa: E402
+from paper_1512_01641_b200 import synth  # noqa: E402
+from paper_1512_01641_b200.classifier import model_vector  # noqa: E402
+from paper_1512_01641_b200.corpus import Document, DocumentPair  # noqa: E402
+from paper_1512_01641_b200.lexicon import Lexicon  # noqa: E402
+
+SCORE_RTOL = 1e-6  # BASELINE.json north_star tolerance for scores
+
+
+def bits_equal(a, b):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _oracle():
+    oracle.build()
+
+
+def test_native_library_is_loaded():
+    from paper_1512_01641_b200 import _native
+
+    L = _native.load()
+    assert b"sm_100a" in L.bimine_version()
+
+
+# ---------------------------------------------------------------- exp
+
+def test_device_exp_matches_reference_math_exp():
+    z = H.load_npz("exp_golden.npz")
+    assert bits_equal(E.exp_device(z["x"]), z["y"])
+
+
+def test_device_exp_matches_host_libm_randomised():
+    rng = np.random.default_rng(7)
+    x = np.concatenate([-rng.uniform(0, 700, 4_000_000), rng.uniform(-745, 710, 2_000_000),
+                        rng.uniform(-1, 1, 1_000_000), -rng.uniform(511.5, 512.5, 500_000)])
+    assert bits_equal(E.exp_device(x), oracle.exp_array(x))
+
+
+# ---------------------------------------------------------------- NW
+
+@pytest.mark.parametrize("family", H.NW_FAMILIES)
+def test_nw_reference_families(family):
+    sims = list(H.nw_family_sims(family))
+    fx = H.nw_family(family)
+    gaps = [float(g) for _, _, _, g in fx]
+    out = E.nw_steps_host(sims, gaps, H.NW_MISMATCH, H.NW_BONUS)
+    for (codes, score), (want, want_score, shape, _) in zip(out, fx):
+        assert np.array_equal(codes, want)
+        assert score == want_score
+
+
+def test_nw_align_api_and_demo_fixtures():
+    # demos.py:18-29 / test_align.py:221-251
+    def exact(src, tgt):
+        return np.array([[1.0 if s == t else 0.0 for t in tgt] for s in src])
+
+    demo = A.MiningConfig(threshold=0.5, gap_penalty=5.0, match_bonus=9.0, mismatch_cost=-4.0)
+    src, tgt = ("a", "d", "c", "d", "e"), ("a", "d", "e", "g", "f")
+    al = A.nw_align(exact(src, tgt), demo)
+    sl, tl = [], []
+    for s in al.steps:
+        if isinstance(s, A.Match):
+            sl.append(src[s.i]); tl.append(tgt[s.j])
+        elif isinstance(s, A.GapSource):
+            sl.append(src[s.i]); tl.append("-")
+        else:
+            sl.append("-"); tl.append(tgt[s.j])
+    assert ", ".join(tl) == "a, d, -, -, e, g, f"
+    assert ", ".join(sl) == "a, d, c, d, e, -, -"
+    ws, wt = ("tablets", "make", "people", "spoil", "children"), ("tablets", "make", "children", "very", "addicted")
+    al = A.nw_align(exact(ws, wt), demo)
+    assert {(ws[s.i], wt[s.j]) for s in al.steps if isinstance(s, A.Match)} == {
+        ("tablets", "tablets"), ("make", "make"), ("children", "children")}
+    eye = A.nw_align(np.eye(5), A.MiningConfig(gap_penalty=1.0))
+    assert eye.steps == tuple(A.Match(i, i) for i in range(5)) and eye.score == 5.0
+    assert A.nw_align_wavefront(np.eye(5), A.MiningConfig(gap_penalty=1.0), 4) == eye
+    with pytest.raises(ValueError):
+        A.nw_align(np.zeros((0, 3)), A.MiningConfig())
+    with pytest.raises(ValueError):
+        A.nw_align(np.array([[0.5, 1.5]]), A.MiningConfig())
+    with pytest.raises(ValueError):
+        A.nw_align(np.array([[np.nan]]), A.MiningConfig())
+    with pytest.raises(ValueError):
+        A.nw_align_wavefront(np.eye(2), A.MiningConfig(), 0)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 70), (70, 1), (31, 33), (32, 32), (33, 31), (64, 65), (200, 220), (513, 300)])
+def test_nw_steps_match_oracle_random(shape):
+    rng = np.random.default_rng(sum(shape))
+    sims = [rng.random(shape) for _ in range(3)] + [rng.integers(0, 2, size=shape).astype(np.float64)]
+    gaps = [0.0, 0.7, 2.0, 0.5]
+    out = E.nw_steps_host(sims, gaps, -1.0, 1.0)
+    for sim, g, (codes, score) in zip(sims, gaps, out):
+        want, _, _, want_score = oracle.nw_align(sim, -1.0, 1.0, g)
+        assert np.array_equal(codes, want)
+        assert bits_equal(score, want_score)
+
+
+def test_nw_fill_b1_contract_bit_identical():
+    """bimine_nw_fill honours the reference FFI: caller boundaries, interior
+    written in place, bit-identical to the reference fill (_nwcore.pyx:19-36)."""
+    rng = np.random.default_rng(11)
+    for shape in [(1, 1), (5, 4), (40, 33), (97, 130), (300, 64)]:
+        sim = rng.random(shape)
+        gap = float(rng.uniform(0, 3))
+        want = oracle.nw_table(sim, -1.0, 1.0, gap)
+        dp = np.empty_like(want)
+        dp[0, :] = -gap * np.arange(shape[1] + 1, dtype=np.float64)
+        dp[1:, 0] = -gap * np.arange(1, shape[0] + 1, dtype=np.float64)
+        E.nw_fill_host(dp, sim, -1.0, 1.0, gap)
+        assert bits_equal(dp, want)
+        # arbitrary caller boundaries are used as given
+        dp2 = np.zeros_like(want)
+        dp2[0, :] = rng.normal(size=shape[1] + 1)
+        dp2[1:, 0] = rng.normal(size=shape[0])
+        ref = dp2.copy()
+        oracle.lib().oracle_nw_fill(ref.ctypes.data_as(oracle._f64p), sim.ctypes.data_as(oracle._f64p),
+                                    shape[0], shape[1], -1.0, 1.0, gap)
+        E.nw_fill_host(dp2, sim, -1.0, 1.0, gap)
+        assert bits_equal(dp2, ref)
+
+
+# ---------------------------------------------------------------- score matrix
+
+def test_toy_score_matrices_bit_exact():
+    model, lex = H.toy_model(), H.toy_lexicon()
+    for (src, tgt), ref in zip(H.toy_pairs(), H.toy_sims()):
+        got = A.build_score_matrix(model, lex, src, tgt)
+        assert bits_equal(got, ref)
+        np.testing.assert_allclose(got, ref, rtol=SCORE_RTOL, atol=0)
+
+
+def test_score_matrix_errors_match_reference():
+    model, lex = H.toy_model(), H.toy_lexicon()
+    with pytest.raises(ValueError) as exc:
+        A.build_score_matrix(model, lex, ["domo"], ["house", "..."])
+    assert str(exc.value) == H.load_json("toy.json")["error_untokenizable"]
+    with pytest.raises(ValueError):
+        A.build_score_matrix(model, lex, [], ["house"])
+
+
+@pytest.mark.parametrize("cfg", ["default", "strict", "loose"])
+def test_toy_mining_rows_bit_exact(cfg):
+    params = {
+        "default": A.MiningConfig(),
+        "strict": A.MiningConfig(threshold=0.8, gap_penalty=0.5),
+        "loose": A.MiningConfig(threshold=0.0, gap_penalty=3.0, match_bonus=2.0, mismatch_cost=-0.5),
+    }[cfg]
+    model, lex = H.toy_model(), H.toy_lexicon()
+    fx = H.load_json("toy.json")["pairs"]
+    pairs = []
+    for p in fx:
+        pair = DocumentPair(
+            topic_id=p["topic_id"],
+            source=Document(id="s", lang="eo", title="t", sentences=tuple(p["source"])),
+            target=Document(id="t", lang="en", title="t", sentences=tuple(p["target"])),
+        )
+        pairs.append(pair)
+        rows = A.mine_document_pair(model, lex, pair, params, engine="nw")
+        want = [(float.fromhex(s), a, b) for s, a, b in p[cfg]["rows"]]
+        assert rows == want, p["topic_id"]
+    outcome = A.mine_corpus(model, lex, pairs, params)
+    assert outcome.failures == ()
+    assert list(outcome.rows) == [(float.fromhex(s), a, b) for p in fx for s, a, b in p[cfg]["rows"]]
+
+
+def test_mine_corpus_failures_and_order():
+    model, lex = H.toy_model(), H.toy_lexicon()
+    fx = H.load_json("toy.json")
+    p0 = fx["pairs"][0]
+    good = DocumentPair("alpha", Document("a", "eo", "t", tuple(p0["source"])), Document("b", "en", "t", tuple(p0["target"])))
+    bad = DocumentPair("bad", Document("b1", "eo", "bad", ("...",)), Document("b2", "en", "bad", ("house",)))
+    out = A.mine_corpus(model, lex, [good, bad], A.MiningConfig(), engine="nw")
+    assert [list(f) for f in out.failures] == fx["mine_corpus_failures"]
+    assert len(out.rows) > 0
+    assert A.mine_corpus(model, lex, [], A.MiningConfig(workers=4)) == A.MiningOutcome((), ())
+    with pytest.raises(ValueError, match="unknown engine"):
+        A.mine_corpus(model, lex, [], A.MiningConfig(), engine="bogus")
+    wide = A.mine_corpus(model, lex, [good, bad, good], A.MiningConfig(workers=16))
+    narrow = A.mine_corpus(model, lex, [good, bad, good], A.MiningConfig(workers=1))
+    assert wide == narrow
+
+
+def _synth_check(corpus, pairs=None, threads=0):
+    model = model_vector(H.synth_model())
+    d = corpus.dictionary
+    od = oracle.OracleDict(d.src, d.tgt, d.prob)
+    batch = corpus.batch if pairs is None else corpus.batch.select(pairs)
+    want_sim = oracle.score_batch(od, model, batch, threads)
+    want_counts, want_rows = oracle.mine_batch(od, model, batch, threads=threads)
+    ctx = E.LexiconContext(vocab=None, coo=(d.src, d.tgt, d.prob), devices={})
+    dd = ctx.on(E.current_device())
+    counts, matches, sim = E.mine_host(dd, model, batch, 2.0, 0.5, -1.0, 1.0, want_sim=True)
+    assert bits_equal(sim, want_sim)
+    assert np.array_equal(counts, want_counts)
+    flat = np.concatenate(want_rows) if want_rows else np.zeros(0, dtype=matches.dtype)
+    assert np.array_equal(matches.view(np.uint8), flat.view(np.uint8))
+    return batch
+
+
+def test_synthetic_fixtures_bit_exact():
+    model = model_vector(H.synth_model())
+    for name, corpus in [("synth_c1", synth.make_config(1)), ("synth_c2", synth.make_config(2, n_pairs=12))]:
+        fx = H.load_json(f"{name}.json")
+        sims = H.load_npz(f"{name}_sims.npz")
+        d = corpus.dictionary
+        ctx = E.LexiconContext(vocab=None, coo=(d.src, d.tgt, d.prob), devices={})
+        dd = ctx.on(E.current_device())
+        sub = corpus.batch.select(fx["pairs"])
+        counts, matches, sim = E.mine_host(dd, model, sub, 2.0, 0.5, -1.0, 1.0, want_sim=True)
+        pos = 0
+        for k, p in enumerate(fx["pairs"]):
+            ref = sims[f"sim{p}"]
+            n, m = ref.shape
+            assert bits_equal(sim[sub.pair_sim_off[k] : sub.pair_sim_off[k] + n * m].reshape(n, m), ref)
+            want = [(float.fromhex(s), i, j) for s, i, j in fx["indices"][k]]
+            got = [(float(r["score"]), int(r["i"]), int(r["j"])) for r in matches[pos : pos + counts[k]]]
+            pos += counts[k]
+            assert got == want
+
+
+def test_synthetic_c2_batch_vs_oracle():
+    _synth_check(synth.make_config(2, n_pairs=400))
+
+
+def test_multi_tile_pairs_vs_oracle():
+    """N, M > 64 (several CTAs per pair) and a C1-shaped pair."""
+    corpus = synth.make_corpus(77, 6, 2_000, shape=(150, 131))
+    _synth_check(corpus)
+    _synth_check(synth.make_config(1))
+
+
+def test_large_pair_global_scratch_vs_oracle():
+    """A pair whose direction table does not fit shared memory."""
+    corpus = synth.make_corpus(78, 1, 5_000, shape=(700, 650))
+    _synth_check(corpus, threads=0)
+
+
+def test_chunked_targets_and_long_sentences():
+    """Sentences with many distinct tokens force several target chunks per
+    tile; long sentences (> 64 tokens) exercise multi-segment streaming;
+    repeated tokens exercise first-occurrence and multiplicity logic."""
+    rng = np.random.default_rng(5)
+    words = [f"w{k}" for k in range(3000)]
+    trans = {w: {f"v{(k * 7 + j) % 3000}": float(round(rng.uniform(0.01, 1.0), 6)) for j in range(rng.integers(1, 9))}
+             for k, w in enumerate(words[:2000])}
+    # one long row (> inline candidate capacity) and a zero / negative entry
+    trans["w1"] = {f"v{k}": 0.01 * (k + 1) for k in range(40)}
+    trans["w2"]["v5"] = 0.0
+    trans["w3"]["v6"] = -0.5
+    lex = Lexicon(trans)
+
+    def sent(n, side):
+        pick = rng.integers(0, 3000, size=n)
+        toks = [(words[i] if side == "s" else f"v{i}") for i in pick]
+        if n > 3:
+            toks[1] = toks[0]  # duplicates
+            toks.append("zz")  # shared token on both sides
+        return " ".join(toks) + "."
+
+    pairs = [([sent(int(rng.integers(1, 150)), "s") for _ in range(70)],
+              [sent(int(rng.integers(1, 150)), "t") for _ in range(90)]) for _ in range(2)]
+    vocab, coo, batch = H.pack_pairs(lex, pairs)
+    model = model_vector(H.toy_model())
+    od = oracle.OracleDict(*coo)
+    want = oracle.score_batch(od, model, batch)
+    ctx = E.LexiconContext(vocab=vocab, coo=coo, devices={})
+    got = E.score_host(ctx.on(E.current_device()), model, batch)
+    assert bits_equal(got, want)
+    for p, (src, tgt) in enumerate(pairs):
+        g = A.build_score_matrix(H.toy_model(), lex, src, tgt)
+        n, m = len(src), len(tgt)
+        assert bits_equal(g, want[batch.pair_sim_off[p] : batch.pair_sim_off[p] + n * m].reshape(n, m))
+
+
+def test_lexicon_duplicates_last_wins():
+    """bimine_dict_create: repeated (src, tgt) keeps the last value."""
+    src = np.array([0, 0, 0, 1], dtype=np.int32)
+    tgt = np.array([5, 5, 6, 5], dtype=np.int32)
+    prob = np.array([0.9, 0.2, 0.0, 0.4])
+    d = E.DeviceDictionary(None, src, tgt, prob, E.current_device())
+    assert d.n_entries == 2  # (0,5)=0.2, (1,5)=0.4; (0,6)=0 dropped
