@@ -1,0 +1,419 @@
+"""Benchmark of the B200 sentence-alignment hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--pairs P]
+    python bench.py --impl reference ...        # the CPU reference arm
+
+A *step* is one mining pass over one batch of synthetic document pairs
+(BASELINE.json configs[1], "C2": 10k pairs of ~50x50 sentences with a
+1M-entry dictionary): score kernel (build_score_matrix) -> NW wavefront
+fill + traceback + threshold filter -> order-preserving compaction, with
+the packed batch resident in HBM.  `value` is doc pairs/s over all ranks;
+NW GCUPS is reported beside it.  Under torchrun each rank mines its own
+batch (weak scaling, no collective on the data path; NCCL only carries
+the barrier and the max-over-ranks timing).
+
+The JSON line also carries `e2e` (the same metric through the C ABI's
+host-buffer call bimine_mine_host: pinned H2D of the packed batch, all
+kernels, D2H of counts + matches), `roofline` (score kernel vs measured
+HBM peak), `cpu_baseline` (the CPU oracle on a bounded sample, rank 0),
+`clocks` and `gpu_launches`.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "doc pairs/s (score + NW + traceback/filter), NW GCUPS beside"
+UNIT = "doc_pairs/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5])
+    ap.add_argument("--pairs", type=int, default=None, help="pairs per rank (default: the config's)")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def load_workload(config: int, pairs: int | None, rank: int):
+    from paper_1512_01641_b200 import synth
+    from paper_1512_01641_b200.classifier import load_model, model_vector
+
+    spec = synth.CONFIGS[config]
+    n_pairs = pairs if pairs is not None else min(spec["n_pairs"], 10_000)
+    rng_seed = 20261018
+    dict_rng = np.random.default_rng(rng_seed + config)
+    dictionary = synth.make_dictionary(dict_rng, spec["n_words"])
+    corpus = synth.make_corpus(rng_seed + 1000 + config + 7919 * rank, n_pairs, spec["n_words"], spec["shape"],
+                               dictionary=dictionary)
+    model = model_vector(load_model(os.path.join(REPO, "tests", "golden", "synth_model.json")))
+    return corpus, model
+
+
+def algorithmic_bytes(batch) -> int:
+    """Score kernel's compulsory HBM traffic: the sim write,
+    the token ids and the per-sentence / per-pair descriptors it reads.
+    The dictionary (replicated, L2 resident) is excluded."""
+    return int(8 * batch.n_cells + 4 * batch.n_tokens + 20 * batch.n_sentences + 48 * batch.n_pairs)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            with open(self.path) as fh:
+                for line in fh:
+                    f = [x.strip() for x in line.split(",")]
+                    if len(f) >= 9:
+                        rows.append(f)
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [num(r[1]) for r in rows if num(r[1]) is not None]
+        smax = [num(r[2]) for r in rows if num(r[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "reasons": reasons,
+            "samples": len(rows),
+        }
+
+
+def measured_peak_hbm():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            v = json.load(fh).get("hbm_gbs")
+        if v:
+            return float(v), "measured"
+    except (OSError, ValueError):
+        pass
+    return 6650.0, "fallback"
+
+
+def cpu_baseline(corpus, model, seconds: float):
+    """The CPU oracle (oracle/, a plain-C port of the reference path) on a
+    bounded sample of the same workload, all host threads."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+
+    oracle.build()
+    threads = oracle.max_threads()
+    d = corpus.dictionary
+    od = oracle.OracleDict(d.src, d.tgt, d.prob)
+    # calibrate on a small slice, then size the sample to ~`seconds`
+    probe = corpus.batch.select(range(min(64, corpus.batch.n_pairs)))
+    t0 = time.perf_counter()
+    oracle.mine_batch(od, model, probe, threads=threads)
+    rate = probe.n_pairs / max(time.perf_counter() - t0, 1e-6)
+    n = int(min(corpus.batch.n_pairs, max(probe.n_pairs, rate * seconds)))
+    sample = corpus.batch.select(range(n))
+    t0 = time.perf_counter()
+    oracle.mine_batch(od, model, sample, threads=threads)
+    dt = time.perf_counter() - t0
+    return {
+        "value": n / dt,
+        "unit": UNIT,
+        "cores": threads,
+        "kind": "port",
+        "sample": f"first {n} of the {corpus.batch.n_pairs} pairs ({sample.n_cells} cells), oracle/bimine_oracle.c "
+                  f"mine_batch with {threads} OpenMP threads, {dt:.1f}s",
+        "gcups": sample.n_cells / dt / 1e9,
+    }
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+
+    corpus, model = load_workload(args.config, args.pairs, 0)
+    oracle.build()
+    threads = oracle.max_threads()
+    d = corpus.dictionary
+    od = oracle.OracleDict(d.src, d.tgt, d.prob)
+    probe = corpus.batch.select(range(min(32, corpus.batch.n_pairs)))
+    t0 = time.perf_counter()
+    oracle.mine_batch(od, model, probe, threads=threads)
+    rate = probe.n_pairs / max(time.perf_counter() - t0, 1e-6)
+    per_step = max(1, int(min(corpus.batch.n_pairs, rate * 150.0 / (args.steps + args.warmup))))
+    sample = corpus.batch.select(range(per_step))
+    for _ in range(args.warmup):
+        oracle.mine_batch(od, model, sample, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.mine_batch(od, model, sample, threads=threads)
+    dt = time.perf_counter() - t0
+    value = per_step * args.steps / dt
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": 0,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (SURVEY.md 8(d) generator, seeded)",
+        "config": {"workload": f"C{args.config}: {corpus.batch.n_pairs} pairs", "sample_pairs_per_step": per_step},
+        "nw_gcups": sample.n_cells * args.steps / dt / 1e9,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{per_step} pairs per step ({sample.n_cells} cells), oracle/bimine_oracle.c, "
+                                   f"{threads} OpenMP threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = local
+
+    from paper_1512_01641_b200 import engine as E
+
+    corpus, model = load_workload(args.config, args.pairs, rank)
+    batch = corpus.batch
+    d = corpus.dictionary
+    ctx = E.LexiconContext(vocab=None, coo=(d.src, d.tgt, d.prob), devices={})
+    dd = ctx.on(dev)
+    stream = torch.cuda.current_stream()
+    db = E.DeviceBatch(batch, dev)
+    sim = torch.empty(max(batch.n_cells, 1), dtype=torch.float64, device=f"cuda:{dev}")
+    gap, thr, mism, bonus = 2.0, 0.5, -1.0, 1.0
+    out = None
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")  # > 126 MB L2
+
+    def step(ev=None):
+        nonlocal out
+        if ev:
+            ev[0].record(stream)
+        E.score_device(dd, model, db, sim, stream)
+        if ev:
+            ev[1].record(stream)
+        out = E.mine_device(db, sim, gap, thr, mism, bonus, out=out, stream=stream)
+        if ev:
+            ev[2].record(stream)
+
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    events = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clocks:
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the event window)
+            step(events[k])
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    score_ms = sum(e[0].elapsed_time(e[1]) for e in events)
+    nw_ms = sum(e[1].elapsed_time(e[2]) for e in events)
+    step_ms = score_ms + nw_ms
+    total_matches = int(out["total"].item())
+    t = torch.tensor([step_ms, score_ms, nw_ms], dtype=torch.float64, device=f"cuda:{dev}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms, score_ms, nw_ms = (float(x) for x in t.tolist())
+    K = args.steps
+    pairs_all = batch.n_pairs * world
+    cells_all = batch.n_cells * world
+    value = pairs_all * K / (step_ms / 1e3)
+
+    # ---- e2e through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        from paper_1512_01641_b200.packing import PackedBatch
+
+        pinned = {}
+        for f in ("tokens", "sent_tok_off", "sent_len", "sent_uniq", "sent_chars", "pair_src", "pair_n",
+                  "pair_tgt", "pair_m", "pair_sim_off"):
+            a = torch.from_numpy(np.ascontiguousarray(getattr(batch, f))).pin_memory()
+            pinned[f] = a.numpy()
+        pb = PackedBatch(**pinned)
+        e2e_steps = max(3, min(K, 10))
+        E.mine_host(dd, model, pb, gap, thr, mism, bonus, stream=stream)  # warm
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            counts, matches, _ = E.mine_host(dd, model, pb, gap, thr, mism, bonus, stream=stream)
+        e2e_s = time.perf_counter() - t0
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{dev}")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        e2e = {
+            "value": pairs_all * e2e_steps / e2e_s,
+            "unit": UNIT,
+            "h2d_bytes_per_step": int(pb.nbytes()),
+            "d2h_bytes_per_step": int(4 * batch.n_pairs + 8 + 16 * int(counts.sum())),
+            "steps": e2e_steps,
+            "path": "bimine_mine_host (C ABI), pinned host buffers",
+        }
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = measured_peak_hbm()
+    alg = algorithmic_bytes(batch)
+    score_launch_s = score_ms / K / 1e3
+    achieved = alg / score_launch_s / 1e9
+    roofline = {
+        "kernel": "score_kernel",
+        "bound": "hbm",
+        "achieved": achieved,
+        "peak": peak,
+        "unit": "GB/s",
+        "frac": achieved / peak,
+        "traffic": None,
+        "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, burst copy)",
+        "algorithmic_bytes_per_launch": alg,
+        "launch_ms": score_ms / K,
+    }
+    prof_traffic = os.path.join(REPO, "profiles", "score_kernel_traffic.json")
+    if os.path.exists(prof_traffic):
+        try:
+            with open(prof_traffic) as fh:
+                tr = json.load(fh)
+            if tr.get("workload") == f"C{args.config}:{batch.n_pairs}":
+                roofline["traffic"] = tr.get("dram_bytes_per_launch")
+                roofline["traffic_source"] = tr.get("source")
+        except (OSError, ValueError):
+            pass
+
+    cpu = None
+    if not args.no_cpu:
+        cpu = cpu_baseline(corpus, model, args.cpu_seconds)
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": K,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": step_ms / K,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (SURVEY.md 8(d) generator, seeded; model trained by the reference's train_classifier)",
+        "config": {
+            "workload": f"C{args.config}: {batch.n_pairs} doc pairs/rank, {batch.n_cells} cells, "
+                        f"{batch.n_tokens} tokens, {len(d.src)}-entry dictionary",
+            "pairs_per_rank": batch.n_pairs,
+            "cells_per_rank": batch.n_cells,
+            "mining": {"threshold": thr, "gap_penalty": gap, "match_bonus": bonus, "mismatch_cost": mism},
+            "l2": "flushed (512 MB write) between timed steps",
+            "parallelism": f"pair shards x{world}, no collective on the data path",
+        },
+        "nw_gcups": cells_all * K / (nw_ms / 1e3) / 1e9,
+        "pipeline_gcups": cells_all * K / (step_ms / 1e3) / 1e9,
+        "score_ms_per_step": score_ms / K,
+        "nw_ms_per_step": nw_ms / K,
+        "matches_per_step": total_matches * world,
+        "e2e": e2e,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+        "gpu_launches": 4 * K,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -311,6 +311,7 @@ int bimine_nw_steps_batch(const double *sim_dev, const int64_t *pair_sim_off, co
   if (max_n < 1 || max_m < 1) return fail(BIMINE_E_ARG, "bimine_nw_steps_batch: empty matrix");
   // one setting per pair: problem q == pair q, gap_dev[q]
   NwArgs A = nw_args_base(sim_dev, pair_sim_off, pair_n, pair_m, n_pairs, 1, gap_dev, mismatch, bonus);
+  A.gap_per_problem = 1;
   A.step_off = step_off_dev;
   A.steps = steps_dev;
   A.n_steps = n_steps_dev;

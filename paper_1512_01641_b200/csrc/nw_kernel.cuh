@@ -42,7 +42,8 @@ struct NwArgs {
   const int64_t *problem_ids;  // [n_problems] or null (identity)
   int64_t n_problems;
   int32_t n_settings;          // problem q -> pair q / n_settings, setting q % n_settings
-  const double *gap;           // [n_settings]
+  const double *gap;           // [n_settings], or [n_problems] if gap_per_problem
+  int gap_per_problem;
   const double *threshold;     // [n_settings] (mine mode)
   double mismatch, bonus;
   // mine mode
@@ -70,7 +71,7 @@ __device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *r
   const int setting = (int)(q % A.n_settings);
   const int N = A.pair_n[pair], M = A.pair_m[pair];
   const double *__restrict__ sim = A.sim + A.sim_off[pair];
-  const double gap = A.gap[setting];
+  const double gap = A.gap_per_problem ? A.gap[q] : A.gap[setting];
   const double ng = -gap;
   const double mismatch = A.mismatch;
   const double span = fsub(A.bonus, A.mismatch);
