@@ -124,16 +124,32 @@ int bimine_dict_destroy(bimine_dict *dict);
 int bimine_dict_view_get(const bimine_dict *dict, bimine_dict_view *view_dev);
 int64_t bimine_dict_entries(const bimine_dict *dict);
 
+/* ---- batch plan -------------------------------------------------------
+ * Host-side summary of a packed batch (host pointers in batch_host):
+ * maxima that size the kernels, and the pairs the per-pair score kernel
+ * does not take (N > 64, M > 64 or a sentence > 255 tokens), which go to
+ * the tiled kernel.  large_ids_host (capacity n_pairs) receives their
+ * indices in ascending order; the caller uploads them and sets
+ * plan->large_ids to the device copy before scoring. */
+typedef struct bimine_plan {
+  int32_t max_n, max_m;        /* over all pairs                          */
+  int32_t max_uniq, max_len;   /* over all sentences                      */
+  int64_t n_large;             /* pairs for the tiled kernel              */
+  const int64_t *large_ids;    /* device array [n_large] (set by caller)  */
+  int32_t large_max_n, large_max_m;
+} bimine_plan;
+
+int bimine_plan_batch(const bimine_batch *batch_host, int64_t *large_ids_host,
+                      bimine_plan *plan);
+
 /* ---- score matrix (align.py:102-129) -------------------------------
  * batch_dev: every pointer in the struct is a device pointer.
  * model: host array of BIMINE_MODEL_DOUBLES.
- * max_n / max_m: max over pairs of N and M (grid extents).
- * max_uniq / max_len: max over sentences of distinct / total tokens
- *   (sizes the shared-memory hash; BIMINE_E_LIMIT above 16384 / 65535).
+ * plan: from bimine_plan_batch, with large_ids uploaded.  BIMINE_E_LIMIT
+ *   if a sentence has more than 4096 distinct or 16384 total tokens.
  * sim_dev: output, written once, row-major per pair at pair_sim_off. */
 int bimine_score_batch(const bimine_dict *dict, const double *model,
-                       const bimine_batch *batch_dev, int32_t max_n,
-                       int32_t max_m, int32_t max_uniq, int32_t max_len,
+                       const bimine_batch *batch_dev, const bimine_plan *plan,
                        double *sim_dev, void *stream);
 
 /* ---- NW + traceback + threshold filter --------------------------------

@@ -66,6 +66,19 @@ class CDictView(ctypes.Structure):
     ]
 
 
+class CPlan(ctypes.Structure):
+    _fields_ = [
+        ("max_n", ctypes.c_int32),
+        ("max_m", ctypes.c_int32),
+        ("max_uniq", ctypes.c_int32),
+        ("max_len", ctypes.c_int32),
+        ("n_large", ctypes.c_int64),
+        ("large_ids", _vp),
+        ("large_max_n", ctypes.c_int32),
+        ("large_max_m", ctypes.c_int32),
+    ]
+
+
 # name -> (restype, argtypes); the complete exported surface of the header
 SIGNATURES = {
     "bimine_last_error": (ctypes.c_char_p, []),
@@ -78,8 +91,8 @@ SIGNATURES = {
     "bimine_dict_destroy": (ctypes.c_int, [_vp]),
     "bimine_dict_view_get": (ctypes.c_int, [_vp, ctypes.POINTER(CDictView)]),
     "bimine_dict_entries": (ctypes.c_int64, [_vp]),
-    "bimine_score_batch": (ctypes.c_int, [_vp, _f64p, ctypes.POINTER(CBatch), ctypes.c_int32, ctypes.c_int32,
-                                          ctypes.c_int32, ctypes.c_int32, _vp, _vp]),
+    "bimine_plan_batch": (ctypes.c_int, [ctypes.POINTER(CBatch), _i64p, ctypes.POINTER(CPlan)]),
+    "bimine_score_batch": (ctypes.c_int, [_vp, _f64p, ctypes.POINTER(CBatch), ctypes.POINTER(CPlan), _vp, _vp]),
     "bimine_nw_mine_batch": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                             ctypes.c_int32, _vp, _vp, ctypes.c_double, ctypes.c_double, _vp, _vp,
                                             _vp, _vp, _vp]),

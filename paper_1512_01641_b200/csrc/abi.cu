@@ -8,7 +8,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdio>
+#include <map>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -18,7 +20,9 @@
 #include "../../include/bimine_b200.h"
 #include "common.cuh"
 #include "nw_kernel.cuh"
+#include "pair_kernel.cuh"
 #include "score_kernel.cuh"
+#include "terms.cuh"
 
 using namespace bimine;
 
@@ -180,33 +184,133 @@ int64_t bimine_dict_entries(const bimine_dict *d) { return d ? d->n_entries : -1
 // score matrix
 // ------------------------------------------------------------------------
 
-int bimine_score_batch(const bimine_dict *dict, const double *model, const bimine_batch *b, int32_t max_n,
-                       int32_t max_m, int32_t max_uniq, int32_t max_len, double *sim_dev, void *stream) {
-  if (!dict || !model || !b || !sim_dev) return fail(BIMINE_E_ARG, "bimine_score_batch: null argument");
+int bimine_plan_batch(const bimine_batch *b, int64_t *large_ids, bimine_plan *plan) {
+  if (!b || !plan || (b->n_pairs > 0 && !large_ids)) return fail(BIMINE_E_ARG, "bimine_plan_batch: null argument");
+  bimine_plan P;
+  memset(&P, 0, sizeof(P));
+  for (int64_t s = 0; s < b->n_sentences; ++s) {
+    P.max_uniq = std::max(P.max_uniq, b->sent_uniq[s]);
+    P.max_len = std::max(P.max_len, b->sent_len[s]);
+  }
+  for (int64_t p = 0; p < b->n_pairs; ++p) {
+    const int32_t n = b->pair_n[p], m = b->pair_m[p];
+    if (n < 1 || m < 1) return fail(BIMINE_E_ARG, "bimine_plan_batch: empty document");
+    P.max_n = std::max(P.max_n, n);
+    P.max_m = std::max(P.max_m, m);
+    int32_t ml = 0;
+    if (n <= kPairMax && m <= kPairMax) {
+      for (int32_t i = 0; i < n; ++i) ml = std::max(ml, b->sent_len[b->pair_src[p] + i]);
+      for (int32_t j = 0; j < m; ++j) ml = std::max(ml, b->sent_len[b->pair_tgt[p] + j]);
+    }
+    if (!pair_is_small(n, m, ml)) {
+      large_ids[P.n_large++] = p;
+      P.large_max_n = std::max(P.large_max_n, n);
+      P.large_max_m = std::max(P.large_max_m, m);
+    }
+  }
+  *plan = P;
+  return BIMINE_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Term tables (terms.cuh) per (device, model), built once on the device.
+struct TermCacheEntry {
+  double *base = nullptr;
+  TermTables T;
+};
+
+std::mutex g_term_mu;
+std::map<std::pair<int, std::array<double, 21>>, TermCacheEntry> g_terms;
+
+int term_tables(const double *model, cudaStream_t st, TermTables *out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::array<double, 21> key;
+  memcpy(key.data(), model, sizeof(double) * 21);
+  std::lock_guard<std::mutex> lock(g_term_mu);
+  auto it = g_terms.find({dev, key});
+  if (it != g_terms.end()) {
+    *out = it->second.T;
+    return BIMINE_OK;
+  }
+  const size_t D2 = (size_t)kTermDim * kTermDim, C2 = (size_t)kCharDim * kCharDim;
+  const size_t total = 4 * D2 + C2 + kRecipDim + 2;
+  TermCacheEntry e;
+  BIMINE_CUDA(cudaMalloc(&e.base, total * sizeof(double)));
+  double *q = e.base;
+  double *t0 = q, *t1 = q + D2, *t2 = q + 2 * D2, *t5 = q + 3 * D2, *t4 = q + 4 * D2;
+  double *rc = t4 + C2, *misc = rc + kRecipDim;
+  const int64_t n = (int64_t)std::max(C2, D2);
+  build_term_tables<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(to_model(model), t0, t1, t2, t5, t4, rc, misc);
+  BIMINE_CUDA(cudaGetLastError());
+  BIMINE_CUDA(cudaStreamSynchronize(st));
+  e.T = TermTables{t0, t1, t2, t5, t4, rc, misc};
+  g_terms[{dev, key}] = e;
+  *out = e.T;
+  return BIMINE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bimine_score_batch(const bimine_dict *dict, const double *model, const bimine_batch *b, const bimine_plan *plan,
+                       double *sim_dev, void *stream) {
+  if (!dict || !model || !b || !plan || !sim_dev) return fail(BIMINE_E_ARG, "bimine_score_batch: null argument");
   if (b->n_pairs == 0) return BIMINE_OK;
-  if (max_n < 1 || max_m < 1 || max_uniq < 1 || max_len < 1)
+  if (plan->max_n < 1 || plan->max_m < 1 || plan->max_uniq < 1 || plan->max_len < 1)
     return fail(BIMINE_E_ARG, "bimine_score_batch: empty document or sentence");
-  if (max_uniq > kMaxCapU || max_len > kMaxCapT)
+  if (plan->max_uniq > kMaxCapU || plan->max_len > kMaxCapT)
     return fail(BIMINE_E_LIMIT, "bimine_score_batch: a sentence has more than 4096 distinct or 16384 total tokens");
   if (b->n_pairs > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: more than 2^31-1 pairs per call");
-  ScoreArgs A;
-  A.b = to_dev(*b);
-  A.d = DictDev{dict->n_rows, dict->row_ptr, dict->tgt, dict->prob};
-  A.md = to_model(model);
-  A.sim = sim_dev;
-  A.cap_u = std::min(kMaxCapU, std::max(1024, next_pow2(max_uniq)));
-  A.cap_t = std::min(kMaxCapT, std::max(4096, next_pow2(max_len)));
-  A.hash_bits = ilog2(2 * A.cap_u);
-  static int *status = nullptr;
-  if (!status) BIMINE_CUDA(cudaMalloc(&status, sizeof(int)));
-  A.status = status;
-  const size_t smem = score_smem_layout(nullptr, A.cap_u, A.cap_t, nullptr);
-  BIMINE_CUDA(cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)b->n_pairs, (unsigned)((max_n + kScoreTile - 1) / kScoreTile),
-            (unsigned)((max_m + kScoreTile - 1) / kScoreTile));
-  if (grid.y > 65535 || grid.z > 65535) return fail(BIMINE_E_LIMIT, "bimine_score_batch: document too long");
-  score_kernel<<<grid, kScoreThreads, smem, as_stream(stream)>>>(A);
-  BIMINE_CUDA(cudaGetLastError());
+  if (plan->n_large > 0 && !plan->large_ids) return fail(BIMINE_E_ARG, "bimine_score_batch: plan.large_ids not set");
+  cudaStream_t st = as_stream(stream);
+  const BatchDev bd = to_dev(*b);
+  const DictDev dd = DictDev{dict->n_rows, dict->row_ptr, dict->tgt, dict->prob};
+  const Model md = to_model(model);
+  // per-pair kernel over every pair; it skips the plan's large pairs
+  if (plan->n_large < b->n_pairs) {
+    PairArgs A;
+    A.b = bd;
+    A.d = dd;
+    A.md = md;
+    int rc = term_tables(model, st, &A.T);
+    if (rc != BIMINE_OK) return rc;
+    A.sim = sim_dev;
+    A.pair_ids = nullptr;
+    A.n = b->n_pairs;
+    A.cap_u = 1024;
+    A.hash_bits = 11;
+    A.cap_t = 2048;
+    const size_t smem = pair_smem_layout(nullptr, A.cap_u, A.hash_bits, A.cap_t, nullptr);
+    BIMINE_CUDA(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    pair_kernel<<<(unsigned)b->n_pairs, kPairThreads, smem, st>>>(A);
+    BIMINE_CUDA(cudaGetLastError());
+  }
+  if (plan->n_large > 0) {
+    ScoreArgs A;
+    A.b = bd;
+    A.d = dd;
+    A.md = md;
+    A.sim = sim_dev;
+    A.pair_ids = plan->large_ids;
+    A.cap_u = std::min(kMaxCapU, std::max(1024, next_pow2(plan->max_uniq)));
+    A.cap_t = std::min(kMaxCapT, std::max(4096, next_pow2(plan->max_len)));
+    A.hash_bits = ilog2(2 * A.cap_u);
+    static int *status = nullptr;
+    if (!status) BIMINE_CUDA(cudaMalloc(&status, sizeof(int)));
+    A.status = status;
+    const size_t smem = score_smem_layout(nullptr, A.cap_u, A.cap_t, nullptr);
+    BIMINE_CUDA(cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((unsigned)plan->n_large, (unsigned)((plan->large_max_n + kScoreTile - 1) / kScoreTile),
+              (unsigned)((plan->large_max_m + kScoreTile - 1) / kScoreTile));
+    if (grid.y > 65535 || grid.z > 65535) return fail(BIMINE_E_LIMIT, "bimine_score_batch: document too long");
+    score_kernel<<<grid, kScoreThreads, smem, st>>>(A);
+    BIMINE_CUDA(cudaGetLastError());
+  }
   return BIMINE_OK;
 }
 
@@ -396,23 +500,22 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   if (P == 0) return BIMINE_OK;
   pool_setup();
   cudaStream_t st = as_stream(stream);
-  int32_t max_n = 0, max_m = 0, max_u = 0, max_l = 0;
-  std::vector<int64_t> out_off(P);
+  std::vector<int64_t> out_off(P), large(P);
+  bimine_plan plan;
+  {
+    int rc = bimine_plan_batch(h, large.data(), &plan);
+    if (rc != BIMINE_OK) return rc;
+  }
+  const int32_t max_n = plan.max_n, max_m = plan.max_m;
   int64_t cap = 0, cells = 0;
   for (int64_t p = 0; p < P; ++p) {
     const int32_t n = h->pair_n[p], m = h->pair_m[p];
-    if (n < 1 || m < 1) return fail(BIMINE_E_ARG, "bimine_mine_host: empty document");
-    max_n = std::max(max_n, n);
-    max_m = std::max(max_m, m);
     out_off[p] = cap;
     cap += std::min(n, m);
     cells = std::max(cells, h->pair_sim_off[p] + (int64_t)n * m);
   }
-  for (int64_t s = 0; s < S; ++s) {
+  for (int64_t s = 0; s < S; ++s)
     if (h->sent_len[s] < 1) return fail(BIMINE_E_ARG, "bimine_mine_host: empty sentence");
-    max_u = std::max(max_u, h->sent_uniq[s]);
-    max_l = std::max(max_l, h->sent_len[s]);
-  }
   if (capacity < cap) return fail(BIMINE_E_ARG, "bimine_mine_host: capacity < sum of min(N, M)");
   // one device arena, carved in 256-byte aligned pieces
   size_t off = 0;
@@ -425,7 +528,8 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
                o_schar = carve(4 * S), o_psrc = carve(8 * P), o_pn = carve(4 * P), o_ptgt = carve(8 * P),
                o_pm = carve(4 * P), o_psim = carve(8 * P), o_outoff = carve(8 * P), o_sim = carve(8 * cells),
                o_slots = carve(sizeof(bimine_match) * cap), o_counts = carve(4 * P), o_base = carve(8 * P),
-               o_comp = carve(sizeof(bimine_match) * cap), o_total = carve(8), o_par = carve(16);
+               o_comp = carve(sizeof(bimine_match) * cap), o_total = carve(8), o_par = carve(16),
+               o_large = carve(8 * plan.n_large);
   char *arena = nullptr;
   BIMINE_CUDA(cudaMallocAsync((void **)&arena, off, st));
   auto H2D = [&](size_t o, const void *src, size_t bytes) {
@@ -445,6 +549,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   e = e ? e : H2D(o_psim, h->pair_sim_off, 8 * P);
   e = e ? e : H2D(o_outoff, out_off.data(), 8 * P);
   e = e ? e : H2D(o_par, par, 16);
+  e = e ? e : H2D(o_large, large.data(), 8 * plan.n_large);
   if (e != cudaSuccess) {
     cudaFreeAsync(arena, st);
     return fail(BIMINE_E_CUDA, std::string("bimine_mine_host H2D: ") + cudaGetErrorString(e));
@@ -464,7 +569,8 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   d.pair_m = (const int32_t *)(arena + o_pm);
   d.pair_sim_off = (const int64_t *)(arena + o_psim);
   double *sim = (double *)(arena + o_sim);
-  int rc = bimine_score_batch(dict, model, &d, max_n, max_m, max_u, max_l, sim, stream);
+  plan.large_ids = (const int64_t *)(arena + o_large);
+  int rc = bimine_score_batch(dict, model, &d, &plan, sim, stream);
   const double *pd = (const double *)(arena + o_par);
   if (rc == BIMINE_OK)
     rc = bimine_nw_mine_batch(sim, d.pair_sim_off, d.pair_n, d.pair_m, P, max_n, max_m, 1, pd, pd + 1, mismatch,

@@ -102,42 +102,61 @@ __device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *r
     const int64_t sdir = (MODE == kNwTable) ? 1 : -1;
     uint32_t bits = 0u;
     const int nsteps = M + 31;
-    for (int s = 0; s < nsteps; ++s) {
-      const int b = s - lane + 1;
-      double up = __shfl_up_sync(kFull, cur, 1);
-      if (lane == 0) {
-        up = (b >= 1 && b <= M) ? rowbuf[b] : 0.0;
-        if (b >= 1 && b <= M) diag = rowbuf[b - 1];
+    // R values for 8 steps at a time, the next 8 prefetched into registers
+    // (one dependent global load per step would make the sweep latency bound)
+    double cur8[8], nxt8[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int b = u - lane + 1;
+      nxt8[u] = (active && b >= 1 && b <= M) ? __ldg(srow + sdir * (b - 1)) : 0.0;
+    }
+    for (int s0 = 0; s0 < nsteps; s0 += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) cur8[u] = nxt8[u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int b = s0 + 8 + u - lane + 1;
+        nxt8[u] = (active && b >= 1 && b <= M) ? __ldg(srow + sdir * (b - 1)) : 0.0;
       }
-      if (active && b >= 1 && b <= M) {
-        const double r = srow[sdir * (b - 1)];
-        const double c = fadd(mismatch, fmul(r, span));
-        double best = fadd(diag, c);
-        uint32_t dir = 0u;
-        double cand = fsub(up, gap);
-        if (cand > best) {
-          best = cand;
-          dir = 1u;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int s = s0 + u;
+        if (s >= nsteps) break;
+        const int b = s - lane + 1;
+        double up = __shfl_up_sync(kFull, cur, 1);
+        if (lane == 0) {
+          up = (b >= 1 && b <= M) ? rowbuf[b] : 0.0;
+          if (b >= 1 && b <= M) diag = rowbuf[b - 1];
         }
-        cand = fsub(cur, gap);
-        if (cand > best) {
-          best = cand;
-          dir = 2u;
-        }
-        cur = best;
-        if (MODE == kNwTable) {
-          table[(int64_t)a * tw + b] = best;
-        } else {
-          bits |= dir << (2 * (b & 15));
-          if ((b & 15) == 15 || b == M) {
-            dirs[(int64_t)a * stride + (b >> 4)] = bits;
-            bits = 0u;
+        if (active && b >= 1 && b <= M) {
+          const double c = fadd(mismatch, fmul(cur8[u], span));
+          double best = fadd(diag, c);
+          uint32_t dir = 0u;
+          double cand = fsub(up, gap);
+          if (cand > best) {
+            best = cand;
+            dir = 1u;
           }
+          cand = fsub(cur, gap);
+          if (cand > best) {
+            best = cand;
+            dir = 2u;
+          }
+          cur = best;
+          if (MODE == kNwTable) {
+            table[(int64_t)a * tw + b] = best;
+          } else {
+            bits |= dir << (2 * (b & 15));
+            if ((b & 15) == 15 || b == M) {
+              dirs[(int64_t)a * stride + (b >> 4)] = bits;
+              bits = 0u;
+            }
+          }
+          if (lane == 31) rowbuf[b] = best;
+          if (a == N && b == M) last = best;
         }
-        if (lane == 31) rowbuf[b] = best;
-        if (a == N && b == M) last = best;
+        if (lane > 0) diag = up;  // dp[a-1][b] becomes next step's diagonal
       }
-      if (lane > 0) diag = up;  // dp[a-1][b] becomes next step's diagonal
     }
     // the next band's lane 0 needs dp[a0+32][0] as its first diagonal
     __syncwarp();

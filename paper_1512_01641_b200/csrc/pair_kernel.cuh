@@ -1,0 +1,434 @@
+// pair_kernel.cuh -- score matrix of one document pair per CTA.
+//
+// build_score_matrix (align.py:102-129) for pairs with N, M <= 64 and
+// sentences of <= 255 tokens (every BASELINE config except the long-pair
+// stress C3 and the 200x220 C1 pair, which take the tiled score_kernel).
+// 8 warps; all per-pair state lives in shared memory and every count is
+// produced 32 cells at a time by bit-matrix transposes:
+//
+//  A  target hash: every target token of the chunk -> dense id d;
+//     colmask[d] = 64-bit set of target sentences containing d.
+//  D  warp per source sentence i, lanes = 32 occurrences at a time, in
+//     order.  Lane k walks its token's dictionary row (p > 0 entries
+//     only, CSR) against the hash: anyhit_k = OR of colmask over its
+//     translations; the top three (colmask, p) by p are kept; reachcol[d]
+//     |= bit i (reachable_targets, classifier.py:54-59).  A 32x32 bit
+//     transpose turns the anyhit rows into, for lane j, the set of
+//     occurrences with a translation in target sentence j; popc adds
+//     `covered`, and walking the set bits in ascending order adds the
+//     max probability to the running sum -- the exact sequential sum of
+//     classifier.py:75-82.  Shared tokens (classifier.py:94) are counted
+//     the same way from the first occurrences of source tokens that are
+//     themselves target tokens.
+//  C  warp per target sentence j, lanes = occurrences: transposing the
+//     reachcol rows gives covered_target(i, j) by popc
+//     (classifier.py:88-92), multiplicities included.
+//  F  all threads, one cell each (flattened, full lanes): six features ->
+//     margin -> logistic (terms.cuh), one coalesced store per cell.
+//
+// If the chunk's distinct target tokens exceed the hash capacity the
+// target side is processed in halves (same results, more passes).
+#pragma once
+
+#include "common.cuh"
+#include "terms.cuh"
+
+namespace bimine {
+
+constexpr int kPairThreads = 256;
+constexpr int kPairWarps = kPairThreads / 32;
+constexpr int kPairMax = 64;         // sentences per side
+constexpr int kPairMaxLen = 255;     // tokens per sentence (u8 counts)
+constexpr int kCellStride = 64;      // per-cell arrays are [64][64]
+
+struct PairArgs {
+  BatchDev b;
+  DictDev d;
+  Model md;
+  TermTables T;
+  double *sim;
+  const int64_t *pair_ids;  // optional: launch over these pairs
+  int64_t n;                // pairs in this launch
+  int cap_u;                // distinct target tokens per chunk (dense arrays)
+  int hash_bits;            // log2(hash slots) >= log2(2 cap_u)
+  int cap_t;                // target occurrences per chunk
+};
+
+struct PairSmem {
+  uint64_t *exp_tab;   // [256]
+  uint64_t *colmask;   // [cap_u]
+  uint64_t *reachcol;  // [cap_u]
+  double *sum;         // [64][64]
+  uint64_t *r_any;     // [warps][32]
+  uint64_t *r_ma;      // [warps][32]
+  uint64_t *r_mb;      // [warps][32]
+  double *r_pa, *r_pb, *r_pc;  // [warps][32]
+  int64_t *src_off, *tgt_off;  // [64]
+  double *tgt_rct;     // [64] RN(1/Ct)
+  int32_t *keys;       // [slots]
+  int32_t *src_len, *src_uniq, *src_chars;  // [64]
+  int32_t *tgt_len, *tgt_uniq, *tgt_chars;  // [64]
+  int32_t *tgt_occ0;   // [65] chunk-local occurrence offsets
+  int32_t *r_tok;      // [warps][32]
+  int32_t *misc;       // [8]
+  int16_t *dense;      // [slots]
+  int16_t *tgt_d;      // [cap_t]
+  uint8_t *cov, *covt, *shr;  // [64][64]
+  uint8_t *r_n;        // [warps][32]
+};
+
+__host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_u, int hash_bits, int cap_t,
+                                                   PairSmem *s) {
+  size_t o = 0;
+  auto take = [&](size_t bytes, size_t al) -> unsigned char * {
+    o = (o + al - 1) / al * al;
+    unsigned char *p = base ? base + o : nullptr;
+    o += bytes;
+    return p;
+  };
+  const size_t slots = (size_t)1 << hash_bits;
+  const size_t W = kPairWarps * 32;
+  PairSmem t;
+  t.exp_tab = (uint64_t *)take(256 * 8, 16);
+  t.colmask = (uint64_t *)take((size_t)cap_u * 8, 16);
+  t.reachcol = (uint64_t *)take((size_t)cap_u * 8, 16);
+  t.sum = (double *)take(64 * 64 * 8, 16);
+  t.r_any = (uint64_t *)take(W * 8, 16);
+  t.r_ma = (uint64_t *)take(W * 8, 16);
+  t.r_mb = (uint64_t *)take(W * 8, 16);
+  t.r_pa = (double *)take(W * 8, 16);
+  t.r_pb = (double *)take(W * 8, 16);
+  t.r_pc = (double *)take(W * 8, 16);
+  t.src_off = (int64_t *)take(64 * 8, 16);
+  t.tgt_off = (int64_t *)take(64 * 8, 16);
+  t.tgt_rct = (double *)take(64 * 8, 16);
+  t.keys = (int32_t *)take(slots * 4, 16);
+  t.src_len = (int32_t *)take(64 * 4, 4);
+  t.src_uniq = (int32_t *)take(64 * 4, 4);
+  t.src_chars = (int32_t *)take(64 * 4, 4);
+  t.tgt_len = (int32_t *)take(64 * 4, 4);
+  t.tgt_uniq = (int32_t *)take(64 * 4, 4);
+  t.tgt_chars = (int32_t *)take(64 * 4, 4);
+  t.tgt_occ0 = (int32_t *)take(65 * 4, 4);
+  t.r_tok = (int32_t *)take(W * 4, 4);
+  t.misc = (int32_t *)take(8 * 4, 4);
+  t.dense = (int16_t *)take(slots * 2, 4);
+  t.tgt_d = (int16_t *)take((size_t)cap_t * 2, 4);
+  t.cov = (uint8_t *)take(64 * 64, 4);
+  t.covt = (uint8_t *)take(64 * 64, 4);
+  t.shr = (uint8_t *)take(64 * 64, 4);
+  t.r_n = (uint8_t *)take(W, 4);
+  if (s) *s = t;
+  return (o + 15) / 16 * 16;
+}
+
+// lane j of the result holds bit k = bit j of lane k's x (32x32 bit transpose)
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t m = (s == 16) ? 0x0000FFFFu : (s == 8) ? 0x00FF00FFu : (s == 4) ? 0x0F0F0F0Fu
+                       : (s == 2) ? 0x33333333u : 0x55555555u;
+    const uint32_t o = __shfl_xor_sync(kFull, x, s);
+    x = (lane & s) ? ((x & ~m) | ((o & ~m) >> s)) : ((x & m) | ((o & m) << s));
+  }
+  return x;
+}
+
+__device__ __forceinline__ int pk_find(const int32_t *keys, const int16_t *dense, int bits, int32_t key) {
+  const uint32_t mask = (1u << bits) - 1u;
+  uint32_t slot = hash_slot(key, 32 - bits);
+  while (true) {
+    const int32_t k = keys[slot];
+    if (k == key) return dense[slot];
+    if (k == -1) return -1;
+    slot = (slot + 1u) & mask;
+  }
+}
+
+__device__ __forceinline__ void pk_insert(int32_t *keys, int bits, int32_t key) {
+  const uint32_t mask = (1u << bits) - 1u;
+  uint32_t slot = hash_slot(key, 32 - bits);
+  while (true) {
+    const int32_t k = keys[slot];
+    if (k == key) return;
+    if (k == -1) {
+      const int32_t prev = atomicCAS(&keys[slot], -1, key);
+      if (prev == -1 || prev == key) return;
+    }
+    slot = (slot + 1u) & mask;
+  }
+}
+
+// Is the pair handled by pair_kernel?  (host and device agree on this rule)
+__host__ __device__ inline bool pair_is_small(int n, int m, int max_len) {
+  return n <= kPairMax && m <= kPairMax && max_len <= kPairMaxLen;
+}
+
+__global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int64_t p = A.pair_ids ? A.pair_ids[blockIdx.x] : (int64_t)blockIdx.x;
+  const int N = A.b.pair_n[p], M = A.b.pair_m[p];
+  if (N > kPairMax || M > kPairMax) return;
+  PairSmem S;
+  const int hbits = A.hash_bits;
+  pair_smem_layout(smem_raw, A.cap_u, hbits, A.cap_t, &S);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t s_first = A.b.pair_src[p], t_first = A.b.pair_tgt[p];
+  const int32_t *__restrict__ tokens = A.b.tokens;
+  const int64_t *__restrict__ row_ptr = A.d.row_ptr;
+  const int32_t *__restrict__ dtgt = A.d.tgt;
+  const double *__restrict__ dprob = A.d.prob;
+  const int64_t n_rows = A.d.n_rows;
+  const int hslots = 1 << hbits;
+
+  // ---- 0: tables and sentence metadata
+  for (int k = tid; k < 256; k += kPairThreads) S.exp_tab[k] = kExpTableDev[k];
+  if (tid < N) {
+    S.src_off[tid] = A.b.sent_tok_off[s_first + tid];
+    S.src_len[tid] = A.b.sent_len[s_first + tid];
+    S.src_uniq[tid] = A.b.sent_uniq[s_first + tid];
+    S.src_chars[tid] = A.b.sent_chars[s_first + tid];
+  } else if (tid >= 64 && tid - 64 < M) {
+    const int j = tid - 64;
+    S.tgt_off[j] = A.b.sent_tok_off[t_first + j];
+    S.tgt_len[j] = A.b.sent_len[t_first + j];
+    S.tgt_uniq[j] = A.b.sent_uniq[t_first + j];
+    const int ct = A.b.sent_chars[t_first + j];
+    S.tgt_chars[j] = ct;
+    S.tgt_rct[j] = fdiv(1.0, (double)ct);
+  }
+  __syncthreads();
+  {  // the rule of pair_is_small: every sentence <= kPairMaxLen tokens
+    const int l = tid < N ? S.src_len[tid] : (tid >= 64 && tid - 64 < M) ? S.tgt_len[tid - 64] : 0;
+    if (__syncthreads_or(l > kPairMaxLen)) return;
+  }
+
+  for (int jc0 = 0; jc0 < M;) {
+    // ---- chunk [jc0, jc1): at most cap_t target occurrences
+    if (warp == 0) {
+      int run = 0, end = jc0;
+      for (int base = jc0; base < M; base += 32) {
+        const int j = base + lane;
+        const int v = j < M ? S.tgt_len[j] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x += y;
+        }
+        const bool fits = j < M && run + x <= A.cap_t;
+        const unsigned ok = __ballot_sync(kFull, fits);
+        const int cnt = __popc(ok);  // prefix property: fitting lanes are a prefix
+        end = base + cnt;
+        if (cnt < 32) break;
+        run += __shfl_sync(kFull, x, 31);
+      }
+      if (lane == 0) S.misc[1] = max(end, jc0 + 1);
+    }
+    __syncthreads();
+    int jc1 = S.misc[1];
+    while (true) {
+      const int nj = jc1 - jc0;
+      // occurrence offsets of the chunk
+      if (warp == 0) {
+        int run = 0;
+        for (int base = 0; base < nj; base += 32) {
+          const int jj = base + lane;
+          const int v = jj < nj ? S.tgt_len[jc0 + jj] : 0;
+          int x = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+          }
+          if (jj < nj) S.tgt_occ0[jj] = run + x - v;
+          run += __shfl_sync(kFull, x, 31);
+        }
+        if (lane == 0) {
+          S.tgt_occ0[nj] = run;
+          S.misc[0] = 0;
+        }
+      }
+      for (int k = tid; k < hslots; k += kPairThreads) S.keys[k] = -1;
+      __syncthreads();
+      // ---- A1: insert
+      for (int jj = warp; jj < nj; jj += kPairWarps) {
+        const int64_t off = S.tgt_off[jc0 + jj];
+        const int L = S.tgt_len[jc0 + jj];
+        for (int k = lane; k < L; k += 32) pk_insert(S.keys, hbits, tokens[off + k]);
+      }
+      __syncthreads();
+      // ---- A2: dense ids
+      for (int k = tid; k < hslots; k += kPairThreads) {
+        if (S.keys[k] != -1) {
+          const int d = atomicAdd(&S.misc[0], 1);
+          if (d < A.cap_u) {
+            S.dense[k] = (int16_t)d;
+            S.colmask[d] = 0ull;
+            S.reachcol[d] = 0ull;
+          }
+        }
+      }
+      __syncthreads();
+      if (S.misc[0] <= A.cap_u || nj == 1) break;
+      jc1 = jc0 + nj / 2;  // too many distinct tokens: halve the chunk
+      __syncthreads();
+    }
+    const int nj = jc1 - jc0;
+    // ---- A3: occurrences -> dense id, sentence sets
+    for (int jj = warp; jj < nj; jj += kPairWarps) {
+      const int64_t off = S.tgt_off[jc0 + jj];
+      const int L = S.tgt_len[jc0 + jj];
+      const int q0 = S.tgt_occ0[jj];
+      for (int k = lane; k < L; k += 32) {
+        const int d = pk_find(S.keys, S.dense, hbits, tokens[off + k]);
+        S.tgt_d[q0 + k] = (int16_t)d;
+        atomicOr((unsigned long long *)&S.colmask[d], 1ull << jj);
+      }
+    }
+    __syncthreads();
+    // ---- D: source side, warp per source sentence
+    {
+      uint64_t *ra = S.r_any + warp * 32, *rma = S.r_ma + warp * 32, *rmb = S.r_mb + warp * 32;
+      double *rpa = S.r_pa + warp * 32, *rpb = S.r_pb + warp * 32, *rpc = S.r_pc + warp * 32;
+      int32_t *rtok = S.r_tok + warp * 32;
+      uint8_t *rn = S.r_n + warp * 32;
+      const int jlo = lane, jhi = lane + 32;
+      for (int i = warp; i < N; i += kPairWarps) {
+        const int64_t off = S.src_off[i];
+        const int L = S.src_len[i];
+        const unsigned long long ibit = 1ull << i;
+        int cov_lo = 0, cov_hi = 0, sh_lo = 0, sh_hi = 0;
+        double sum_lo = 0.0, sum_hi = 0.0;
+        for (int seg = 0; seg < L; seg += 32) {
+          const int k = seg + lane;
+          const bool valid = k < L;
+          const int32_t s = valid ? tokens[off + k] : -1;
+          // shared tokens: first occurrence of a source token that is a chunk token
+          const int ds = valid ? pk_find(S.keys, S.dense, hbits, s) : -1;
+          const unsigned peers = __match_any_sync(kFull, s);
+          bool first = (__ffs(peers) - 1) == lane;
+          if (ds >= 0 && first && seg > 0)
+            for (int kk = 0; kk < seg; ++kk)
+              if (tokens[off + kk] == s) {
+                first = false;
+                break;
+              }
+          const uint64_t shm = (ds >= 0 && first) ? S.colmask[ds] : 0ull;
+          // dictionary row against the chunk: anyhit + top-3 (mask, p) by p
+          uint64_t any = 0ull, ma = 0ull, mb = 0ull;
+          double pa = 0.0, pb = 0.0, pc = 0.0;
+          int n = 0;
+          if (valid && s >= 0 && s < n_rows) {
+            const int64_t e0 = row_ptr[s], e1 = row_ptr[s + 1];
+            for (int64_t e = e0; e < e1; ++e) {
+              const int d = pk_find(S.keys, S.dense, hbits, dtgt[e]);
+              if (d < 0) continue;
+              const uint64_t m = S.colmask[d];
+              const double pr = dprob[e];
+              any |= m;
+              atomicOr((unsigned long long *)&S.reachcol[d], ibit);
+              ++n;
+              if (pr > pa) {
+                pc = pb; pb = pa; mb = ma; pa = pr; ma = m;
+              } else if (pr > pb) {
+                pc = pb; pb = pr; mb = m;
+              } else if (pr > pc) {
+                pc = pr;
+              }
+            }
+          }
+          ra[lane] = any;
+          rma[lane] = ma;
+          rmb[lane] = mb;
+          rpa[lane] = pa;
+          rpb[lane] = pb;
+          rpc[lane] = pc;
+          rn[lane] = (uint8_t)(n > 3 ? 255 : n);
+          rtok[lane] = s;
+          __syncwarp();
+          if (__any_sync(kFull, shm != 0ull)) {
+            sh_lo += __popc(transpose32((uint32_t)shm, lane));
+            sh_hi += __popc(transpose32((uint32_t)(shm >> 32), lane));
+          }
+          uint32_t hl = transpose32((uint32_t)any, lane);
+          uint32_t hh = transpose32((uint32_t)(any >> 32), lane);
+          cov_lo += __popc(hl);
+          cov_hi += __popc(hh);
+          // ordered sums: ascending occurrence index = reference order
+#pragma unroll 1
+          for (int half = 0; half < 2; ++half) {
+            uint32_t h = half ? hh : hl;
+            const int j = half ? jhi : jlo;
+            double acc = half ? sum_hi : sum_lo;
+            while (h) {
+              const int kk = __ffs(h) - 1;
+              h &= h - 1u;
+              const int c = rn[kk];
+              double best;
+              if (c == 1) {
+                best = rpa[kk];
+              } else if (c == 2) {
+                best = ((rma[kk] >> j) & 1ull) ? rpa[kk] : rpb[kk];
+              } else if (c == 3) {
+                best = ((rma[kk] >> j) & 1ull) ? rpa[kk] : ((rmb[kk] >> j) & 1ull) ? rpb[kk] : rpc[kk];
+              } else {  // more than three translations in the chunk: walk the row again
+                best = 0.0;
+                const int32_t sk = rtok[kk];
+                const int64_t e1 = row_ptr[sk + 1];
+                for (int64_t e = row_ptr[sk]; e < e1; ++e) {
+                  const int d = pk_find(S.keys, S.dense, hbits, dtgt[e]);
+                  if (d >= 0 && ((S.colmask[d] >> j) & 1ull) && dprob[e] > best) best = dprob[e];
+                }
+              }
+              acc = fadd(acc, best);
+            }
+            if (half) sum_hi = acc;
+            else sum_lo = acc;
+          }
+          __syncwarp();
+        }
+        if (jlo < nj) {
+          const int c = i * kCellStride + jc0 + jlo;
+          S.cov[c] = (uint8_t)cov_lo;
+          S.sum[c] = sum_lo;
+          S.shr[c] = (uint8_t)sh_lo;
+        }
+        if (jhi < nj) {
+          const int c = i * kCellStride + jc0 + jhi;
+          S.cov[c] = (uint8_t)cov_hi;
+          S.sum[c] = sum_hi;
+          S.shr[c] = (uint8_t)sh_hi;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- C: covered_target, warp per target sentence, lanes over occurrences
+    for (int jj = warp; jj < nj; jj += kPairWarps) {
+      const int q0 = S.tgt_occ0[jj];
+      const int L = S.tgt_len[jc0 + jj];
+      int c_lo = 0, c_hi = 0;
+      for (int seg = 0; seg < L; seg += 32) {
+        const uint64_t r = (seg + lane < L) ? S.reachcol[S.tgt_d[q0 + seg + lane]] : 0ull;
+        c_lo += __popc(transpose32((uint32_t)r, lane));
+        c_hi += __popc(transpose32((uint32_t)(r >> 32), lane));
+      }
+      if (lane < N) S.covt[lane * kCellStride + jc0 + jj] = (uint8_t)c_lo;
+      if (lane + 32 < N) S.covt[(lane + 32) * kCellStride + jc0 + jj] = (uint8_t)c_hi;
+    }
+    jc0 = jc1;
+    __syncthreads();
+  }
+
+  // ---- F: finalize, one cell per thread, coalesced stores
+  double *__restrict__ out = A.sim + A.b.pair_sim_off[p];
+  const int cells = N * M;
+  for (int c = tid; c < cells; c += kPairThreads) {
+    const int i = c / M, j = c - i * M;
+    const int x = i * kCellStride + j;
+    out[c] = cell_score_t(A.md, A.T, S.src_len[i], S.src_uniq[i], S.src_chars[i], S.tgt_len[j], S.tgt_uniq[j],
+                          S.tgt_chars[j], S.cov[x], S.sum[x], S.covt[x], S.shr[x], S.exp_tab);
+  }
+}
+
+}  // namespace bimine

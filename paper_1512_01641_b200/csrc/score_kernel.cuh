@@ -45,6 +45,7 @@ struct ScoreArgs {
   DictDev d;
   Model md;
   double *sim;
+  const int64_t *pair_ids;  // pairs of this launch (blockIdx.x indexes it); null = identity
   int cap_u;       // distinct target tokens per chunk
   int cap_t;       // target occurrences per chunk
   int hash_bits;   // log2(hash slots) = log2(2 * cap_u)
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const ScoreArgs
   ScoreSmem S;
   score_smem_layout(smem_raw, A.cap_u, A.cap_t, &S);
 
-  const int64_t p = blockIdx.x;
+  const int64_t p = A.pair_ids ? A.pair_ids[blockIdx.x] : (int64_t)blockIdx.x;
   const int N = A.b.pair_n[p];
   const int M = A.b.pair_m[p];
   const int i0 = blockIdx.y * kScoreTile;

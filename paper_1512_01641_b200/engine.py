@@ -86,6 +86,7 @@ def lexicon_context(lexicon) -> LexiconContext:
 
 
 def current_device() -> int:
+    N.load()  # raises NativeUnavailable without the library or a GPU
     return _torch().cuda.current_device()
 
 
@@ -111,13 +112,23 @@ class DeviceBatch:
                 a = a.pin_memory()
             self.t[f] = a.to(f"cuda:{device}", non_blocking=pinned)
         self.struct = N.batch_struct_device(self.t, batch.n_pairs, batch.n_sentences, batch.n_tokens)
-        self.max_n = int(batch.pair_n.max(initial=0))
-        self.max_m = int(batch.pair_m.max(initial=0))
-        self.max_uniq = int(batch.sent_uniq.max(initial=0))
-        self.max_len = int(batch.sent_len.max(initial=0))
+        self.plan, large = plan_batch(batch)
+        self.t["large_ids"] = torch.from_numpy(large).to(f"cuda:{device}")
+        self.plan.large_ids = self.t["large_ids"].data_ptr() if large.size else None
+        self.max_n, self.max_m = int(self.plan.max_n), int(self.plan.max_m)
         cap = batch.match_capacity()
         self.capacity = int(cap[-1])
         self.t["out_off"] = torch.from_numpy(cap[:-1].copy()).to(f"cuda:{device}")
+
+
+def plan_batch(batch: PackedBatch):
+    """bimine_plan_batch on the host arrays -> (CPlan, large pair ids)."""
+    L = N.load(require_gpu=False)
+    large = np.zeros(max(batch.n_pairs, 1), dtype=np.int64)
+    plan = N.CPlan()
+    cb = N.batch_struct_host(batch)
+    N.check(L.bimine_plan_batch(ctypes.byref(cb), N.ptr(large, N._i64p), ctypes.byref(plan)))
+    return plan, large[: int(plan.n_large)].copy()
 
 
 def stream_ptr(stream=None) -> int:
@@ -130,8 +141,8 @@ def score_device(dd: DeviceDictionary, model_vec: np.ndarray, db: DeviceBatch, s
     """build_score_matrix for every pair of a device batch into `sim` (torch f64)."""
     L = N.load()
     mv = np.ascontiguousarray(model_vec, dtype=np.float64)
-    N.check(L.bimine_score_batch(dd.handle, N.ptr(mv, N._f64p), ctypes.byref(db.struct), db.max_n, db.max_m,
-                                 db.max_uniq, db.max_len, sim.data_ptr(), stream_ptr(stream)))
+    N.check(L.bimine_score_batch(dd.handle, N.ptr(mv, N._f64p), ctypes.byref(db.struct), ctypes.byref(db.plan),
+                                 sim.data_ptr(), stream_ptr(stream)))
 
 
 def mine_device(db: DeviceBatch, sim, gap: float, threshold: float, mismatch: float, bonus: float,

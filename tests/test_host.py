@@ -1,0 +1,178 @@
+"""CPU-only checks of the host side: tokenizer, packing, the exp
+restatement, the C ABI surface, configuration and sharding logic."""
+
+import ctypes
+import os
+import re
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import helpers as H
+from paper_1512_01641_b200 import align as A
+from paper_1512_01641_b200 import synth
+from paper_1512_01641_b200.packing import BatchBuilder, PackedBatch, Vocabulary, unique_counts
+from paper_1512_01641_b200.text import tokenize
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CSRC = os.path.join(REPO, "paper_1512_01641_b200", "csrc")
+HEADER = os.path.join(REPO, "include", "bimine_b200.h")
+
+
+def test_tokenize_matches_reference_rules():
+    # text.py:97-104: lower, split on whitespace, strip ASCII punctuation
+    assert tokenize("Domo, kato!") == ["domo", "kato"]
+    assert tokenize("...") == []
+    assert tokenize("  A\tb\nC  ") == ["a", "b", "c"]
+    assert tokenize("(dog) -- x.y 'z'") == ["dog", "x.y", "z"]
+    assert tokenize("Żółw «ok»") == ["żółw", "«ok»"]  # non-ASCII punctuation is kept
+    assert tokenize("ǅ") == ["ǆ"]
+
+
+def test_batch_builder_profiles_and_errors():
+    vocab = Vocabulary()
+    b = BatchBuilder(vocab)
+    b.add_pair(["a b a.", "Żółw!"], ["b c", "a"])
+    with pytest.raises(ValueError, match="target sentence 1: untokenizable sentence: '...'"):
+        b.add_pair(["a"], ["b", "..."])
+    with pytest.raises(ValueError, match="both sentence sequences must be non-empty"):
+        b.add_pair([], ["b"])
+    pb = b.build()
+    assert pb.n_pairs == 1 and pb.n_sentences == 4
+    assert pb.sent_len.tolist() == [3, 1, 2, 1]
+    assert pb.sent_uniq.tolist() == [2, 1, 2, 1]
+    assert pb.sent_chars.tolist() == [len("a b a."), len("Żółw!"), 3, 1]
+    assert pb.pair_src.tolist() == [0] and pb.pair_tgt.tolist() == [2]
+    assert pb.pair_sim_off.tolist() == [0] and pb.n_cells == 4
+    assert [vocab.words[t] for t in pb.tokens.tolist()] == ["a", "b", "a", "żółw", "b", "c", "a"]
+
+
+def test_unique_counts_and_select():
+    corpus = synth.make_config(2, n_pairs=5)
+    b = corpus.batch
+    want = [len(set(b.tokens[o : o + l].tolist())) for o, l in zip(b.sent_tok_off, b.sent_len)]
+    assert unique_counts(b.tokens, b.sent_len).tolist() == want
+    sub = b.select([3, 1])
+    assert sub.n_pairs == 2
+    assert sub.pair_n.tolist() == [b.pair_n[3], b.pair_n[1]]
+    s3 = b.tokens[b.sent_tok_off[b.pair_src[3]] : b.sent_tok_off[b.pair_src[3]] + b.sent_len[b.pair_src[3]]]
+    assert np.array_equal(sub.tokens[: len(s3)], s3)
+
+
+def test_synthetic_generator_is_deterministic_and_shaped():
+    a = synth.make_config(2, n_pairs=20)
+    b = synth.make_config(2, n_pairs=20)
+    assert np.array_equal(a.batch.tokens, b.batch.tokens)
+    assert a.batch.pair_n.min() >= 40 and a.batch.pair_n.max() <= 60
+    assert np.all(np.abs(a.batch.pair_m - a.batch.pair_n) <= 5)
+    assert a.batch.sent_len.min() >= 1
+    assert 3 <= np.median(a.batch.sent_len) <= 40
+    assert len(a.dictionary.src) > 900_000  # ~1M-entry dictionary
+    for p, ref in enumerate(a.reference):
+        assert all(i2 > i1 and j2 > j1 for (i1, j1), (i2, j2) in zip(ref, ref[1:]))
+    src, tgt = a.pair_sentences(0)
+    assert len(src) == a.batch.pair_n[0] and all(s.endswith(".") for s in src)
+
+
+def test_exp_table_matches_definition():
+    sys.path.insert(0, CSRC)
+    import gen_exp_table
+
+    with open(os.path.join(CSRC, "exp_table.inc")) as fh:
+        assert fh.read() == gen_exp_table.render()
+
+
+def test_host_compiled_exp_matches_libm(tmp_path):
+    """glibc_exp.cuh compiled for the host equals libm exp (math.exp)."""
+    src = tmp_path / "t.cpp"
+    src.write_text(
+        '#include "%s/glibc_exp.cuh"\n#include <cstdio>\n#include <random>\n#include <cmath>\n'
+        "int main(){std::mt19937_64 g(3);long bad=0;std::uniform_real_distribution<double> u(-750,720);\n"
+        "for(long i=0;i<3000000;++i){double x=i%%3?u(g):bimine::u2d(g());double a=bimine::glibc_exp(x,bimine::kExpTable),b=exp(x);\n"
+        "if(bimine::d2u(a)!=bimine::d2u(b)&&!(std::isnan(a)&&std::isnan(b)))++bad;}printf(\"%%ld\\n\",bad);return bad!=0;}\n" % CSRC
+    )
+    exe = tmp_path / "t"
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-std=c++17", str(src), "-o", str(exe), "-lm"], check=True)
+    res = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert res.returncode == 0, res.stdout
+
+
+def _declared_symbols():
+    with open(HEADER) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\**\s*(bimine_[a-z_0-9]+)\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1512_01641_b200 import _native, build
+
+    build.build()
+    L = _native.load(require_gpu=False)
+    declared = _declared_symbols()
+    assert len(declared) >= 14
+    for name in declared:
+        assert hasattr(L, name), name
+        assert name in _native.SIGNATURES, name
+    assert L.bimine_version().startswith(b"bimine_b200")
+    out = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH], capture_output=True, text=True).stdout
+    for name in declared:
+        assert re.search(rf"\bT {name}$", out, re.M), name
+
+
+def test_library_is_sm100a():
+    from paper_1512_01641_b200 import _native
+
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_product_path_fails_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1512_01641_b200 import _native
+
+    with pytest.raises(_native.NativeUnavailable):
+        A.build_score_matrix(H.toy_model(), H.toy_lexicon(), ["domo"], ["house"])
+    with pytest.raises(_native.NativeUnavailable):
+        A.nw_align(np.eye(3), A.MiningConfig())
+
+
+def test_config_and_engine_validation():
+    with pytest.raises(ValueError):
+        A.MiningConfig(threshold=1.5)
+    with pytest.raises(ValueError):
+        A.MiningConfig(gap_penalty=-0.1)
+    with pytest.raises(ValueError):
+        A.MiningConfig(workers=0)
+    with pytest.raises(ValueError, match="unknown engine"):
+        A.mine_corpus(None, None, [], A.MiningConfig(), engine="bogus")
+    with pytest.raises(NotImplementedError):
+        A.mine_corpus(None, None, [], A.MiningConfig(), engine="astar_constrained")
+    with pytest.raises(ValueError):
+        A.nw_align(np.zeros((0, 3)), A.MiningConfig())
+    with pytest.raises(ValueError):
+        A.nw_align(np.array([[np.nan]]), A.MiningConfig())
+
+
+def test_filter_by_threshold_kat():
+    sim = np.array([[0.9, 0.0, 0.0], [0.0, 0.4, 0.0], [0.0, 0.0, 0.7]])
+    al = A.Alignment(steps=(A.Match(0, 0), A.Match(1, 1), A.Match(2, 2)), score=0.0)
+    assert A.filter_by_threshold(sim, al, 0.5) == [(0.9, 0, 0), (0.7, 2, 2)]
+
+
+def test_steps_from_codes():
+    steps = A._steps_from_codes(np.array([0, 1, 2, 0, 2], dtype=np.uint8))
+    assert steps == (A.Match(0, 0), A.GapSource(1), A.GapTarget(1), A.Match(2, 2), A.GapTarget(3))
+
+
+def test_shard_bounds_cover_in_order():
+    w = np.array([5, 1, 1, 8, 2, 2, 2, 9, 1], dtype=np.int64)
+    for parts in (1, 2, 3, 4, 8, 20):
+        b = A._shard_bounds(w, parts)
+        assert b[0][0] == 0 and b[-1][1] == len(w)
+        assert all(x[1] == y[0] for x, y in zip(b, b[1:]))
+        assert len(b) <= parts
