@@ -10,9 +10,10 @@
 //     colmask[d] = 64-bit set of target sentences containing d.
 //  D  warp per source sentence i, lanes = 32 occurrences at a time, in
 //     order.  Lane k walks its token's dictionary row (p > 0 entries
-//     only, CSR) against the hash: anyhit_k = OR of colmask over its
-//     translations; the top three (colmask, p) by p are kept; reachcol[d]
-//     |= bit i (reachable_targets, classifier.py:54-59).  A 32x32 bit
+//     only, CSR) against the hash (behind a Bloom prefilter): anyhit_k =
+//     OR of colmask over its translations; up to six (colmask, p) are kept
+//     sorted by p; reachcol[d] |= bit i (reachable_targets,
+//     classifier.py:54-59).  A 32x32 bit
 //     transpose turns the anyhit rows into, for lane j, the set of
 //     occurrences with a translation in target sentence j; popc adds
 //     `covered`, and walking the set bits in ascending order adds the
@@ -24,7 +25,9 @@
 //     reachcol rows gives covered_target(i, j) by popc
 //     (classifier.py:88-92), multiplicities included.
 //  F  all threads, one cell each (flattened, full lanes): six features ->
-//     margin -> logistic (terms.cuh), one coalesced store per cell.
+//     margin -> logistic (terms.cuh), one coalesced store per cell.  The
+//     running sums of D are parked in the cell's own output slot (L2) and
+//     overwritten here.
 //
 // If the chunk's distinct target tokens exceed the hash capacity the
 // target side is processed in halves (same results, more passes).
@@ -54,23 +57,25 @@ struct PairArgs {
   int cap_t;                // target occurrences per chunk
 };
 
+constexpr int kCand = 6;        // in-chunk translations kept per occurrence (more -> re-walk)
+constexpr int kCandStride = 7;  // padded record stride (u64 words), spreads banks
+constexpr int kBloomBits = 14;  // 16384-bit prefilter in front of the hash
+
 struct PairSmem {
   uint64_t *exp_tab;   // [256]
   uint64_t *colmask;   // [cap_u]
   uint64_t *reachcol;  // [cap_u]
-  double *sum;         // [64][64]
   uint64_t *r_any;     // [warps][32]
-  uint64_t *r_ma;      // [warps][32]
-  uint64_t *r_mb;      // [warps][32]
-  double *r_pa, *r_pb, *r_pc;  // [warps][32]
+  uint64_t *r_m;       // [warps][32][kCandStride] candidate colmasks, p descending
+  double *r_p;         // [warps][32][kCandStride] candidate probabilities
   int64_t *src_off, *tgt_off;  // [64]
-  double *tgt_rct;     // [64] RN(1/Ct)
+  uint32_t *bloom;     // [2^kBloomBits / 32]
   int32_t *keys;       // [slots]
   int32_t *src_len, *src_uniq, *src_chars;  // [64]
   int32_t *tgt_len, *tgt_uniq, *tgt_chars;  // [64]
   int32_t *tgt_occ0;   // [65] chunk-local occurrence offsets
   int32_t *r_tok;      // [warps][32]
-  int32_t *misc;       // [8]
+  int32_t *misc;       // [8]: 0 distinct count, 1 chunk end, 2 D work counter, 3 C work counter
   int16_t *dense;      // [slots]
   int16_t *tgt_d;      // [cap_t]
   uint8_t *cov, *covt, *shr;  // [64][64]
@@ -92,16 +97,12 @@ __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_
   t.exp_tab = (uint64_t *)take(256 * 8, 16);
   t.colmask = (uint64_t *)take((size_t)cap_u * 8, 16);
   t.reachcol = (uint64_t *)take((size_t)cap_u * 8, 16);
-  t.sum = (double *)take(64 * 64 * 8, 16);
   t.r_any = (uint64_t *)take(W * 8, 16);
-  t.r_ma = (uint64_t *)take(W * 8, 16);
-  t.r_mb = (uint64_t *)take(W * 8, 16);
-  t.r_pa = (double *)take(W * 8, 16);
-  t.r_pb = (double *)take(W * 8, 16);
-  t.r_pc = (double *)take(W * 8, 16);
+  t.r_m = (uint64_t *)take(W * kCandStride * 8, 16);
+  t.r_p = (double *)take(W * kCandStride * 8, 16);
   t.src_off = (int64_t *)take(64 * 8, 16);
   t.tgt_off = (int64_t *)take(64 * 8, 16);
-  t.tgt_rct = (double *)take(64 * 8, 16);
+  t.bloom = (uint32_t *)take(((size_t)1 << kBloomBits) / 8, 16);
   t.keys = (int32_t *)take(slots * 4, 16);
   t.src_len = (int32_t *)take(64 * 4, 4);
   t.src_uniq = (int32_t *)take(64 * 4, 4);
@@ -134,6 +135,10 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
   return x;
 }
 
+__device__ __forceinline__ uint32_t bloom_bit(int32_t key) {
+  return ((uint32_t)key * 0x85EBCA6Bu) >> (32 - kBloomBits);
+}
+
 __device__ __forceinline__ int pk_find(const int32_t *keys, const int16_t *dense, int bits, int32_t key) {
   const uint32_t mask = (1u << bits) - 1u;
   uint32_t slot = hash_slot(key, 32 - bits);
@@ -143,6 +148,14 @@ __device__ __forceinline__ int pk_find(const int32_t *keys, const int16_t *dense
     if (k == -1) return -1;
     slot = (slot + 1u) & mask;
   }
+}
+
+// lookup behind the Bloom prefilter (most dictionary translations are absent)
+__device__ __forceinline__ int pk_find_f(const uint32_t *bloom, const int32_t *keys, const int16_t *dense, int bits,
+                                         int32_t key) {
+  const uint32_t b = bloom_bit(key);
+  if (!((bloom[b >> 5] >> (b & 31)) & 1u)) return -1;
+  return pk_find(keys, dense, bits, key);
 }
 
 __device__ __forceinline__ void pk_insert(int32_t *keys, int bits, int32_t key) {
@@ -180,6 +193,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
   const double *__restrict__ dprob = A.d.prob;
   const int64_t n_rows = A.d.n_rows;
   const int hslots = 1 << hbits;
+  double *__restrict__ out = A.sim + A.b.pair_sim_off[p];  // also the running-sum scratch
 
   // ---- 0: tables and sentence metadata
   for (int k = tid; k < 256; k += kPairThreads) S.exp_tab[k] = kExpTableDev[k];
@@ -193,9 +207,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
     S.tgt_off[j] = A.b.sent_tok_off[t_first + j];
     S.tgt_len[j] = A.b.sent_len[t_first + j];
     S.tgt_uniq[j] = A.b.sent_uniq[t_first + j];
-    const int ct = A.b.sent_chars[t_first + j];
-    S.tgt_chars[j] = ct;
-    S.tgt_rct[j] = fdiv(1.0, (double)ct);
+    S.tgt_chars[j] = A.b.sent_chars[t_first + j];
   }
   __syncthreads();
   {  // the rule of pair_is_small: every sentence <= kPairMaxLen tokens
@@ -216,9 +228,8 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
           const int y = __shfl_up_sync(kFull, x, o);
           if (lane >= o) x += y;
         }
-        const bool fits = j < M && run + x <= A.cap_t;
-        const unsigned ok = __ballot_sync(kFull, fits);
-        const int cnt = __popc(ok);  // prefix property: fitting lanes are a prefix
+        const unsigned ok = __ballot_sync(kFull, j < M && run + x <= A.cap_t);
+        const int cnt = __popc(ok);  // lengths >= 0: the fitting lanes are a prefix
         end = base + cnt;
         if (cnt < 32) break;
         run += __shfl_sync(kFull, x, 31);
@@ -229,8 +240,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
     int jc1 = S.misc[1];
     while (true) {
       const int nj = jc1 - jc0;
-      // occurrence offsets of the chunk
-      if (warp == 0) {
+      if (warp == 0) {  // chunk-local occurrence offsets
         int run = 0;
         for (int base = 0; base < nj; base += 32) {
           const int jj = base + lane;
@@ -247,15 +257,23 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
         if (lane == 0) {
           S.tgt_occ0[nj] = run;
           S.misc[0] = 0;
+          S.misc[2] = 0;
+          S.misc[3] = 0;
         }
       }
       for (int k = tid; k < hslots; k += kPairThreads) S.keys[k] = -1;
+      for (int k = tid; k < (1 << kBloomBits) / 32; k += kPairThreads) S.bloom[k] = 0u;
       __syncthreads();
-      // ---- A1: insert
+      // ---- A1: insert the chunk's target tokens (+ prefilter bits)
       for (int jj = warp; jj < nj; jj += kPairWarps) {
         const int64_t off = S.tgt_off[jc0 + jj];
         const int L = S.tgt_len[jc0 + jj];
-        for (int k = lane; k < L; k += 32) pk_insert(S.keys, hbits, tokens[off + k]);
+        for (int k = lane; k < L; k += 32) {
+          const int32_t t = tokens[off + k];
+          pk_insert(S.keys, hbits, t);
+          const uint32_t b = bloom_bit(t);
+          atomicOr(&S.bloom[b >> 5], 1u << (b & 31));
+        }
       }
       __syncthreads();
       // ---- A2: dense ids
@@ -287,14 +305,19 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
       }
     }
     __syncthreads();
-    // ---- D: source side, warp per source sentence
+    // ---- D: source side, warps take sentences dynamically
     {
-      uint64_t *ra = S.r_any + warp * 32, *rma = S.r_ma + warp * 32, *rmb = S.r_mb + warp * 32;
-      double *rpa = S.r_pa + warp * 32, *rpb = S.r_pb + warp * 32, *rpc = S.r_pc + warp * 32;
+      uint64_t *ra = S.r_any + warp * 32;
+      uint64_t *rm = S.r_m + warp * 32 * kCandStride;
+      double *rp = S.r_p + warp * 32 * kCandStride;
       int32_t *rtok = S.r_tok + warp * 32;
       uint8_t *rn = S.r_n + warp * 32;
       const int jlo = lane, jhi = lane + 32;
-      for (int i = warp; i < N; i += kPairWarps) {
+      while (true) {
+        int i = 0;
+        if (lane == 0) i = atomicAdd(&S.misc[2], 1);
+        i = __shfl_sync(kFull, i, 0);
+        if (i >= N) break;
         const int64_t off = S.src_off[i];
         const int L = S.src_len[i];
         const unsigned long long ibit = 1ull << i;
@@ -305,7 +328,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
           const bool valid = k < L;
           const int32_t s = valid ? tokens[off + k] : -1;
           // shared tokens: first occurrence of a source token that is a chunk token
-          const int ds = valid ? pk_find(S.keys, S.dense, hbits, s) : -1;
+          const int ds = valid ? pk_find_f(S.bloom, S.keys, S.dense, hbits, s) : -1;
           const unsigned peers = __match_any_sync(kFull, s);
           bool first = (__ffs(peers) - 1) == lane;
           if (ds >= 0 && first && seg > 0)
@@ -315,36 +338,35 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
                 break;
               }
           const uint64_t shm = (ds >= 0 && first) ? S.colmask[ds] : 0ull;
-          // dictionary row against the chunk: anyhit + top-3 (mask, p) by p
-          uint64_t any = 0ull, ma = 0ull, mb = 0ull;
-          double pa = 0.0, pb = 0.0, pc = 0.0;
+          // dictionary row against the chunk: anyhit + candidates, p descending
+          uint64_t any = 0ull;
           int n = 0;
+          uint64_t *mym = rm + lane * kCandStride;
+          double *myp = rp + lane * kCandStride;
           if (valid && s >= 0 && s < n_rows) {
             const int64_t e0 = row_ptr[s], e1 = row_ptr[s + 1];
             for (int64_t e = e0; e < e1; ++e) {
-              const int d = pk_find(S.keys, S.dense, hbits, dtgt[e]);
+              const int d = pk_find_f(S.bloom, S.keys, S.dense, hbits, dtgt[e]);
               if (d < 0) continue;
               const uint64_t m = S.colmask[d];
               const double pr = dprob[e];
               any |= m;
               atomicOr((unsigned long long *)&S.reachcol[d], ibit);
-              ++n;
-              if (pr > pa) {
-                pc = pb; pb = pa; mb = ma; pa = pr; ma = m;
-              } else if (pr > pb) {
-                pc = pb; pb = pr; mb = m;
-              } else if (pr > pc) {
-                pc = pr;
+              if (n < kCand) {  // insertion, p descending
+                int c = n;
+                while (c > 0 && myp[c - 1] < pr) {
+                  myp[c] = myp[c - 1];
+                  mym[c] = mym[c - 1];
+                  --c;
+                }
+                myp[c] = pr;
+                mym[c] = m;
               }
+              ++n;
             }
           }
           ra[lane] = any;
-          rma[lane] = ma;
-          rmb[lane] = mb;
-          rpa[lane] = pa;
-          rpb[lane] = pb;
-          rpc[lane] = pc;
-          rn[lane] = (uint8_t)(n > 3 ? 255 : n);
+          rn[lane] = (uint8_t)(n > kCand ? 255 : n);
           rtok[lane] = s;
           __syncwarp();
           if (__any_sync(kFull, shm != 0ull)) {
@@ -365,19 +387,20 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
               const int kk = __ffs(h) - 1;
               h &= h - 1u;
               const int c = rn[kk];
-              double best;
-              if (c == 1) {
-                best = rpa[kk];
-              } else if (c == 2) {
-                best = ((rma[kk] >> j) & 1ull) ? rpa[kk] : rpb[kk];
-              } else if (c == 3) {
-                best = ((rma[kk] >> j) & 1ull) ? rpa[kk] : ((rmb[kk] >> j) & 1ull) ? rpb[kk] : rpc[kk];
-              } else {  // more than three translations in the chunk: walk the row again
-                best = 0.0;
+              double best = 0.0;
+              if (c != 255) {  // first candidate (p descending) present in sentence j
+                const uint64_t *cm = rm + kk * kCandStride;
+                const double *cp = rp + kk * kCandStride;
+                for (int x = 0; x < c; ++x)
+                  if ((cm[x] >> j) & 1ull) {
+                    best = cp[x];
+                    break;
+                  }
+              } else {  // more than kCand translations in the chunk: walk the row again
                 const int32_t sk = rtok[kk];
                 const int64_t e1 = row_ptr[sk + 1];
                 for (int64_t e = row_ptr[sk]; e < e1; ++e) {
-                  const int d = pk_find(S.keys, S.dense, hbits, dtgt[e]);
+                  const int d = pk_find_f(S.bloom, S.keys, S.dense, hbits, dtgt[e]);
                   if (d >= 0 && ((S.colmask[d] >> j) & 1ull) && dprob[e] > best) best = dprob[e];
                 }
               }
@@ -389,22 +412,24 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
           __syncwarp();
         }
         if (jlo < nj) {
-          const int c = i * kCellStride + jc0 + jlo;
-          S.cov[c] = (uint8_t)cov_lo;
-          S.sum[c] = sum_lo;
-          S.shr[c] = (uint8_t)sh_lo;
+          S.cov[i * kCellStride + jc0 + jlo] = (uint8_t)cov_lo;
+          S.shr[i * kCellStride + jc0 + jlo] = (uint8_t)sh_lo;
+          out[i * M + jc0 + jlo] = sum_lo;
         }
         if (jhi < nj) {
-          const int c = i * kCellStride + jc0 + jhi;
-          S.cov[c] = (uint8_t)cov_hi;
-          S.sum[c] = sum_hi;
-          S.shr[c] = (uint8_t)sh_hi;
+          S.cov[i * kCellStride + jc0 + jhi] = (uint8_t)cov_hi;
+          S.shr[i * kCellStride + jc0 + jhi] = (uint8_t)sh_hi;
+          out[i * M + jc0 + jhi] = sum_hi;
         }
       }
     }
     __syncthreads();
-    // ---- C: covered_target, warp per target sentence, lanes over occurrences
-    for (int jj = warp; jj < nj; jj += kPairWarps) {
+    // ---- C: covered_target, warps take target sentences, lanes over occurrences
+    while (true) {
+      int jj = 0;
+      if (lane == 0) jj = atomicAdd(&S.misc[3], 1);
+      jj = __shfl_sync(kFull, jj, 0);
+      if (jj >= nj) break;
       const int q0 = S.tgt_occ0[jj];
       const int L = S.tgt_len[jc0 + jj];
       int c_lo = 0, c_hi = 0;
@@ -420,14 +445,13 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
     __syncthreads();
   }
 
-  // ---- F: finalize, one cell per thread, coalesced stores
-  double *__restrict__ out = A.sim + A.b.pair_sim_off[p];
+  // ---- F: finalize, one cell per thread, coalesced loads/stores
   const int cells = N * M;
   for (int c = tid; c < cells; c += kPairThreads) {
     const int i = c / M, j = c - i * M;
     const int x = i * kCellStride + j;
     out[c] = cell_score_t(A.md, A.T, S.src_len[i], S.src_uniq[i], S.src_chars[i], S.tgt_len[j], S.tgt_uniq[j],
-                          S.tgt_chars[j], S.cov[x], S.sum[x], S.covt[x], S.shr[x], S.exp_tab);
+                          S.tgt_chars[j], S.cov[x], out[c], S.covt[x], S.shr[x], S.exp_tab);
   }
 }
 
