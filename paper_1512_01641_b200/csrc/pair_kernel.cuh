@@ -57,29 +57,27 @@ struct PairArgs {
   int cap_t;                // target occurrences per chunk
 };
 
-constexpr int kCand = 6;        // in-chunk translations kept per occurrence (more -> re-walk)
-constexpr int kCandStride = 7;  // padded record stride (u64 words), spreads banks
+constexpr int kSegItems = 64;   // dictionary entries examined per warp segment
 constexpr int kBloomBits = 14;  // 16384-bit prefilter in front of the hash
 
 struct PairSmem {
   uint64_t *exp_tab;   // [256]
   uint64_t *colmask;   // [cap_u]
   uint64_t *reachcol;  // [cap_u]
-  uint64_t *r_any;     // [warps][32]
-  uint64_t *r_m;       // [warps][32][kCandStride] candidate colmasks, p descending
-  double *r_p;         // [warps][32][kCandStride] candidate probabilities
+  uint64_t *o_any;     // [warps][32] per occurrence: OR of its translations' colmasks
+  uint64_t *c_m;       // [warps][kSegItems] in-chunk translations: colmask
+  double *c_p;         // [warps][kSegItems]                        probability
   int64_t *src_off, *tgt_off;  // [64]
   uint32_t *bloom;     // [2^kBloomBits / 32]
   int32_t *keys;       // [slots]
   int32_t *src_len, *src_uniq, *src_chars;  // [64]
   int32_t *tgt_len, *tgt_uniq, *tgt_chars;  // [64]
   int32_t *tgt_occ0;   // [65] chunk-local occurrence offsets
-  int32_t *r_tok;      // [warps][32]
+  int32_t *o_n;        // [warps][32] translations found per occurrence
   int32_t *misc;       // [8]: 0 distinct count, 1 chunk end, 2 D work counter, 3 C work counter
   int16_t *dense;      // [slots]
   int16_t *tgt_d;      // [cap_t]
   uint8_t *cov, *covt, *shr;  // [64][64]
-  uint8_t *r_n;        // [warps][32]
 };
 
 __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_u, int hash_bits, int cap_t,
@@ -97,9 +95,9 @@ __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_
   t.exp_tab = (uint64_t *)take(256 * 8, 16);
   t.colmask = (uint64_t *)take((size_t)cap_u * 8, 16);
   t.reachcol = (uint64_t *)take((size_t)cap_u * 8, 16);
-  t.r_any = (uint64_t *)take(W * 8, 16);
-  t.r_m = (uint64_t *)take(W * kCandStride * 8, 16);
-  t.r_p = (double *)take(W * kCandStride * 8, 16);
+  t.o_any = (uint64_t *)take(W * 8, 16);
+  t.c_m = (uint64_t *)take((size_t)kPairWarps * kSegItems * 8, 16);
+  t.c_p = (double *)take((size_t)kPairWarps * kSegItems * 8, 16);
   t.src_off = (int64_t *)take(64 * 8, 16);
   t.tgt_off = (int64_t *)take(64 * 8, 16);
   t.bloom = (uint32_t *)take(((size_t)1 << kBloomBits) / 8, 16);
@@ -111,14 +109,13 @@ __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_
   t.tgt_uniq = (int32_t *)take(64 * 4, 4);
   t.tgt_chars = (int32_t *)take(64 * 4, 4);
   t.tgt_occ0 = (int32_t *)take(65 * 4, 4);
-  t.r_tok = (int32_t *)take(W * 4, 4);
+  t.o_n = (int32_t *)take(W * 4, 4);
   t.misc = (int32_t *)take(8 * 4, 4);
   t.dense = (int16_t *)take(slots * 2, 4);
   t.tgt_d = (int16_t *)take((size_t)cap_t * 2, 4);
   t.cov = (uint8_t *)take(64 * 64, 4);
   t.covt = (uint8_t *)take(64 * 64, 4);
   t.shr = (uint8_t *)take(64 * 64, 4);
-  t.r_n = (uint8_t *)take(W, 4);
   if (s) *s = t;
   return (o + 15) / 16 * 16;
 }
@@ -307,12 +304,12 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
     __syncthreads();
     // ---- D: source side, warps take sentences dynamically
     {
-      uint64_t *ra = S.r_any + warp * 32;
-      uint64_t *rm = S.r_m + warp * 32 * kCandStride;
-      double *rp = S.r_p + warp * 32 * kCandStride;
-      int32_t *rtok = S.r_tok + warp * 32;
-      uint8_t *rn = S.r_n + warp * 32;
+      uint64_t *oany = S.o_any + warp * 32;
+      int32_t *on = S.o_n + warp * 32;
+      uint64_t *cm = S.c_m + warp * kSegItems;
+      double *cp = S.c_p + warp * kSegItems;
       const int jlo = lane, jhi = lane + 32;
+      const unsigned lt_mask = (1u << lane) - 1u;
       while (true) {
         int i = 0;
         if (lane == 0) i = atomicAdd(&S.misc[2], 1);
@@ -323,13 +320,32 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
         const unsigned long long ibit = 1ull << i;
         int cov_lo = 0, cov_hi = 0, sh_lo = 0, sh_hi = 0;
         double sum_lo = 0.0, sum_hi = 0.0;
-        for (int seg = 0; seg < L; seg += 32) {
+        for (int seg = 0; seg < L;) {
           const int k = seg + lane;
           const bool valid = k < L;
           const int32_t s = valid ? tokens[off + k] : -1;
+          int64_t e0 = 0;
+          int rl = 0;
+          if (valid && s >= 0 && s < n_rows) {
+            e0 = row_ptr[s];
+            rl = (int)(row_ptr[s + 1] - e0);
+          }
+          // segment: the longest prefix of occurrences whose rows total
+          // <= kSegItems entries (at least one occurrence)
+          int x = rl;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+          }
+          const unsigned fitm = __ballot_sync(kFull, valid && (x <= kSegItems || lane == 0));
+          const int cnt = __popc(fitm);
+          const bool in_seg = lane < cnt;
+          const int items = min(kSegItems, __shfl_sync(kFull, x, cnt - 1));
+          const int ofs = x - rl;  // exclusive prefix: first item of this occurrence
           // shared tokens: first occurrence of a source token that is a chunk token
-          const int ds = valid ? pk_find_f(S.bloom, S.keys, S.dense, hbits, s) : -1;
-          const unsigned peers = __match_any_sync(kFull, s);
+          const int ds = in_seg ? pk_find_f(S.bloom, S.keys, S.dense, hbits, s) : -1;
+          const unsigned peers = __match_any_sync(kFull, in_seg ? s : -1);
           bool first = (__ffs(peers) - 1) == lane;
           if (ds >= 0 && first && seg > 0)
             for (int kk = 0; kk < seg; ++kk)
@@ -338,78 +354,105 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
                 break;
               }
           const uint64_t shm = (ds >= 0 && first) ? S.colmask[ds] : 0ull;
-          // dictionary row against the chunk: anyhit + candidates, p descending
-          uint64_t any = 0ull;
-          int n = 0;
-          uint64_t *mym = rm + lane * kCandStride;
-          double *myp = rp + lane * kCandStride;
-          if (valid && s >= 0 && s < n_rows) {
-            const int64_t e0 = row_ptr[s], e1 = row_ptr[s + 1];
-            for (int64_t e = e0; e < e1; ++e) {
-              const int d = pk_find_f(S.bloom, S.keys, S.dense, hbits, dtgt[e]);
-              if (d < 0) continue;
-              const uint64_t m = S.colmask[d];
-              const double pr = dprob[e];
-              any |= m;
-              atomicOr((unsigned long long *)&S.reachcol[d], ibit);
-              if (n < kCand) {  // insertion, p descending
-                int c = n;
-                while (c > 0 && myp[c - 1] < pr) {
-                  myp[c] = myp[c - 1];
-                  mym[c] = mym[c - 1];
-                  --c;
-                }
-                myp[c] = pr;
-                mym[c] = m;
-              }
-              ++n;
-            }
-          }
-          ra[lane] = any;
-          rn[lane] = (uint8_t)(n > kCand ? 255 : n);
-          rtok[lane] = s;
-          __syncwarp();
           if (__any_sync(kFull, shm != 0ull)) {
             sh_lo += __popc(transpose32((uint32_t)shm, lane));
             sh_hi += __popc(transpose32((uint32_t)(shm >> 32), lane));
           }
-          uint32_t hl = transpose32((uint32_t)any, lane);
-          uint32_t hh = transpose32((uint32_t)(any >> 32), lane);
-          cov_lo += __popc(hl);
-          cov_hi += __popc(hh);
-          // ordered sums: ascending occurrence index = reference order
-#pragma unroll 1
-          for (int half = 0; half < 2; ++half) {
-            uint32_t h = half ? hh : hl;
-            const int j = half ? jhi : jlo;
-            double acc = half ? sum_hi : sum_lo;
-            while (h) {
-              const int kk = __ffs(h) - 1;
-              h &= h - 1u;
-              const int c = rn[kk];
-              double best = 0.0;
-              if (c != 255) {  // first candidate (p descending) present in sentence j
-                const uint64_t *cm = rm + kk * kCandStride;
-                const double *cp = rp + kk * kCandStride;
-                for (int x = 0; x < c; ++x)
-                  if ((cm[x] >> j) & 1ull) {
-                    best = cp[x];
-                    break;
-                  }
-              } else {  // more than kCand translations in the chunk: walk the row again
-                const int32_t sk = rtok[kk];
-                const int64_t e1 = row_ptr[sk + 1];
-                for (int64_t e = row_ptr[sk]; e < e1; ++e) {
-                  const int d = pk_find_f(S.bloom, S.keys, S.dense, hbits, dtgt[e]);
-                  if (d >= 0 && ((S.colmask[d] >> j) & 1ull) && dprob[e] > best) best = dprob[e];
-                }
+          const int rl0 = __shfl_sync(kFull, rl, 0);
+          if (rl0 > kSegItems) {
+            // a lone occurrence whose row exceeds the segment (cnt == 1): the
+            // whole warp walks the row and reduces the per-sentence maxima
+            const int64_t r0 = __shfl_sync(kFull, e0, 0);
+            uint64_t a = 0ull;
+            double bl = 0.0, bh = 0.0;
+            for (int base = 0; base < rl0; base += 32) {
+              const int it = base + lane;
+              int d = -1;
+              if (it < rl0) d = pk_find_f(S.bloom, S.keys, S.dense, hbits, dtgt[r0 + it]);
+              const uint64_t m = d >= 0 ? S.colmask[d] : 0ull;
+              const double pr = d >= 0 ? dprob[r0 + it] : 0.0;
+              if (d >= 0) atomicOr((unsigned long long *)&S.reachcol[d], ibit);
+              unsigned bal = __ballot_sync(kFull, d >= 0);
+              while (bal) {
+                const int src = __ffs(bal) - 1;
+                bal &= bal - 1u;
+                const uint64_t mm = __shfl_sync(kFull, m, src);
+                const double pp = __shfl_sync(kFull, pr, src);
+                a |= mm;
+                if (((mm >> jlo) & 1ull) && pp > bl) bl = pp;
+                if (((mm >> jhi) & 1ull) && pp > bh) bh = pp;
               }
-              acc = fadd(acc, best);
             }
-            if (half) sum_hi = acc;
-            else sum_lo = acc;
+            if (a != 0ull) {
+              sum_lo = fadd(sum_lo, bl);
+              sum_hi = fadd(sum_hi, bh);
+              cov_lo += (int)((a >> jlo) & 1ull);
+              cov_hi += (int)((a >> jhi) & 1ull);
+            }
+            seg += 1;
+            continue;
+          }
+          oany[lane] = 0ull;
+          on[lane] = 0;
+          __syncwarp();
+          // all dictionary entries of the segment, 32 at a time, in order
+          int ncand = 0;
+          for (int base = 0; base < items; base += 32) {
+            const int it = base + lane;
+            const bool live = it < items;
+            int owner = 0;  // last segment lane whose first item <= it
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+              const int cand = owner + step;
+              const int v = __shfl_sync(kFull, ofs, cand & 31);
+              if (cand < cnt && v <= it) owner = cand;
+            }
+            const int64_t oe0 = __shfl_sync(kFull, e0, owner);
+            const int oofs = __shfl_sync(kFull, ofs, owner);
+            int d = -1;
+            int64_t e = 0;
+            if (live) {
+              e = oe0 + (it - oofs);
+              d = pk_find_f(S.bloom, S.keys, S.dense, hbits, dtgt[e]);
+            }
+            const bool pres = d >= 0;
+            const unsigned bal = __ballot_sync(kFull, pres);
+            if (pres) {
+              const uint64_t m = S.colmask[d];
+              const int pos = ncand + __popc(bal & lt_mask);
+              cm[pos] = m;
+              cp[pos] = dprob[e];
+              atomicOr((unsigned long long *)&S.reachcol[d], ibit);
+              atomicOr((unsigned long long *)&oany[owner], m);
+              atomicAdd(&on[owner], 1);
+            }
+            ncand += __popc(bal);
           }
           __syncwarp();
+          // occurrence-major, in order: max p over the occurrence's
+          // translations present in sentence j, added to the running sum
+          // (adding +0.0 when absent leaves the non-negative sum unchanged)
+          int cs = 0;
+          for (int kk = 0; kk < cnt; ++kk) {
+            const uint64_t a = oany[kk];
+            const int n = on[kk];
+            if (a != 0ull) {
+              double bl = 0.0, bh = 0.0;
+              for (int c = cs; c < cs + n; ++c) {
+                const uint64_t m = cm[c];
+                const double pr = cp[c];
+                if (((m >> jlo) & 1ull) && pr > bl) bl = pr;
+                if (((m >> jhi) & 1ull) && pr > bh) bh = pr;
+              }
+              sum_lo = fadd(sum_lo, bl);
+              sum_hi = fadd(sum_hi, bh);
+              cov_lo += (int)((a >> jlo) & 1ull);
+              cov_hi += (int)((a >> jhi) & 1ull);
+            }
+            cs += n;
+          }
+          __syncwarp();
+          seg += cnt;
         }
         if (jlo < nj) {
           S.cov[i * kCellStride + jc0 + jlo] = (uint8_t)cov_lo;

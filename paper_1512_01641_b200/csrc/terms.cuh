@@ -102,16 +102,16 @@ __device__ __forceinline__ double cell_score_t(const Model &md, const TermTables
   d = fadd(d, t4);
   d = fadd(d, t5);
   const double z = fadd(fmul(md.a, d), md.b);
+  // one exp and one division for both branches of score_from_margin:
+  // z >= 0: exp(-z) / (1 + exp(-z)); z < 0: 1 / (1 + exp(z)); NaN takes
+  // the z < 0 branch and its cut-off, as in Python
+  const bool pos = z >= 0.0;
   double p;
-  if (z >= 0.0) {
-    if (z < 700.0) {
-      const double e = glibc_exp(-z, tab);
-      p = fdiv(e, fadd(1.0, e));
-    } else {
-      p = 0.0;
-    }
+  if (pos ? (z < 700.0) : (z > -700.0)) {
+    const double e = glibc_exp(pos ? -z : z, tab);
+    p = fdiv(pos ? e : 1.0, fadd(1.0, e));
   } else {
-    p = (z > -700.0) ? fdiv(1.0, fadd(1.0, glibc_exp(z, tab))) : 1.0;
+    p = pos ? 0.0 : 1.0;
   }
   if (0.0 > p) p = 0.0;
   if (1.0 < p) p = 1.0;

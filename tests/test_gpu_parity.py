@@ -269,7 +269,7 @@ def test_chunked_targets_and_long_sentences():
     trans = {w: {f"v{(k * 7 + j) % 3000}": float(round(rng.uniform(0.01, 1.0), 6)) for j in range(rng.integers(1, 9))}
              for k, w in enumerate(words[:2000])}
     # one long row (> inline candidate capacity) and a zero / negative entry
-    trans["w1"] = {f"v{k}": 0.01 * (k + 1) for k in range(40)}
+    trans["w1"] = {f"v{k}": 0.001 * (k + 1) for k in range(100)}  # longer than a segment
     trans["w2"]["v5"] = 0.0
     trans["w3"]["v6"] = -0.5
     lex = Lexicon(trans)
