@@ -287,6 +287,7 @@ int bimine_score_batch(const bimine_dict *dict, const double *model, const bimin
     A.cap_t = 2048;
     const size_t smem = pair_smem_layout(nullptr, A.cap_u, A.hash_bits, A.cap_t, nullptr);
     BIMINE_CUDA(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    BIMINE_CUDA(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     pair_kernel<<<(unsigned)b->n_pairs, kPairThreads, smem, st>>>(A);
     BIMINE_CUDA(cudaGetLastError());
   }

@@ -174,7 +174,7 @@ __host__ __device__ inline bool pair_is_small(int n, int m, int max_len) {
   return n <= kPairMax && m <= kPairMax && max_len <= kPairMaxLen;
 }
 
-__global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A) {
+__global__ void __launch_bounds__(kPairThreads, 3) pair_kernel(const PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t p = A.pair_ids ? A.pair_ids[blockIdx.x] : (int64_t)blockIdx.x;
   const int N = A.b.pair_n[p], M = A.b.pair_m[p];
@@ -432,22 +432,27 @@ __global__ void __launch_bounds__(kPairThreads, 2) pair_kernel(const PairArgs A)
           // occurrence-major, in order: max p over the occurrence's
           // translations present in sentence j, added to the running sum
           // (adding +0.0 when absent leaves the non-negative sum unchanged)
+          const uint32_t lbit = 1u << lane;  // bit of target jlo in the low word, jhi in the high word
           int cs = 0;
           for (int kk = 0; kk < cnt; ++kk) {
             const uint64_t a = oany[kk];
             const int n = on[kk];
             if (a != 0ull) {
-              double bl = 0.0, bh = 0.0;
-              for (int c = cs; c < cs + n; ++c) {
+              double bl, bh;
+              const uint64_t m0 = cm[cs];
+              const double p0 = cp[cs];
+              bl = ((uint32_t)m0 & lbit) ? p0 : 0.0;
+              bh = ((uint32_t)(m0 >> 32) & lbit) ? p0 : 0.0;
+              for (int c = cs + 1; c < cs + n; ++c) {
                 const uint64_t m = cm[c];
                 const double pr = cp[c];
-                if (((m >> jlo) & 1ull) && pr > bl) bl = pr;
-                if (((m >> jhi) & 1ull) && pr > bh) bh = pr;
+                if (((uint32_t)m & lbit) && pr > bl) bl = pr;
+                if (((uint32_t)(m >> 32) & lbit) && pr > bh) bh = pr;
               }
               sum_lo = fadd(sum_lo, bl);
               sum_hi = fadd(sum_hi, bh);
-              cov_lo += (int)((a >> jlo) & 1ull);
-              cov_hi += (int)((a >> jhi) & 1ull);
+              cov_lo += ((uint32_t)a & lbit) ? 1 : 0;
+              cov_hi += ((uint32_t)(a >> 32) & lbit) ? 1 : 0;
             }
             cs += n;
           }
