@@ -125,22 +125,28 @@ int bimine_dict_view_get(const bimine_dict *dict, bimine_dict_view *view_dev);
 int64_t bimine_dict_entries(const bimine_dict *dict);
 
 /* ---- batch plan -------------------------------------------------------
- * Host-side summary of a packed batch (host pointers in batch_host):
- * maxima that size the kernels, and the pairs the per-pair score kernel
- * does not take (N > 64, M > 64 or a sentence > 255 tokens), which go to
- * the tiled kernel.  large_ids_host (capacity n_pairs) receives their
- * indices in ascending order; the caller uploads them and sets
- * plan->large_ids to the device copy before scoring. */
+ * Host-side summary of a packed batch (host pointers in batch_host): the
+ * maxima that size the kernels and the work the per-pair score kernel
+ * does not take in its one-CTA-per-pair launch:
+ *   tiles     pairs with N > 64 or M > 64: (pair, i0, j0) per 64x64 tile
+ *   long ids  pairs with a sentence of more than 255 tokens (tiled
+ *             fallback kernel)
+ * work_host (capacity work_cap int64) receives 3 * n_tiles tile triples
+ * followed by n_long pair ids; plan->work_len is the length needed
+ * (BIMINE_E_ARG if work_cap is smaller).  The caller uploads
+ * work_host[0 : work_len] and sets plan->work to the device copy. */
 typedef struct bimine_plan {
   int32_t max_n, max_m;        /* over all pairs                          */
   int32_t max_uniq, max_len;   /* over all sentences                      */
-  int64_t n_large;             /* pairs for the tiled kernel              */
-  const int64_t *large_ids;    /* device array [n_large] (set by caller)  */
-  int32_t large_max_n, large_max_m;
+  int64_t n_tiles;             /* 64x64 tiles of large pairs              */
+  int64_t n_long;              /* pairs for the fallback kernel           */
+  int32_t long_max_n, long_max_m;
+  int64_t work_len;            /* 3 * n_tiles + n_long                    */
+  const int64_t *work;         /* device copy of work_host (set by caller)*/
 } bimine_plan;
 
-int bimine_plan_batch(const bimine_batch *batch_host, int64_t *large_ids_host,
-                      bimine_plan *plan);
+int bimine_plan_batch(const bimine_batch *batch_host, int64_t *work_host,
+                      int64_t work_cap, bimine_plan *plan);
 
 /* ---- score matrix (align.py:102-129) -------------------------------
  * batch_dev: every pointer in the struct is a device pointer.

@@ -184,31 +184,46 @@ int64_t bimine_dict_entries(const bimine_dict *d) { return d ? d->n_entries : -1
 // score matrix
 // ------------------------------------------------------------------------
 
-int bimine_plan_batch(const bimine_batch *b, int64_t *large_ids, bimine_plan *plan) {
-  if (!b || !plan || (b->n_pairs > 0 && !large_ids)) return fail(BIMINE_E_ARG, "bimine_plan_batch: null argument");
+int bimine_plan_batch(const bimine_batch *b, int64_t *work, int64_t work_cap, bimine_plan *plan) {
+  if (!b || !plan || (work_cap > 0 && !work)) return fail(BIMINE_E_ARG, "bimine_plan_batch: null argument");
   bimine_plan P;
   memset(&P, 0, sizeof(P));
   for (int64_t s = 0; s < b->n_sentences; ++s) {
     P.max_uniq = std::max(P.max_uniq, b->sent_uniq[s]);
     P.max_len = std::max(P.max_len, b->sent_len[s]);
   }
+  std::vector<int64_t> longs;
+  int64_t t = 0;
   for (int64_t p = 0; p < b->n_pairs; ++p) {
     const int32_t n = b->pair_n[p], m = b->pair_m[p];
     if (n < 1 || m < 1) return fail(BIMINE_E_ARG, "bimine_plan_batch: empty document");
     P.max_n = std::max(P.max_n, n);
     P.max_m = std::max(P.max_m, m);
     int32_t ml = 0;
-    if (n <= kPairMax && m <= kPairMax) {
-      for (int32_t i = 0; i < n; ++i) ml = std::max(ml, b->sent_len[b->pair_src[p] + i]);
-      for (int32_t j = 0; j < m; ++j) ml = std::max(ml, b->sent_len[b->pair_tgt[p] + j]);
-    }
-    if (!pair_is_small(n, m, ml)) {
-      large_ids[P.n_large++] = p;
-      P.large_max_n = std::max(P.large_max_n, n);
-      P.large_max_m = std::max(P.large_max_m, m);
+    for (int32_t i = 0; i < n; ++i) ml = std::max(ml, b->sent_len[b->pair_src[p] + i]);
+    for (int32_t j = 0; j < m; ++j) ml = std::max(ml, b->sent_len[b->pair_tgt[p] + j]);
+    if (ml > kPairMaxLen) {
+      longs.push_back(p);
+      P.long_max_n = std::max(P.long_max_n, n);
+      P.long_max_m = std::max(P.long_max_m, m);
+    } else if (n > kPairMax || m > kPairMax) {
+      for (int32_t i0 = 0; i0 < n; i0 += kPairMax)
+        for (int32_t j0 = 0; j0 < m; j0 += kPairMax) {
+          if (3 * t + 3 <= work_cap) {
+            work[3 * t] = p;
+            work[3 * t + 1] = i0;
+            work[3 * t + 2] = j0;
+          }
+          ++t;
+        }
     }
   }
+  P.n_tiles = t;
+  P.n_long = (int64_t)longs.size();
+  P.work_len = 3 * P.n_tiles + P.n_long;
   *plan = P;
+  if (P.work_len > work_cap) return fail(BIMINE_E_ARG, "bimine_plan_batch: work_cap < plan->work_len");
+  for (int64_t k = 0; k < P.n_long; ++k) work[3 * P.n_tiles + k] = longs[k];
   return BIMINE_OK;
 }
 
@@ -266,13 +281,12 @@ int bimine_score_batch(const bimine_dict *dict, const double *model, const bimin
   if (plan->max_uniq > kMaxCapU || plan->max_len > kMaxCapT)
     return fail(BIMINE_E_LIMIT, "bimine_score_batch: a sentence has more than 4096 distinct or 16384 total tokens");
   if (b->n_pairs > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: more than 2^31-1 pairs per call");
-  if (plan->n_large > 0 && !plan->large_ids) return fail(BIMINE_E_ARG, "bimine_score_batch: plan.large_ids not set");
+  if (plan->work_len > 0 && !plan->work) return fail(BIMINE_E_ARG, "bimine_score_batch: plan.work not set");
   cudaStream_t st = as_stream(stream);
   const BatchDev bd = to_dev(*b);
   const DictDev dd = DictDev{dict->n_rows, dict->row_ptr, dict->tgt, dict->prob};
   const Model md = to_model(model);
-  // per-pair kernel over every pair; it skips the plan's large pairs
-  if (plan->n_large < b->n_pairs) {
+  {
     PairArgs A;
     A.b = bd;
     A.d = dd;
@@ -280,24 +294,33 @@ int bimine_score_batch(const bimine_dict *dict, const double *model, const bimin
     int rc = term_tables(model, st, &A.T);
     if (rc != BIMINE_OK) return rc;
     A.sim = sim_dev;
-    A.pair_ids = nullptr;
-    A.n = b->n_pairs;
     A.cap_u = 1024;
     A.hash_bits = 11;
     A.cap_t = 2048;
     const size_t smem = pair_smem_layout(nullptr, A.cap_u, A.hash_bits, A.cap_t, nullptr);
     BIMINE_CUDA(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     BIMINE_CUDA(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    // one CTA per pair (it skips pairs larger than 64x64) ...
+    A.tiles = nullptr;
+    A.n = b->n_pairs;
     pair_kernel<<<(unsigned)b->n_pairs, kPairThreads, smem, st>>>(A);
     BIMINE_CUDA(cudaGetLastError());
+    // ... and one CTA per 64x64 tile of the larger ones
+    if (plan->n_tiles > 0) {
+      if (plan->n_tiles > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: too many tiles");
+      A.tiles = plan->work;
+      A.n = plan->n_tiles;
+      pair_kernel<<<(unsigned)plan->n_tiles, kPairThreads, smem, st>>>(A);
+      BIMINE_CUDA(cudaGetLastError());
+    }
   }
-  if (plan->n_large > 0) {
+  if (plan->n_long > 0) {
     ScoreArgs A;
     A.b = bd;
     A.d = dd;
     A.md = md;
     A.sim = sim_dev;
-    A.pair_ids = plan->large_ids;
+    A.pair_ids = plan->work + 3 * plan->n_tiles;
     A.cap_u = std::min(kMaxCapU, std::max(1024, next_pow2(plan->max_uniq)));
     A.cap_t = std::min(kMaxCapT, std::max(4096, next_pow2(plan->max_len)));
     A.hash_bits = ilog2(2 * A.cap_u);
@@ -306,8 +329,8 @@ int bimine_score_batch(const bimine_dict *dict, const double *model, const bimin
     A.status = status;
     const size_t smem = score_smem_layout(nullptr, A.cap_u, A.cap_t, nullptr);
     BIMINE_CUDA(cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dim3 grid((unsigned)plan->n_large, (unsigned)((plan->large_max_n + kScoreTile - 1) / kScoreTile),
-              (unsigned)((plan->large_max_m + kScoreTile - 1) / kScoreTile));
+    dim3 grid((unsigned)plan->n_long, (unsigned)((plan->long_max_n + kScoreTile - 1) / kScoreTile),
+              (unsigned)((plan->long_max_m + kScoreTile - 1) / kScoreTile));
     if (grid.y > 65535 || grid.z > 65535) return fail(BIMINE_E_LIMIT, "bimine_score_batch: document too long");
     score_kernel<<<grid, kScoreThreads, smem, st>>>(A);
     BIMINE_CUDA(cudaGetLastError());
@@ -501,10 +524,14 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   if (P == 0) return BIMINE_OK;
   pool_setup();
   cudaStream_t st = as_stream(stream);
-  std::vector<int64_t> out_off(P), large(P);
+  std::vector<int64_t> out_off(P);
+  int64_t work_cap = P;
+  for (int64_t p = 0; p < P; ++p)
+    work_cap += 3 * (int64_t)((h->pair_n[p] + kPairMax - 1) / kPairMax) * ((h->pair_m[p] + kPairMax - 1) / kPairMax);
+  std::vector<int64_t> work(std::max<int64_t>(work_cap, 1));
   bimine_plan plan;
   {
-    int rc = bimine_plan_batch(h, large.data(), &plan);
+    int rc = bimine_plan_batch(h, work.data(), work_cap, &plan);
     if (rc != BIMINE_OK) return rc;
   }
   const int32_t max_n = plan.max_n, max_m = plan.max_m;
@@ -530,7 +557,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
                o_pm = carve(4 * P), o_psim = carve(8 * P), o_outoff = carve(8 * P), o_sim = carve(8 * cells),
                o_slots = carve(sizeof(bimine_match) * cap), o_counts = carve(4 * P), o_base = carve(8 * P),
                o_comp = carve(sizeof(bimine_match) * cap), o_total = carve(8), o_par = carve(16),
-               o_large = carve(8 * plan.n_large);
+               o_work = carve(8 * plan.work_len);
   char *arena = nullptr;
   BIMINE_CUDA(cudaMallocAsync((void **)&arena, off, st));
   auto H2D = [&](size_t o, const void *src, size_t bytes) {
@@ -550,7 +577,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   e = e ? e : H2D(o_psim, h->pair_sim_off, 8 * P);
   e = e ? e : H2D(o_outoff, out_off.data(), 8 * P);
   e = e ? e : H2D(o_par, par, 16);
-  e = e ? e : H2D(o_large, large.data(), 8 * plan.n_large);
+  e = e ? e : H2D(o_work, work.data(), 8 * plan.work_len);
   if (e != cudaSuccess) {
     cudaFreeAsync(arena, st);
     return fail(BIMINE_E_CUDA, std::string("bimine_mine_host H2D: ") + cudaGetErrorString(e));
@@ -570,7 +597,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   d.pair_m = (const int32_t *)(arena + o_pm);
   d.pair_sim_off = (const int64_t *)(arena + o_psim);
   double *sim = (double *)(arena + o_sim);
-  plan.large_ids = (const int64_t *)(arena + o_large);
+  plan.work = (const int64_t *)(arena + o_work);
   int rc = bimine_score_batch(dict, model, &d, &plan, sim, stream);
   const double *pd = (const double *)(arena + o_par);
   if (rc == BIMINE_OK)

@@ -1,8 +1,8 @@
 // pair_kernel.cuh -- score matrix of one document pair per CTA.
 //
 // build_score_matrix (align.py:102-129) for pairs with N, M <= 64 and
-// sentences of <= 255 tokens (every BASELINE config except the long-pair
-// stress C3 and the 200x220 C1 pair, which take the tiled score_kernel).
+// sentences of <= 255 tokens (all C2/C4/C5 pairs); larger pairs (C1, C3)
+// run the same kernel over 64x64 sentence tiles, (pair, i0, j0) per CTA.
 // 8 warps; all per-pair state lives in shared memory and every count is
 // produced 32 cells at a time by bit-matrix transposes:
 //
@@ -50,8 +50,8 @@ struct PairArgs {
   Model md;
   TermTables T;
   double *sim;
-  const int64_t *pair_ids;  // optional: launch over these pairs
-  int64_t n;                // pairs in this launch
+  const int64_t *tiles;     // optional: (pair, i0, j0) per CTA for pairs larger than 64x64
+  int64_t n;                // CTAs in this launch
   int cap_u;                // distinct target tokens per chunk (dense arrays)
   int hash_bits;            // log2(hash slots) >= log2(2 cap_u)
   int cap_t;                // target occurrences per chunk
@@ -176,21 +176,32 @@ __host__ __device__ inline bool pair_is_small(int n, int m, int max_len) {
 
 __global__ void __launch_bounds__(kPairThreads, 3) pair_kernel(const PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int64_t p = A.pair_ids ? A.pair_ids[blockIdx.x] : (int64_t)blockIdx.x;
-  const int N = A.b.pair_n[p], M = A.b.pair_m[p];
-  if (N > kPairMax || M > kPairMax) return;
+  int64_t p;
+  int i0 = 0, j0 = 0;
+  if (A.tiles) {
+    p = A.tiles[3 * (int64_t)blockIdx.x];
+    i0 = (int)A.tiles[3 * (int64_t)blockIdx.x + 1];
+    j0 = (int)A.tiles[3 * (int64_t)blockIdx.x + 2];
+  } else {
+    p = blockIdx.x;
+  }
+  const int Nfull = A.b.pair_n[p], Mfull = A.b.pair_m[p];
+  if (!A.tiles && (Nfull > kPairMax || Mfull > kPairMax)) return;  // tiled launch covers it
+  // this CTA's block: source sentences [i0, i0 + N), target sentences [j0, j0 + M)
+  const int N = min(kPairMax, Nfull - i0), M = min(kPairMax, Mfull - j0);
   PairSmem S;
   const int hbits = A.hash_bits;
   pair_smem_layout(smem_raw, A.cap_u, hbits, A.cap_t, &S);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t s_first = A.b.pair_src[p], t_first = A.b.pair_tgt[p];
+  const int64_t s_first = A.b.pair_src[p] + i0, t_first = A.b.pair_tgt[p] + j0;
   const int32_t *__restrict__ tokens = A.b.tokens;
   const int64_t *__restrict__ row_ptr = A.d.row_ptr;
   const int32_t *__restrict__ dtgt = A.d.tgt;
   const double *__restrict__ dprob = A.d.prob;
   const int64_t n_rows = A.d.n_rows;
   const int hslots = 1 << hbits;
-  double *__restrict__ out = A.sim + A.b.pair_sim_off[p];  // also the running-sum scratch
+  // the block's cell (i, j) lives at out[i * Mfull + j]; also the running-sum scratch
+  double *__restrict__ out = A.sim + A.b.pair_sim_off[p] + (int64_t)i0 * Mfull + j0;
 
   // ---- 0: tables and sentence metadata
   for (int k = tid; k < 256; k += kPairThreads) S.exp_tab[k] = kExpTableDev[k];
@@ -462,12 +473,12 @@ __global__ void __launch_bounds__(kPairThreads, 3) pair_kernel(const PairArgs A)
         if (jlo < nj) {
           S.cov[i * kCellStride + jc0 + jlo] = (uint8_t)cov_lo;
           S.shr[i * kCellStride + jc0 + jlo] = (uint8_t)sh_lo;
-          out[i * M + jc0 + jlo] = sum_lo;
+          out[(int64_t)i * Mfull + jc0 + jlo] = sum_lo;
         }
         if (jhi < nj) {
           S.cov[i * kCellStride + jc0 + jhi] = (uint8_t)cov_hi;
           S.shr[i * kCellStride + jc0 + jhi] = (uint8_t)sh_hi;
-          out[i * M + jc0 + jhi] = sum_hi;
+          out[(int64_t)i * Mfull + jc0 + jhi] = sum_hi;
         }
       }
     }
@@ -498,8 +509,9 @@ __global__ void __launch_bounds__(kPairThreads, 3) pair_kernel(const PairArgs A)
   for (int c = tid; c < cells; c += kPairThreads) {
     const int i = c / M, j = c - i * M;
     const int x = i * kCellStride + j;
-    out[c] = cell_score_t(A.md, A.T, S.src_len[i], S.src_uniq[i], S.src_chars[i], S.tgt_len[j], S.tgt_uniq[j],
-                          S.tgt_chars[j], S.cov[x], out[c], S.covt[x], S.shr[x], S.exp_tab);
+    const int64_t o = (int64_t)i * Mfull + j;
+    out[o] = cell_score_t(A.md, A.T, S.src_len[i], S.src_uniq[i], S.src_chars[i], S.tgt_len[j], S.tgt_uniq[j],
+                          S.tgt_chars[j], S.cov[x], out[o], S.covt[x], S.shr[x], S.exp_tab);
   }
 }
 

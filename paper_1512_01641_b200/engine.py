@@ -112,9 +112,9 @@ class DeviceBatch:
                 a = a.pin_memory()
             self.t[f] = a.to(f"cuda:{device}", non_blocking=pinned)
         self.struct = N.batch_struct_device(self.t, batch.n_pairs, batch.n_sentences, batch.n_tokens)
-        self.plan, large = plan_batch(batch)
-        self.t["large_ids"] = torch.from_numpy(large).to(f"cuda:{device}")
-        self.plan.large_ids = self.t["large_ids"].data_ptr() if large.size else None
+        self.plan, work = plan_batch(batch)
+        self.t["work"] = torch.from_numpy(work).to(f"cuda:{device}")
+        self.plan.work = self.t["work"].data_ptr() if work.size else None
         self.max_n, self.max_m = int(self.plan.max_n), int(self.plan.max_m)
         cap = batch.match_capacity()
         self.capacity = int(cap[-1])
@@ -122,13 +122,16 @@ class DeviceBatch:
 
 
 def plan_batch(batch: PackedBatch):
-    """bimine_plan_batch on the host arrays -> (CPlan, large pair ids)."""
+    """bimine_plan_batch on the host arrays -> (CPlan, int64 work array)."""
     L = N.load(require_gpu=False)
-    large = np.zeros(max(batch.n_pairs, 1), dtype=np.int64)
+    n = batch.pair_n.astype(np.int64)
+    m = batch.pair_m.astype(np.int64)
+    cap = int(batch.n_pairs + 3 * np.sum(((n + 63) // 64) * ((m + 63) // 64)))
+    work = np.zeros(max(cap, 1), dtype=np.int64)
     plan = N.CPlan()
     cb = N.batch_struct_host(batch)
-    N.check(L.bimine_plan_batch(ctypes.byref(cb), N.ptr(large, N._i64p), ctypes.byref(plan)))
-    return plan, large[: int(plan.n_large)].copy()
+    N.check(L.bimine_plan_batch(ctypes.byref(cb), N.ptr(work, N._i64p), cap, ctypes.byref(plan)))
+    return plan, work[: int(plan.work_len)].copy()
 
 
 def stream_ptr(stream=None) -> int:

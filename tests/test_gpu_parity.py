@@ -304,3 +304,29 @@ def test_lexicon_duplicates_last_wins():
     prob = np.array([0.9, 0.2, 0.0, 0.4])
     d = E.DeviceDictionary(None, src, tgt, prob, E.current_device())
     assert d.n_entries == 2  # (0,5)=0.2, (1,5)=0.4; (0,6)=0 dropped
+
+
+def test_sentences_longer_than_255_tokens_use_fallback_kernel():
+    """u8 counters in pair_kernel: such pairs go to the tiled fallback; same bits."""
+    rng = np.random.default_rng(8)
+    lex = Lexicon({f"w{k}": {f"v{(k * 3 + j) % 500}": 0.1 + 0.1 * j for j in range(3)} for k in range(500)})
+    def sent(n, pre):
+        return " ".join(f"{pre}{i}" for i in rng.integers(0, 500, size=n)) + "."
+    pairs = [([sent(300, "w"), sent(5, "w")], [sent(280, "v"), sent(4, "v"), sent(7, "v")]),
+             ([sent(20, "w")] * 3, [sent(20, "v")] * 2)]
+    vocab, coo, batch = H.pack_pairs(lex, pairs)
+    model = model_vector(H.toy_model())
+    want = oracle.score_batch(oracle.OracleDict(*coo), model, batch)
+    ctx = E.LexiconContext(vocab=vocab, coo=coo, devices={})
+    plan, _ = E.plan_batch(batch)
+    assert plan.n_long == 1 and plan.n_tiles == 0
+    got = E.score_host(ctx.on(E.current_device()), model, batch)
+    assert bits_equal(got, want)
+
+
+def test_plan_tiles_for_large_pairs():
+    corpus = synth.make_corpus(79, 3, 2_000, shape=(130, 65))
+    plan, work = E.plan_batch(corpus.batch)
+    assert plan.n_tiles == 3 * 3 * 2 and plan.n_long == 0
+    assert work.reshape(-1, 3)[:, 0].tolist() == [0] * 6 + [1] * 6 + [2] * 6
+    _synth_check(corpus)
