@@ -203,6 +203,21 @@ int bimine_compact_matches(const bimine_match *matches_dev,
                            int64_t *match_base_dev, bimine_match *compact_dev,
                            int64_t *total_dev, void *stream);
 
+/* ---- tuning agreement (tuning.py:60-82) --------------------------------
+ * For every problem q = pair * n_settings + s of a bimine_nw_mine_batch
+ * call: candidate = its match slots (out_off_dev[q], counts_dev[q]) read
+ * as (i, j); reference = ref_ij_dev[2 * ref_off_dev[pair] ...] int32
+ * (i, j) pairs, ref_len_dev[pair] of them.  matched_dev[q] = Match steps
+ * joining equal pairs in the NW alignment of the two lists (match +1,
+ * mismatch -1, gap 1).  The agreement percentage and the empty-list rules
+ * are applied by the caller.  max_k / max_r bound the list lengths. */
+int bimine_agreement_batch(const bimine_match *matches_dev,
+                           const int64_t *out_off_dev, const int32_t *counts_dev,
+                           int64_t n_pairs, int32_t n_settings,
+                           const int32_t *ref_ij_dev, const int64_t *ref_off_dev,
+                           const int32_t *ref_len_dev, int32_t max_k,
+                           int32_t max_r, int32_t *matched_dev, void *stream);
+
 /* ---- end to end from host buffers (the e2e call) ----------------------
  * batch_host: host pointers.  Copies the packed batch to the device,
  * scores, aligns under one setting, filters, compacts and copies back.

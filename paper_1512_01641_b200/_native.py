@@ -100,6 +100,8 @@ SIGNATURES = {
                                             _vp, _vp, _vp]),
     "bimine_nw_steps_batch": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                              _vp, ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _vp, _vp]),
+    "bimine_agreement_batch": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp, _vp,
+                                              ctypes.c_int32, ctypes.c_int32, _vp, _vp]),
     "bimine_compact_matches": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp]),
     "bimine_mine_host": (ctypes.c_int, [_vp, _f64p, ctypes.POINTER(CBatch), ctypes.c_double, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_double, _i32p, _vp, ctypes.c_int64, _i64p,

@@ -463,6 +463,38 @@ int bimine_compact_matches(const bimine_match *matches_dev, const int64_t *out_o
   return BIMINE_OK;
 }
 
+int bimine_agreement_batch(const bimine_match *matches_dev, const int64_t *out_off_dev, const int32_t *counts_dev,
+                           int64_t n_pairs, int32_t n_settings, const int32_t *ref_ij_dev, const int64_t *ref_off_dev,
+                           const int32_t *ref_len_dev, int32_t max_k, int32_t max_r, int32_t *matched_dev,
+                           void *stream) {
+  if (!matches_dev || !out_off_dev || !counts_dev || !ref_ij_dev || !ref_off_dev || !ref_len_dev || !matched_dev ||
+      n_settings < 1)
+    return fail(BIMINE_E_ARG, "bimine_agreement_batch: bad arguments");
+  const int64_t n = n_pairs * n_settings;
+  if (n == 0) return BIMINE_OK;
+  AgreeArgs A;
+  A.matches = matches_dev;
+  A.out_off = out_off_dev;
+  A.counts = counts_dev;
+  A.n_problems = n;
+  A.n_settings = n_settings;
+  A.ref_ij = ref_ij_dev;
+  A.ref_off = ref_off_dev;
+  A.ref_len = ref_len_dev;
+  A.matched = matched_dev;
+  const int mk = std::max(1, max_k), mr = std::max(1, max_r);
+  A.row_doubles_per_warp = ((mr + 1) + 1) & ~1;
+  const int64_t dw = (int64_t)(mk + 1) * ((mr >> 4) + 1);
+  const size_t per_block = (size_t)kNwWarpsPerBlock * (A.row_doubles_per_warp * 8 + dw * 4);
+  if (per_block > kNwSmemPerBlockMax) return fail(BIMINE_E_LIMIT, "bimine_agreement_batch: lists too long");
+  A.dir_words_per_warp = (int)dw;
+  BIMINE_CUDA(cudaFuncSetAttribute(agree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per_block));
+  agree_kernel<<<(unsigned)((n + kNwWarpsPerBlock - 1) / kNwWarpsPerBlock), kNwWarpsPerBlock * 32, per_block,
+                 as_stream(stream)>>>(A);
+  BIMINE_CUDA(cudaGetLastError());
+  return BIMINE_OK;
+}
+
 // ------------------------------------------------------------------------
 // B1 shim: the reference's _nwcore.nw_fill / nw_fill_wavefront
 // ------------------------------------------------------------------------

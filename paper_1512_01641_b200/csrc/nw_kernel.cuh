@@ -286,3 +286,120 @@ __global__ void gather_matches_kernel(const bimine_match *slots, const int64_t *
 }
 
 }  // namespace bimine
+
+namespace bimine {
+
+// ---- tuning agreement (tuning.py:60-82) ------------------------------------
+//
+// alignment_agreement(candidate, reference): NW over the two index-pair
+// lists with exact-equality scoring (match +1, mismatch -1, gap 1,
+// _AGREEMENT_CONFIG tuning.py:28), counting Match steps that join equal
+// pairs.  One warp per (pair, setting); the candidate list is the mining
+// NW's match slots of that problem, the reference list the pair's
+// human-aligned indices.  Same reversed fill / tie order / traceback as
+// nw_problem (all values are small integers, exact in binary64).
+struct AgreeArgs {
+  const bimine_match *matches;
+  const int64_t *out_off;
+  const int32_t *counts;
+  int64_t n_problems;
+  int32_t n_settings;
+  const int32_t *ref_ij;   // (i, j) int32 pairs
+  const int64_t *ref_off;  // [pairs] first pair
+  const int32_t *ref_len;  // [pairs]
+  int32_t *matched;        // [problems]
+  int dir_words_per_warp;
+  int row_doubles_per_warp;
+};
+
+__device__ __forceinline__ bool agree_eq(const bimine_match *cand, const int32_t *ref, int a, int b) {
+  return cand[a].i == ref[2 * b] && cand[a].j == ref[2 * b + 1];
+}
+
+__global__ void __launch_bounds__(128) agree_kernel(const AgreeArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (q >= A.n_problems) return;
+  double *rowbuf = (double *)smem_raw + (size_t)warp * A.row_doubles_per_warp;
+  uint32_t *dirs = (uint32_t *)((double *)smem_raw + (size_t)(blockDim.x >> 5) * A.row_doubles_per_warp) +
+                   (size_t)warp * A.dir_words_per_warp;
+  const int64_t pair = q / A.n_settings;
+  const int K = A.counts[q];
+  const int R = A.ref_len[pair];
+  if (K == 0 || R == 0) {  // handled on the host (tuning.py:69-72)
+    if (lane == 0) A.matched[q] = 0;
+    return;
+  }
+  const bimine_match *cand = A.matches + A.out_off[q];
+  const int32_t *ref = A.ref_ij + 2 * A.ref_off[pair];
+  const double gap = 1.0, ng = -1.0;
+  const int stride = (R >> 4) + 1;
+  for (int b = lane; b <= R; b += 32) rowbuf[b] = fmul(ng, (double)b);
+  __syncwarp();
+  for (int a0 = 0; a0 < K; a0 += 32) {
+    const int a = a0 + 1 + lane;
+    const bool active = a <= K;
+    const double left0 = fmul(ng, (double)a);
+    double cur = left0;
+    double diag = rowbuf[0];
+    {
+      const double prev_row0 = __shfl_up_sync(kFull, left0, 1);
+      if (lane > 0) diag = prev_row0;
+    }
+    uint32_t bits = 0u;
+    for (int s = 0; s < R + 31; ++s) {
+      const int b = s - lane + 1;
+      double up = __shfl_up_sync(kFull, cur, 1);
+      if (lane == 0) {
+        up = (b >= 1 && b <= R) ? rowbuf[b] : 0.0;
+        if (b >= 1 && b <= R) diag = rowbuf[b - 1];
+      }
+      if (active && b >= 1 && b <= R) {
+        // reversed problem: R[a-1][b-1] = sim[K-a][R-b]; c = -1 + sim * 2
+        const double c = agree_eq(cand, ref, K - a, R - b) ? 1.0 : -1.0;
+        double best = fadd(diag, c);
+        uint32_t dir = 0u;
+        double cand_v = fsub(up, gap);
+        if (cand_v > best) {
+          best = cand_v;
+          dir = 1u;
+        }
+        cand_v = fsub(cur, gap);
+        if (cand_v > best) {
+          best = cand_v;
+          dir = 2u;
+        }
+        cur = best;
+        bits |= dir << (2 * (b & 15));
+        if ((b & 15) == 15 || b == R) {
+          dirs[(int64_t)a * stride + (b >> 4)] = bits;
+          bits = 0u;
+        }
+        if (lane == 31) rowbuf[b] = best;
+      }
+      if (lane > 0) diag = up;
+    }
+    __syncwarp();
+    if (lane == 31) rowbuf[0] = left0;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    int a = K, b = R, m = 0;
+    while (a > 0 && b > 0) {
+      const uint32_t d = (dirs[(int64_t)a * stride + (b >> 4)] >> (2 * (b & 15))) & 3u;
+      if (d == 0u) {
+        if (agree_eq(cand, ref, K - a, R - b)) ++m;
+        --a;
+        --b;
+      } else if (d == 1u) {
+        --a;
+      } else {
+        --b;
+      }
+    }
+    A.matched[q] = m;
+  }
+}
+
+}  // namespace bimine

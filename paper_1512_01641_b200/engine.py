@@ -265,3 +265,48 @@ def exp_device(x: np.ndarray) -> np.ndarray:
     y = np.empty_like(x)
     N.check(L.bimine_exp_device(N.ptr(x, N._f64p), N.ptr(y, N._f64p), x.size))
     return y
+
+
+def tune_device(dd: DeviceDictionary, model_vec: np.ndarray, batch: PackedBatch, thresholds, gaps,
+                mismatch: float, bonus: float, refs: list, stream=None):
+    """Score every pair once, align it under every (threshold, gap) trial in
+    one batched launch (problem = pair * S + trial) and compute each trial's
+    agreement NW on device.  Returns (counts[P*S], matched[P*S]) on host."""
+    torch = _torch()
+    L = N.load()
+    dev = f"cuda:{dd.device}"
+    P, S = batch.n_pairs, len(gaps)
+    sp = stream_ptr(stream)
+    with torch.cuda.device(dd.device):
+        db = DeviceBatch(batch, dd.device)
+        sim = torch.empty(max(batch.n_cells, 1), dtype=torch.float64, device=dev)
+        score_device(dd, model_vec, db, sim, stream)
+        cap = np.minimum(batch.pair_n, batch.pair_m).astype(np.int64)
+        per_problem = np.repeat(cap, S)
+        out_off = np.zeros(P * S, dtype=np.int64)
+        if P * S > 1:
+            np.cumsum(per_problem[:-1], out=out_off[1:])
+        total_cap = int(per_problem.sum())
+        t_off = torch.from_numpy(out_off).to(dev)
+        t_gap = torch.tensor(np.asarray(gaps, dtype=np.float64)).to(dev)
+        t_thr = torch.tensor(np.asarray(thresholds, dtype=np.float64)).to(dev)
+        slots = torch.empty(max(total_cap, 1) * 16, dtype=torch.uint8, device=dev)
+        counts = torch.empty(max(P * S, 1), dtype=torch.int32, device=dev)
+        N.check(L.bimine_nw_mine_batch(sim.data_ptr(), db.t["pair_sim_off"].data_ptr(), db.t["pair_n"].data_ptr(),
+                                       db.t["pair_m"].data_ptr(), P, db.max_n, db.max_m, S, t_gap.data_ptr(),
+                                       t_thr.data_ptr(), mismatch, bonus, t_off.data_ptr(), slots.data_ptr(),
+                                       counts.data_ptr(), None, sp))
+        ref_len = np.array([len(r) for r in refs], dtype=np.int32)
+        ref_off = np.zeros(P, dtype=np.int64)
+        if P > 1:
+            np.cumsum(ref_len[:-1].astype(np.int64), out=ref_off[1:])
+        ref_ij = np.array([x for r in refs for pair in r for x in pair], dtype=np.int32)
+        t_rij = torch.from_numpy(ref_ij if ref_ij.size else np.zeros(2, np.int32)).to(dev)
+        t_roff = torch.from_numpy(ref_off).to(dev)
+        t_rlen = torch.from_numpy(ref_len).to(dev)
+        matched = torch.empty(max(P * S, 1), dtype=torch.int32, device=dev)
+        N.check(L.bimine_agreement_batch(slots.data_ptr(), t_off.data_ptr(), counts.data_ptr(), P, S,
+                                         t_rij.data_ptr(), t_roff.data_ptr(), t_rlen.data_ptr(),
+                                         int(cap.max(initial=1)), int(ref_len.max(initial=1)), matched.data_ptr(),
+                                         sp))
+        return counts[: P * S].cpu().numpy(), matched[: P * S].cpu().numpy()

@@ -330,3 +330,64 @@ def test_plan_tiles_for_large_pairs():
     assert plan.n_tiles == 3 * 3 * 2 and plan.n_long == 0
     assert work.reshape(-1, 3)[:, 0].tolist() == [0] * 6 + [1] * 6 + [2] * 6
     _synth_check(corpus)
+
+
+# ---------------------------------------------------------------- tuning (C4)
+
+def test_tune_matches_reference_fixture():
+    from paper_1512_01641_b200 import tuning as T
+
+    fx = H.load_json("tune_golden.json")
+    corpus = synth.make_config(fx["config"], n_pairs=fx["n_pairs"])
+    lex = Lexicon(corpus.dictionary.table())
+    samples = []
+    for p in range(fx["n_pairs"]):
+        src, tgt = corpus.pair_sentences(p)
+        pair = DocumentPair(f"tune-{p}", Document(f"tune-{p}-s", "pl", str(p), tuple(src)),
+                            Document(f"tune-{p}-t", "en", str(p), tuple(tgt)))
+        samples.append(T.TuningSample(pair=pair, reference=tuple(tuple(r) for r in corpus.reference[p])))
+    res = T.tune(H.synth_model(), lex, samples, budget=fx["budget"], seed=fx["seed"], engine="nw")
+    want = fx["result"]
+    assert res.threshold.hex() == want["threshold"] and res.gap_penalty.hex() == want["gap_penalty"]
+    assert res.agreement.hex() == want["agreement"] and res.trials == want["trials"]
+    assert [v.hex() for v in res.per_sample] == want["per_sample"]
+    assert res.default_agreement.hex() == want["default_agreement"]
+
+
+def test_alignment_agreement_kats():
+    from paper_1512_01641_b200 import tuning as T
+
+    assert T.alignment_agreement([(0, 0), (1, 1)], [(0, 0), (1, 1)]) == 100.0
+    assert T.alignment_agreement([], [(0, 0)]) == 0.0
+    assert T.alignment_agreement([], []) == 100.0
+    assert T.alignment_agreement([(0, 0)], []) == 0.0
+    assert T.alignment_agreement([(0, 0), (2, 2)], [(0, 0), (1, 1), (2, 2)]) == 200.0 / 3.0
+    assert T.alignment_agreement([(0, 0), (1, 1), (2, 2)], [(0, 0), (2, 2)]) == 100.0
+    for ref, cand, v in H.load_json("tune_golden.json")["agreement_kats"]:
+        assert T.alignment_agreement([tuple(x) for x in cand], [tuple(x) for x in ref]).hex() == v
+
+
+def test_tune_trials_agree_with_per_trial_recomputation():
+    """Batched device agreements == per-trial mining + alignment_agreement."""
+    from paper_1512_01641_b200 import tuning as T
+
+    corpus = synth.make_config(4, n_pairs=5)
+    lex = Lexicon(corpus.dictionary.table())
+    model = H.synth_model()
+    samples = []
+    for p in range(5):
+        src, tgt = corpus.pair_sentences(p)
+        pair = DocumentPair(f"t{p}", Document("s", "pl", "t", tuple(src)), Document("t", "en", "t", tuple(tgt)))
+        samples.append(T.TuningSample(pair=pair, reference=tuple(tuple(r) for r in corpus.reference[p])))
+    res = T.tune(model, lex, samples, budget=12, seed=3)
+    thr, gaps = T.draw_trials(A.MiningConfig(), 12, 3)
+    rows = []
+    for t in range(12):
+        cfg = A.MiningConfig(threshold=thr[t], gap_penalty=gaps[t])
+        row = []
+        for s in samples:
+            cand = [(i, j) for _, i, j in A.align_pair_indices(model, lex, s.pair, cfg)]
+            row.append(T.alignment_agreement(cand, list(s.reference)))
+        rows.append(row)
+    want = T.select_best(np.array(rows), thr, gaps, 12)
+    assert res == want
