@@ -131,8 +131,11 @@ int64_t bimine_dict_entries(const bimine_dict *dict);
  *   tiles     pairs with N > 64 or M > 64: (pair, i0, j0) per 64x64 tile
  *   long ids  pairs with a sentence of more than 255 tokens (tiled
  *             fallback kernel)
- * work_host (capacity work_cap int64) receives 3 * n_tiles tile triples
- * followed by n_long pair ids; plan->work_len is the length needed
+ *   large ids every pair of the two groups above, ascending (their NW runs
+ *             as a separate launch; one-CTA pairs fuse it)
+ * work_host (capacity work_cap int64) receives 3 * n_tiles tile triples,
+ * then n_long pair ids, then n_large pair ids; plan->work_len is the length
+ * needed
  * (BIMINE_E_ARG if work_cap is smaller).  The caller uploads
  * work_host[0 : work_len] and sets plan->work to the device copy. */
 typedef struct bimine_plan {
@@ -141,7 +144,8 @@ typedef struct bimine_plan {
   int64_t n_tiles;             /* 64x64 tiles of large pairs              */
   int64_t n_long;              /* pairs for the fallback kernel           */
   int32_t long_max_n, long_max_m;
-  int64_t work_len;            /* 3 * n_tiles + n_long                    */
+  int64_t n_large;             /* pairs not in the one-CTA-per-pair launch */
+  int64_t work_len;            /* 3 * n_tiles + n_long + n_large          */
   const int64_t *work;         /* device copy of work_host (set by caller)*/
 } bimine_plan;
 
@@ -157,6 +161,21 @@ int bimine_plan_batch(const bimine_batch *batch_host, int64_t *work_host,
 int bimine_score_batch(const bimine_dict *dict, const double *model,
                        const bimine_batch *batch_dev, const bimine_plan *plan,
                        double *sim_dev, void *stream);
+
+/* ---- the fused mining step ---------------------------------------------
+ * build_score_matrix + nw_align + filter_by_threshold for every pair of a
+ * device batch under one setting: sim_dev receives the score matrices
+ * (written once); pairs of at most 64x64 sentences run the NW wavefront,
+ * traceback and filter inside the score kernel on the on-chip tile, the
+ * plan's large pairs in a separate NW launch.  Outputs as in
+ * bimine_nw_mine_batch with n_settings = 1 (out_off_dev: capacity
+ * min(N, M) slots per pair; score_dev optional). */
+int bimine_mine_batch(const bimine_dict *dict, const double *model,
+                      const bimine_batch *batch_dev, const bimine_plan *plan,
+                      double gap, double threshold, double mismatch, double bonus,
+                      double *sim_dev, const int64_t *out_off_dev,
+                      bimine_match *matches_dev, int32_t *counts_dev,
+                      double *score_dev, void *stream);
 
 /* ---- NW + traceback + threshold filter --------------------------------
  * Problem p = pair * n_settings + s aligns pair `pair` under setting s

@@ -76,6 +76,7 @@ class CPlan(ctypes.Structure):
         ("n_long", ctypes.c_int64),
         ("long_max_n", ctypes.c_int32),
         ("long_max_m", ctypes.c_int32),
+        ("n_large", ctypes.c_int64),
         ("work_len", ctypes.c_int64),
         ("work", _vp),
     ]
@@ -95,6 +96,9 @@ SIGNATURES = {
     "bimine_dict_entries": (ctypes.c_int64, [_vp]),
     "bimine_plan_batch": (ctypes.c_int, [ctypes.POINTER(CBatch), _i64p, ctypes.c_int64, ctypes.POINTER(CPlan)]),
     "bimine_score_batch": (ctypes.c_int, [_vp, _f64p, ctypes.POINTER(CBatch), ctypes.POINTER(CPlan), _vp, _vp]),
+    "bimine_mine_batch": (ctypes.c_int, [_vp, _f64p, ctypes.POINTER(CBatch), ctypes.POINTER(CPlan), ctypes.c_double,
+                                         ctypes.c_double, ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _vp, _vp,
+                                         _vp]),
     "bimine_nw_mine_batch": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                             ctypes.c_int32, _vp, _vp, ctypes.c_double, ctypes.c_double, _vp, _vp,
                                             _vp, _vp, _vp]),

@@ -192,7 +192,7 @@ int bimine_plan_batch(const bimine_batch *b, int64_t *work, int64_t work_cap, bi
     P.max_uniq = std::max(P.max_uniq, b->sent_uniq[s]);
     P.max_len = std::max(P.max_len, b->sent_len[s]);
   }
-  std::vector<int64_t> longs;
+  std::vector<int64_t> longs, larges;
   int64_t t = 0;
   for (int64_t p = 0; p < b->n_pairs; ++p) {
     const int32_t n = b->pair_n[p], m = b->pair_m[p];
@@ -202,6 +202,7 @@ int bimine_plan_batch(const bimine_batch *b, int64_t *work, int64_t work_cap, bi
     int32_t ml = 0;
     for (int32_t i = 0; i < n; ++i) ml = std::max(ml, b->sent_len[b->pair_src[p] + i]);
     for (int32_t j = 0; j < m; ++j) ml = std::max(ml, b->sent_len[b->pair_tgt[p] + j]);
+    if (ml > kPairMaxLen || n > kPairMax || m > kPairMax) larges.push_back(p);
     if (ml > kPairMaxLen) {
       longs.push_back(p);
       P.long_max_n = std::max(P.long_max_n, n);
@@ -220,10 +221,12 @@ int bimine_plan_batch(const bimine_batch *b, int64_t *work, int64_t work_cap, bi
   }
   P.n_tiles = t;
   P.n_long = (int64_t)longs.size();
-  P.work_len = 3 * P.n_tiles + P.n_long;
+  P.n_large = (int64_t)larges.size();
+  P.work_len = 3 * P.n_tiles + P.n_long + P.n_large;
   *plan = P;
   if (P.work_len > work_cap) return fail(BIMINE_E_ARG, "bimine_plan_batch: work_cap < plan->work_len");
   for (int64_t k = 0; k < P.n_long; ++k) work[3 * P.n_tiles + k] = longs[k];
+  for (int64_t k = 0; k < P.n_large; ++k) work[3 * P.n_tiles + P.n_long + k] = larges[k];
   return BIMINE_OK;
 }
 
@@ -272,8 +275,20 @@ int term_tables(const double *model, cudaStream_t st, TermTables *out) {
 
 extern "C" {
 
-int bimine_score_batch(const bimine_dict *dict, const double *model, const bimine_batch *b, const bimine_plan *plan,
-                       double *sim_dev, void *stream) {
+}  // extern "C"
+
+namespace {
+
+struct FusedNw {
+  double gap, threshold, mismatch, bonus;
+  const int64_t *out_off;
+  bimine_match *matches;
+  int32_t *counts;
+  double *score;
+};
+
+int launch_scores(const bimine_dict *dict, const double *model, const bimine_batch *b, const bimine_plan *plan,
+                  double *sim_dev, const FusedNw *nw, cudaStream_t st) {
   if (!dict || !model || !b || !plan || !sim_dev) return fail(BIMINE_E_ARG, "bimine_score_batch: null argument");
   if (b->n_pairs == 0) return BIMINE_OK;
   if (plan->max_n < 1 || plan->max_m < 1 || plan->max_uniq < 1 || plan->max_len < 1)
@@ -282,12 +297,12 @@ int bimine_score_batch(const bimine_dict *dict, const double *model, const bimin
     return fail(BIMINE_E_LIMIT, "bimine_score_batch: a sentence has more than 4096 distinct or 16384 total tokens");
   if (b->n_pairs > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: more than 2^31-1 pairs per call");
   if (plan->work_len > 0 && !plan->work) return fail(BIMINE_E_ARG, "bimine_score_batch: plan.work not set");
-  cudaStream_t st = as_stream(stream);
   const BatchDev bd = to_dev(*b);
   const DictDev dd = DictDev{dict->n_rows, dict->row_ptr, dict->tgt, dict->prob};
   const Model md = to_model(model);
   {
     PairArgs A;
+    memset(&A, 0, sizeof(A));
     A.b = bd;
     A.d = dd;
     A.md = md;
@@ -297,7 +312,20 @@ int bimine_score_batch(const bimine_dict *dict, const double *model, const bimin
     A.cap_u = 1024;
     A.hash_bits = 11;
     A.cap_t = 2048;
-    const size_t smem = pair_smem_layout(nullptr, A.cap_u, A.hash_bits, A.cap_t, nullptr);
+    PairSmem lay;
+    const size_t smem = pair_smem_layout(nullptr, A.cap_u, A.hash_bits, A.cap_t, &lay);
+    if (lay.overlay_bytes < kNwTileBytes + kNwRowBytes + kNwDirBytes)
+      return fail(BIMINE_E_LIMIT, "pair_kernel: overlay too small for the fused NW");
+    if (nw) {
+      A.nw_matches = nw->matches;
+      A.nw_out_off = nw->out_off;
+      A.nw_counts = nw->counts;
+      A.nw_score = nw->score;
+      A.gap = nw->gap;
+      A.threshold = nw->threshold;
+      A.mismatch = nw->mismatch;
+      A.bonus = nw->bonus;
+    }
     BIMINE_CUDA(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     BIMINE_CUDA(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     // one CTA per pair (it skips pairs larger than 64x64) ...
@@ -305,11 +333,12 @@ int bimine_score_batch(const bimine_dict *dict, const double *model, const bimin
     A.n = b->n_pairs;
     pair_kernel<<<(unsigned)b->n_pairs, kPairThreads, smem, st>>>(A);
     BIMINE_CUDA(cudaGetLastError());
-    // ... and one CTA per 64x64 tile of the larger ones
+    // ... and one CTA per 64x64 tile of the larger ones (score only)
     if (plan->n_tiles > 0) {
       if (plan->n_tiles > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: too many tiles");
       A.tiles = plan->work;
       A.n = plan->n_tiles;
+      A.nw_matches = nullptr;
       pair_kernel<<<(unsigned)plan->n_tiles, kPairThreads, smem, st>>>(A);
       BIMINE_CUDA(cudaGetLastError());
     }
@@ -336,6 +365,15 @@ int bimine_score_batch(const bimine_dict *dict, const double *model, const bimin
     BIMINE_CUDA(cudaGetLastError());
   }
   return BIMINE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bimine_score_batch(const bimine_dict *dict, const double *model, const bimine_batch *b, const bimine_plan *plan,
+                       double *sim_dev, void *stream) {
+  return launch_scores(dict, model, b, plan, sim_dev, nullptr, as_stream(stream));
 }
 
 }  // extern "C"
@@ -427,6 +465,34 @@ int bimine_nw_mine_batch(const double *sim_dev, const int64_t *pair_sim_off, con
   A.counts = counts_dev;
   A.score = score_dev;
   return launch_nw<kNwMine>(A, max_n, max_m, as_stream(stream));
+}
+
+int bimine_mine_batch(const bimine_dict *dict, const double *model, const bimine_batch *b, const bimine_plan *plan,
+                      double gap, double threshold, double mismatch, double bonus, double *sim_dev,
+                      const int64_t *out_off_dev, bimine_match *matches_dev, int32_t *counts_dev, double *score_dev,
+                      void *stream) {
+  if (!out_off_dev || !matches_dev || !counts_dev) return fail(BIMINE_E_ARG, "bimine_mine_batch: null output");
+  if (!b || b->n_pairs == 0) return BIMINE_OK;
+  cudaStream_t st = as_stream(stream);
+  pool_setup();
+  FusedNw nw{gap, threshold, mismatch, bonus, out_off_dev, matches_dev, counts_dev, score_dev};
+  int rc = launch_scores(dict, model, b, plan, sim_dev, &nw, st);
+  if (rc != BIMINE_OK || plan->n_large == 0) return rc;
+  // pairs larger than one CTA: their NW as a separate launch
+  double *par = nullptr;
+  BIMINE_CUDA(cudaMallocAsync((void **)&par, 2 * sizeof(double), st));
+  const double hpar[2] = {gap, threshold};
+  BIMINE_CUDA(cudaMemcpyAsync(par, hpar, sizeof(hpar), cudaMemcpyHostToDevice, st));
+  NwArgs A = nw_args_base(sim_dev, b->pair_sim_off, b->pair_n, b->pair_m, plan->n_large, 1, par, mismatch, bonus);
+  A.problem_ids = plan->work + 3 * plan->n_tiles + plan->n_long;
+  A.threshold = par + 1;
+  A.out_off = out_off_dev;
+  A.matches = matches_dev;
+  A.counts = counts_dev;
+  A.score = score_dev;
+  rc = launch_nw<kNwMine>(A, plan->max_n, plan->max_m, st);
+  cudaFreeAsync(par, st);
+  return rc;
 }
 
 int bimine_nw_steps_batch(const double *sim_dev, const int64_t *pair_sim_off, const int32_t *pair_n,
@@ -630,12 +696,11 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   d.pair_sim_off = (const int64_t *)(arena + o_psim);
   double *sim = (double *)(arena + o_sim);
   plan.work = (const int64_t *)(arena + o_work);
-  int rc = bimine_score_batch(dict, model, &d, &plan, sim, stream);
   const double *pd = (const double *)(arena + o_par);
-  if (rc == BIMINE_OK)
-    rc = bimine_nw_mine_batch(sim, d.pair_sim_off, d.pair_n, d.pair_m, P, max_n, max_m, 1, pd, pd + 1, mismatch,
-                              bonus, (const int64_t *)(arena + o_outoff), (bimine_match *)(arena + o_slots),
-                              (int32_t *)(arena + o_counts), nullptr, stream);
+  (void)pd;
+  int rc = bimine_mine_batch(dict, model, &d, &plan, gap, threshold, mismatch, bonus, sim,
+                             (const int64_t *)(arena + o_outoff), (bimine_match *)(arena + o_slots),
+                             (int32_t *)(arena + o_counts), nullptr, stream);
   if (rc == BIMINE_OK)
     rc = bimine_compact_matches((const bimine_match *)(arena + o_slots), (const int64_t *)(arena + o_outoff),
                                 (const int32_t *)(arena + o_counts), P, (int64_t *)(arena + o_base),

@@ -64,19 +64,19 @@ struct NwArgs {
   double *g_rows;
 };
 
-template <int MODE>
-__device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *rowbuf) {
+// One problem on one warp.  `sim` is the problem's row-major matrix with
+// row stride `ld` (global memory, or a shared-memory tile in the fused
+// score kernel); table mode reads the already reversed matrix.  Outputs:
+// mine mode -> out[0..count) matches (i ascending), steps mode -> codes.
+template <int MODE, bool kGlobal>
+__device__ __forceinline__ void nw_solve(const double *__restrict__ sim, int ld, int N, int M, double gap,
+                                         double mismatch, double bonus, double threshold, double *table,
+                                         uint32_t *dirs, double *rowbuf, bimine_match *out, uint8_t *steps,
+                                         int32_t *count_out, double *score_out) {
   const int lane = threadIdx.x & 31;
-  const int64_t pair = q / A.n_settings;
-  const int setting = (int)(q % A.n_settings);
-  const int N = A.pair_n[pair], M = A.pair_m[pair];
-  const double *__restrict__ sim = A.sim + A.sim_off[pair];
-  const double gap = A.gap_per_problem ? A.gap[q] : A.gap[setting];
   const double ng = -gap;
-  const double mismatch = A.mismatch;
-  const double span = fsub(A.bonus, A.mismatch);
+  const double span = fsub(bonus, mismatch);
   const int stride = (M >> 4) + 1;  // direction words per row (cells b = 0..M)
-  double *table = A.table;
   const int64_t tw = (int64_t)M + 1;
 
   // row 0 of the reversed table (kernels.py:46, or the caller's in table mode)
@@ -98,26 +98,25 @@ __device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *r
     // this lane's row of R: the reversed matrix row a-1 is sim row N - a
     // walked backwards (table mode receives the reversed matrix itself,
     // as kernels.fill_sequential passes it, kernels.py:55-57)
-    const double *srow = (MODE == kNwTable) ? sim + (int64_t)(a - 1) * M : sim + (int64_t)(N - a) * M + (M - 1);
+    const double *srow = (MODE == kNwTable) ? sim + (int64_t)(a - 1) * ld : sim + (int64_t)(N - a) * ld + (M - 1);
     const int64_t sdir = (MODE == kNwTable) ? 1 : -1;
+    auto ldr = [&](int b) -> double {
+      if (!(active && b >= 1 && b <= M)) return 0.0;
+      const double *q = srow + sdir * (b - 1);
+      return kGlobal ? __ldg(q) : *q;
+    };
     uint32_t bits = 0u;
     const int nsteps = M + 31;
     // R values for 8 steps at a time, the next 8 prefetched into registers
-    // (one dependent global load per step would make the sweep latency bound)
+    // (one dependent load per step would make the sweep latency bound)
     double cur8[8], nxt8[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int b = u - lane + 1;
-      nxt8[u] = (active && b >= 1 && b <= M) ? __ldg(srow + sdir * (b - 1)) : 0.0;
-    }
+    for (int u = 0; u < 8; ++u) nxt8[u] = ldr(u - lane + 1);
     for (int s0 = 0; s0 < nsteps; s0 += 8) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) cur8[u] = nxt8[u];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int b = s0 + 8 + u - lane + 1;
-        nxt8[u] = (active && b >= 1 && b <= M) ? __ldg(srow + sdir * (b - 1)) : 0.0;
-      }
+      for (int u = 0; u < 8; ++u) nxt8[u] = ldr(s0 + 8 + u - lane + 1);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int s = s0 + u;
@@ -170,14 +169,12 @@ __device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *r
     int a = N, b = M;
     int64_t cnt = 0;
     if (MODE == kNwMine) {
-      const double thr = A.threshold[setting];
-      bimine_match *out = A.matches + A.out_off[q];
       while (a > 0 && b > 0) {
         const uint32_t d = (dirs[(int64_t)a * stride + (b >> 4)] >> (2 * (b & 15))) & 3u;
         if (d == 0u) {
           const int i = N - a, j = M - b;
-          const double v = sim[(int64_t)i * M + j];
-          if (v >= thr) {
+          const double v = sim[(int64_t)i * ld + j];
+          if (v >= threshold) {
             out[cnt].score = v;
             out[cnt].i = i;
             out[cnt].j = j;
@@ -191,12 +188,10 @@ __device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *r
           --b;
         }
       }
-      A.counts[q] = (int32_t)cnt;
     } else {
-      uint8_t *st = A.steps + A.step_off[q];
       while (a > 0 && b > 0) {
         const uint32_t d = (dirs[(int64_t)a * stride + (b >> 4)] >> (2 * (b & 15))) & 3u;
-        st[cnt++] = (uint8_t)d;
+        steps[cnt++] = (uint8_t)d;
         if (d == 0u) {
           --a;
           --b;
@@ -207,18 +202,33 @@ __device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *r
         }
       }
       while (a > 0) {
-        st[cnt++] = 1u;
+        steps[cnt++] = 1u;
         --a;
       }
       while (b > 0) {
-        st[cnt++] = 2u;
+        steps[cnt++] = 2u;
         --b;
       }
-      A.n_steps[q] = (int32_t)cnt;
     }
-    if (A.score) A.score[q] = last;
+    *count_out = (int32_t)cnt;
+    if (score_out) *score_out = last;
   }
   __syncwarp();
+}
+
+template <int MODE>
+__device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *rowbuf) {
+  const int64_t pair = q / A.n_settings;
+  const int setting = (int)(q % A.n_settings);
+  const int N = A.pair_n[pair], M = A.pair_m[pair];
+  const double gap = A.gap_per_problem ? A.gap[q] : A.gap[setting];
+  const double thr = (MODE == kNwMine) ? A.threshold[setting] : 0.0;
+  bimine_match *out = (MODE == kNwMine) ? A.matches + A.out_off[q] : nullptr;
+  uint8_t *st = (MODE == kNwSteps) ? A.steps + A.step_off[q] : nullptr;
+  int32_t *cnt = (MODE == kNwMine) ? A.counts + q : (MODE == kNwSteps) ? A.n_steps + q : nullptr;
+  int32_t dummy;
+  nw_solve<MODE, true>(A.sim + A.sim_off[pair], M, N, M, gap, A.mismatch, A.bonus, thr, A.table, dirs, rowbuf, out,
+                       st, cnt ? cnt : &dummy, A.score ? A.score + q : nullptr);
 }
 
 // Warps loop over problems; each warp owns one direction area and one

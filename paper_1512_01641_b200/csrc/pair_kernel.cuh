@@ -34,6 +34,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "nw_kernel.cuh"
 #include "terms.cuh"
 
 namespace bimine {
@@ -55,6 +56,12 @@ struct PairArgs {
   int cap_u;                // distinct target tokens per chunk (dense arrays)
   int hash_bits;            // log2(hash slots) >= log2(2 cap_u)
   int cap_t;                // target occurrences per chunk
+  // fused NW + traceback + filter for one-CTA pairs (null: score only)
+  bimine_match *nw_matches;  // slots at nw_out_off[pair]
+  const int64_t *nw_out_off;
+  int32_t *nw_counts;
+  double *nw_score;          // optional
+  double gap, threshold, mismatch, bonus;
 };
 
 constexpr int kSegItems = 64;   // dictionary entries examined per warp segment
@@ -78,7 +85,13 @@ struct PairSmem {
   int16_t *dense;      // [slots]
   int16_t *tgt_d;      // [cap_t]
   uint8_t *cov, *covt, *shr;  // [64][64]
+  size_t overlay_bytes;  // bytes of the reusable region at the start
 };
+
+// fused-NW scratch inside the overlay: sim tile [64][64] f64, row buffer, directions
+constexpr size_t kNwTileBytes = 64 * 64 * 8;
+constexpr size_t kNwRowBytes = 66 * 8;
+constexpr size_t kNwDirBytes = 65 * 5 * 4;
 
 __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_u, int hash_bits, int cap_t,
                                                    PairSmem *s) {
@@ -92,16 +105,22 @@ __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_
   const size_t slots = (size_t)1 << hash_bits;
   const size_t W = kPairWarps * 32;
   PairSmem t;
-  t.exp_tab = (uint64_t *)take(256 * 8, 16);
+  // region reused by the fused NW once the score phases are done
   t.colmask = (uint64_t *)take((size_t)cap_u * 8, 16);
   t.reachcol = (uint64_t *)take((size_t)cap_u * 8, 16);
   t.o_any = (uint64_t *)take(W * 8, 16);
   t.c_m = (uint64_t *)take((size_t)kPairWarps * kSegItems * 8, 16);
   t.c_p = (double *)take((size_t)kPairWarps * kSegItems * 8, 16);
-  t.src_off = (int64_t *)take(64 * 8, 16);
-  t.tgt_off = (int64_t *)take(64 * 8, 16);
   t.bloom = (uint32_t *)take(((size_t)1 << kBloomBits) / 8, 16);
   t.keys = (int32_t *)take(slots * 4, 16);
+  t.dense = (int16_t *)take(slots * 2, 4);
+  t.tgt_d = (int16_t *)take((size_t)cap_t * 2, 4);
+  t.o_n = (int32_t *)take(W * 4, 4);
+  t.overlay_bytes = o;
+  // live until the end
+  t.exp_tab = (uint64_t *)take(256 * 8, 16);
+  t.src_off = (int64_t *)take(64 * 8, 16);
+  t.tgt_off = (int64_t *)take(64 * 8, 16);
   t.src_len = (int32_t *)take(64 * 4, 4);
   t.src_uniq = (int32_t *)take(64 * 4, 4);
   t.src_chars = (int32_t *)take(64 * 4, 4);
@@ -109,10 +128,7 @@ __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_
   t.tgt_uniq = (int32_t *)take(64 * 4, 4);
   t.tgt_chars = (int32_t *)take(64 * 4, 4);
   t.tgt_occ0 = (int32_t *)take(65 * 4, 4);
-  t.o_n = (int32_t *)take(W * 4, 4);
   t.misc = (int32_t *)take(8 * 4, 4);
-  t.dense = (int16_t *)take(slots * 2, 4);
-  t.tgt_d = (int16_t *)take((size_t)cap_t * 2, 4);
   t.cov = (uint8_t *)take(64 * 64, 4);
   t.covt = (uint8_t *)take(64 * 64, 4);
   t.shr = (uint8_t *)take(64 * 64, 4);
@@ -505,13 +521,28 @@ __global__ void __launch_bounds__(kPairThreads, 3) pair_kernel(const PairArgs A)
   }
 
   // ---- F: finalize, one cell per thread, coalesced loads/stores
+  const bool fuse_nw = A.nw_matches != nullptr && !A.tiles;
+  double *tile = (double *)smem_raw;  // overlay: dead after phase C
   const int cells = N * M;
   for (int c = tid; c < cells; c += kPairThreads) {
     const int i = c / M, j = c - i * M;
     const int x = i * kCellStride + j;
     const int64_t o = (int64_t)i * Mfull + j;
-    out[o] = cell_score_t(A.md, A.T, S.src_len[i], S.src_uniq[i], S.src_chars[i], S.tgt_len[j], S.tgt_uniq[j],
-                          S.tgt_chars[j], S.cov[x], out[o], S.covt[x], S.shr[x], S.exp_tab);
+    const double v = cell_score_t(A.md, A.T, S.src_len[i], S.src_uniq[i], S.src_chars[i], S.tgt_len[j],
+                                  S.tgt_uniq[j], S.tgt_chars[j], S.cov[x], out[o], S.covt[x], S.shr[x], S.exp_tab);
+    out[o] = v;
+    if (fuse_nw) tile[i * 64 + j] = v;
+  }
+  if (!fuse_nw) return;
+  __syncthreads();
+  // ---- NW fill + traceback + threshold filter on the tile (align.py:170-181,
+  //      132-163, 323-332), one warp; the other warps are done
+  if (warp == 0) {
+    double *rowbuf = (double *)(smem_raw + kNwTileBytes);
+    uint32_t *dirs = (uint32_t *)(smem_raw + kNwTileBytes + kNwRowBytes);
+    nw_solve<kNwMine, false>(tile, 64, N, M, A.gap, A.mismatch, A.bonus, A.threshold, nullptr, dirs, rowbuf,
+                             A.nw_matches + A.nw_out_off[p], nullptr, A.nw_counts + p,
+                             A.nw_score ? A.nw_score + p : nullptr);
   }
 }
 

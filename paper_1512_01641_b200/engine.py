@@ -126,7 +126,7 @@ def plan_batch(batch: PackedBatch):
     L = N.load(require_gpu=False)
     n = batch.pair_n.astype(np.int64)
     m = batch.pair_m.astype(np.int64)
-    cap = int(batch.n_pairs + 3 * np.sum(((n + 63) // 64) * ((m + 63) // 64)))
+    cap = int(2 * batch.n_pairs + 3 * np.sum(((n + 63) // 64) * ((m + 63) // 64)))
     work = np.zeros(max(cap, 1), dtype=np.int64)
     plan = N.CPlan()
     cb = N.batch_struct_host(batch)
@@ -148,33 +148,55 @@ def score_device(dd: DeviceDictionary, model_vec: np.ndarray, db: DeviceBatch, s
                                  sim.data_ptr(), stream_ptr(stream)))
 
 
-def mine_device(db: DeviceBatch, sim, gap: float, threshold: float, mismatch: float, bonus: float,
-                out: dict | None = None, stream=None) -> dict:
-    """NW + traceback + filter + compaction on device; returns device tensors
-    (counts, base, compact, total)."""
+def mine_device(dd: DeviceDictionary, model_vec: np.ndarray, db: DeviceBatch, sim, gap: float, threshold: float,
+                mismatch: float, bonus: float, out: dict | None = None, stream=None, events=None) -> dict:
+    """The fused mining step on a device batch (score kernel with the NW
+    tail for one-CTA pairs, NW launch for the rest) + order-preserving
+    compaction; returns device tensors (counts, base, compact, total).
+    `events` (3 CUDA events) bracket the mining call and the compaction."""
     torch = _torch()
     L = N.load()
     dev = f"cuda:{db.device}"
     P = db.batch.n_pairs
     if out is None:
         out = {
-            "par": torch.tensor([gap, threshold], dtype=torch.float64, device=dev),
             "slots": torch.empty(max(db.capacity, 1) * 16, dtype=torch.uint8, device=dev),
             "counts": torch.empty(max(P, 1), dtype=torch.int32, device=dev),
             "base": torch.empty(max(P, 1), dtype=torch.int64, device=dev),
             "compact": torch.empty(max(db.capacity, 1) * 16, dtype=torch.uint8, device=dev),
             "total": torch.zeros(1, dtype=torch.int64, device=dev),
         }
-    par = out["par"]
     sp = stream_ptr(stream)
-    N.check(L.bimine_nw_mine_batch(sim.data_ptr(), db.t["pair_sim_off"].data_ptr(), db.t["pair_n"].data_ptr(),
-                                   db.t["pair_m"].data_ptr(), P, db.max_n, db.max_m, 1, par.data_ptr(),
-                                   par.data_ptr() + 8, mismatch, bonus, db.t["out_off"].data_ptr(),
-                                   out["slots"].data_ptr(), out["counts"].data_ptr(), None, sp))
+    s = stream if stream is not None else torch.cuda.current_stream()
+    mv = np.ascontiguousarray(model_vec, dtype=np.float64)
+    if events:
+        events[0].record(s)
+    N.check(L.bimine_mine_batch(dd.handle, N.ptr(mv, N._f64p), ctypes.byref(db.struct), ctypes.byref(db.plan), gap,
+                                threshold, mismatch, bonus, sim.data_ptr(), db.t["out_off"].data_ptr(),
+                                out["slots"].data_ptr(), out["counts"].data_ptr(), None, sp))
+    if events:
+        events[1].record(s)
     N.check(L.bimine_compact_matches(out["slots"].data_ptr(), db.t["out_off"].data_ptr(), out["counts"].data_ptr(),
                                      P, out["base"].data_ptr(), out["compact"].data_ptr(), out["total"].data_ptr(),
                                      sp))
+    if events:
+        events[2].record(s)
     return out
+
+
+def nw_device(db: DeviceBatch, sim, gap: float, threshold: float, mismatch: float, bonus: float, out: dict,
+              stream=None) -> None:
+    """Standalone NW + traceback + filter over every pair of a scored batch
+    (bimine_nw_mine_batch), for NW-only measurements."""
+    torch = _torch()
+    L = N.load()
+    if "par" not in out:
+        out["par"] = torch.tensor([gap, threshold], dtype=torch.float64, device=f"cuda:{db.device}")
+    par = out["par"]
+    N.check(L.bimine_nw_mine_batch(sim.data_ptr(), db.t["pair_sim_off"].data_ptr(), db.t["pair_n"].data_ptr(),
+                                   db.t["pair_m"].data_ptr(), db.batch.n_pairs, db.max_n, db.max_m, 1,
+                                   par.data_ptr(), par.data_ptr() + 8, mismatch, bonus, db.t["out_off"].data_ptr(),
+                                   out["slots"].data_ptr(), out["counts"].data_ptr(), None, stream_ptr(stream)))
 
 
 # ---------------------------------------------------------------------------

@@ -33,8 +33,7 @@ def main():
     sim = torch.empty(max(corpus.batch.n_cells, 1), dtype=torch.float64, device="cuda:0")
     out = None
     for _ in range(args.repeat):
-        E.score_device(dd, model, db, sim)
-        out = E.mine_device(db, sim, 2.0, 0.5, -1.0, 1.0, out=out)
+        out = E.mine_device(dd, model, db, sim, 2.0, 0.5, -1.0, 1.0, out=out)
     torch.cuda.synchronize()
     print("matches", int(out["total"].item()), "cells", corpus.batch.n_cells)
 
