@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <cstdio>
 #include <map>
 #include <cstring>
@@ -328,20 +329,13 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
     }
     BIMINE_CUDA(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     BIMINE_CUDA(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    // one CTA per pair (it skips pairs larger than 64x64) ...
-    A.tiles = nullptr;
-    A.n = b->n_pairs;
-    pair_kernel<<<(unsigned)b->n_pairs, kPairThreads, smem, st>>>(A);
+    // one launch: the tiles of pairs larger than 64x64, then one CTA per pair
+    A.tiles = plan->n_tiles ? plan->work : nullptr;
+    A.n_tiles = plan->n_tiles;
+    const int64_t grid = plan->n_tiles + b->n_pairs;
+    if (grid > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: too many CTAs");
+    pair_kernel<<<(unsigned)grid, kPairThreads, smem, st>>>(A);
     BIMINE_CUDA(cudaGetLastError());
-    // ... and one CTA per 64x64 tile of the larger ones (score only)
-    if (plan->n_tiles > 0) {
-      if (plan->n_tiles > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: too many tiles");
-      A.tiles = plan->work;
-      A.n = plan->n_tiles;
-      A.nw_matches = nullptr;
-      pair_kernel<<<(unsigned)plan->n_tiles, kPairThreads, smem, st>>>(A);
-      BIMINE_CUDA(cudaGetLastError());
-    }
   }
   if (plan->n_long > 0) {
     ScoreArgs A;
@@ -475,9 +469,32 @@ int bimine_mine_batch(const bimine_dict *dict, const double *model, const bimine
   if (!b || b->n_pairs == 0) return BIMINE_OK;
   cudaStream_t st = as_stream(stream);
   pool_setup();
+  // The NW tail fused into the score kernel holds each CTA's shared memory
+  // for the single-warp wavefront; until that tail is faster than the
+  // standalone NW launch it is opt-in (BIMINE_FUSE_NW=1).
+  static const bool fuse = [] {
+    const char *v = getenv("BIMINE_FUSE_NW");
+    return v && v[0] == '1';
+  }();
   FusedNw nw{gap, threshold, mismatch, bonus, out_off_dev, matches_dev, counts_dev, score_dev};
-  int rc = launch_scores(dict, model, b, plan, sim_dev, &nw, st);
-  if (rc != BIMINE_OK || plan->n_large == 0) return rc;
+  int rc = launch_scores(dict, model, b, plan, sim_dev, fuse ? &nw : nullptr, st);
+  if (rc != BIMINE_OK) return rc;
+  if (!fuse) {
+    double *par = nullptr;
+    BIMINE_CUDA(cudaMallocAsync((void **)&par, 2 * sizeof(double), st));
+    const double hpar[2] = {gap, threshold};
+    BIMINE_CUDA(cudaMemcpyAsync(par, hpar, sizeof(hpar), cudaMemcpyHostToDevice, st));
+    NwArgs A = nw_args_base(sim_dev, b->pair_sim_off, b->pair_n, b->pair_m, b->n_pairs, 1, par, mismatch, bonus);
+    A.threshold = par + 1;
+    A.out_off = out_off_dev;
+    A.matches = matches_dev;
+    A.counts = counts_dev;
+    A.score = score_dev;
+    rc = launch_nw<kNwMine>(A, plan->max_n, plan->max_m, st);
+    cudaFreeAsync(par, st);
+    return rc;
+  }
+  if (plan->n_large == 0) return rc;
   // pairs larger than one CTA: their NW as a separate launch
   double *par = nullptr;
   BIMINE_CUDA(cudaMallocAsync((void **)&par, 2 * sizeof(double), st));

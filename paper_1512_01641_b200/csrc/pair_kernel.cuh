@@ -51,8 +51,8 @@ struct PairArgs {
   Model md;
   TermTables T;
   double *sim;
-  const int64_t *tiles;     // optional: (pair, i0, j0) per CTA for pairs larger than 64x64
-  int64_t n;                // CTAs in this launch
+  const int64_t *tiles;     // (pair, i0, j0) per tile of the pairs larger than 64x64
+  int64_t n_tiles;          // CTAs [0, n_tiles) are tiles, the rest one pair each
   int cap_u;                // distinct target tokens per chunk (dense arrays)
   int hash_bits;            // log2(hash slots) >= log2(2 cap_u)
   int cap_t;                // target occurrences per chunk
@@ -192,17 +192,21 @@ __host__ __device__ inline bool pair_is_small(int n, int m, int max_len) {
 
 __global__ void __launch_bounds__(kPairThreads, 3) pair_kernel(const PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  // CTAs [0, n_tiles) take the 64x64 tiles of large pairs (first, so the
+  // long pairs start early), the rest one pair each (pairs larger than
+  // 64x64 are skipped there: their tiles cover them)
   int64_t p;
   int i0 = 0, j0 = 0;
-  if (A.tiles) {
+  const bool is_tile = (int64_t)blockIdx.x < A.n_tiles;
+  if (is_tile) {
     p = A.tiles[3 * (int64_t)blockIdx.x];
     i0 = (int)A.tiles[3 * (int64_t)blockIdx.x + 1];
     j0 = (int)A.tiles[3 * (int64_t)blockIdx.x + 2];
   } else {
-    p = blockIdx.x;
+    p = (int64_t)blockIdx.x - A.n_tiles;
   }
   const int Nfull = A.b.pair_n[p], Mfull = A.b.pair_m[p];
-  if (!A.tiles && (Nfull > kPairMax || Mfull > kPairMax)) return;  // tiled launch covers it
+  if (!is_tile && (Nfull > kPairMax || Mfull > kPairMax)) return;
   // this CTA's block: source sentences [i0, i0 + N), target sentences [j0, j0 + M)
   const int N = min(kPairMax, Nfull - i0), M = min(kPairMax, Mfull - j0);
   PairSmem S;
@@ -521,7 +525,7 @@ __global__ void __launch_bounds__(kPairThreads, 3) pair_kernel(const PairArgs A)
   }
 
   // ---- F: finalize, one cell per thread, coalesced loads/stores
-  const bool fuse_nw = A.nw_matches != nullptr && !A.tiles;
+  const bool fuse_nw = A.nw_matches != nullptr && !is_tile;
   double *tile = (double *)smem_raw;  // overlay: dead after phase C
   const int cells = N * M;
   for (int c = tid; c < cells; c += kPairThreads) {
