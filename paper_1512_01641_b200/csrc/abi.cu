@@ -380,8 +380,8 @@ namespace {
 template <int MODE>
 int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
   if (A.n_problems == 0) return BIMINE_OK;
-  const int row_d = ((max_m + 1) + 1) & ~1;  // doubles, even
-  const int64_t dir_w = (MODE == kNwTable) ? 0 : nw2_dir_words(max_n, max_m);  // u32 words
+  const int row_d = ((max_m + 1) + 1) & ~1;                      // doubles, even
+  const int64_t dir_w = (int64_t)(max_n + 1) * ((max_m >> 4) + 1);  // u32 words
   const size_t per_warp = (size_t)row_d * 8 + (size_t)dir_w * 4;
   A.row_doubles_per_warp = row_d;
   if (MODE == kNwTable) A.dir_words_per_warp = 0;

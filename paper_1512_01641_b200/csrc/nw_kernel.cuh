@@ -216,180 +216,6 @@ __device__ __forceinline__ void nw_solve(const double *__restrict__ sim, int ld,
   __syncwarp();
 }
 
-// Mine / steps modes, two 32-row bands per sweep.  Lane l owns rows
-// A = a0+1+l and B = a0+33+l; band B runs 32 steps behind band A (its
-// lane 0 takes row a0+32 from band A's lane 31 through the same rotated
-// shuffle that feeds every other lane its upper neighbour), so one sweep
-// of M+63 steps fills 64 rows with two independent dependency chains per
-// lane.  Steps are branch free: invalid cells are computed and discarded
-// by selects, and each step's direction bits are collected with two
-// ballots per band (diagonal-major: word (band, step) holds bit l of
-// lane l's cell), so no lane ever takes a private branch.
-template <int MODE, bool kGlobal>
-__device__ __forceinline__ void nw_solve2(const double *__restrict__ sim, int ld, int N, int M, double gap,
-                                          double mismatch, double bonus, double threshold, uint32_t *dirs,
-                                          double *rowbuf, bimine_match *out, uint8_t *steps, int32_t *count_out,
-                                          double *score_out) {
-  const int lane = threadIdx.x & 31;
-  const double ng = -gap;
-  const double span = fsub(bonus, mismatch);
-  const int T = M + 31;  // direction steps per band
-  const int up_src = (lane + 31) & 31;
-  for (int b = lane; b <= M; b += 32) rowbuf[b] = fmul(ng, (double)b);  // row 0 (kernels.py:46)
-  __syncwarp();
-  double last = 0.0;
-  for (int a0 = 0; a0 < N; a0 += 64) {
-    const int aA = a0 + 1 + lane, aB = a0 + 33 + lane;
-    const bool actA = aA <= N, actB = aB <= N;
-    const bool twoB = a0 + 33 <= N;  // band B has rows in this sweep
-    const double leftA = fmul(ng, (double)aA), leftB = fmul(ng, (double)aB);  // column 0 (kernels.py:47)
-    double curA = leftA, curB = leftB;
-    // diagonals before the first cell: dp[row-1][0]
-    double diagA = __shfl_up_sync(kFull, leftA, 1);
-    if (lane == 0) diagA = rowbuf[0];
-    double diagB = __shfl_sync(kFull, lane == 31 ? leftA : leftB, up_src);
-    const double *srowA = sim + (int64_t)(N - aA) * ld + (M - 1);
-    const double *srowB = sim + (int64_t)(N - aB) * ld + (M - 1);
-    auto ld_r = [&](const double *row, bool act, int b) -> double {
-      if (!(act && b >= 1 && b <= M)) return 0.0;
-      const double *q = row - (b - 1);
-      return kGlobal ? __ldg(q) : *q;
-    };
-    const int nsteps = twoB ? M + 63 : M + 31;
-    const int gA = a0 >> 5, gB = gA + 1;
-    double rA[8], rB[8], nA[8], nB[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      nA[u] = ld_r(srowA, actA, u - lane + 1);
-      nB[u] = ld_r(srowB, actB, u - lane - 31);
-    }
-    for (int s0 = 0; s0 < nsteps; s0 += 8) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        rA[u] = nA[u];
-        rB[u] = nB[u];
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        nA[u] = ld_r(srowA, actA, s0 + 8 + u - lane + 1);
-        nB[u] = ld_r(srowB, actB, s0 + 8 + u - lane - 31);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int s = s0 + u;
-        if (s >= nsteps) break;
-        const int bA = s - lane + 1, bB = s - lane - 31;
-        const bool vA = actA && bA >= 1 && bA <= M;
-        const bool vB = actB && bB >= 1 && bB <= M;
-        // upper neighbours: band A from lane-1 (lane 0: the row buffer),
-        // band B from lane-1 (lane 0: band A's lane 31)
-        double upA = __shfl_up_sync(kFull, curA, 1);
-        const int bc = min(max(bA, 1), M);
-        const double rbu = rowbuf[bc], rbd = rowbuf[bc - 1];
-        if (lane == 0) {
-          upA = rbu;
-          diagA = rbd;
-        }
-        const double upB = __shfl_sync(kFull, lane == 31 ? curA : curB, up_src);
-        // band A cell
-        double best = fadd(diagA, fadd(mismatch, fmul(rA[u], span)));
-        uint32_t dA = 0u;
-        double cand = fsub(upA, gap);
-        if (cand > best) { best = cand; dA = 1u; }
-        cand = fsub(curA, gap);
-        if (cand > best) { best = cand; dA = 2u; }
-        curA = vA ? best : curA;
-        if (vA && aA == N && bA == M) last = best;
-        // band B cell
-        double bestB = fadd(diagB, fadd(mismatch, fmul(rB[u], span)));
-        uint32_t dB = 0u;
-        cand = fsub(upB, gap);
-        if (cand > bestB) { bestB = cand; dB = 1u; }
-        cand = fsub(curB, gap);
-        if (cand > bestB) { bestB = cand; dB = 2u; }
-        curB = vB ? bestB : curB;
-        if (vB && aB == N && bB == M) last = bestB;
-        if (vB && lane == 31) rowbuf[bB] = bestB;  // next sweep's upper boundary
-        diagA = upA;
-        diagB = upB;
-        const uint32_t a_lo = __ballot_sync(kFull, vA && (dA & 1u));
-        const uint32_t a_hi = __ballot_sync(kFull, vA && (dA & 2u));
-        const uint32_t b_lo = __ballot_sync(kFull, vB && (dB & 1u));
-        const uint32_t b_hi = __ballot_sync(kFull, vB && (dB & 2u));
-        if (lane == 0 && s < T) {
-          dirs[2 * ((int64_t)gA * T + s)] = a_lo;
-          dirs[2 * ((int64_t)gA * T + s) + 1] = a_hi;
-        }
-        if (lane == 0 && twoB && s >= 32) {
-          dirs[2 * ((int64_t)gB * T + s - 32)] = b_lo;
-          dirs[2 * ((int64_t)gB * T + s - 32) + 1] = b_hi;
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 31) rowbuf[0] = leftB;  // dp[a0+64][0] for the next sweep
-    __syncwarp();
-  }
-  last = __shfl_sync(kFull, last, (N - 1) & 31);
-  if (lane == 0) {
-    int a = N, b = M;
-    int64_t cnt = 0;
-    auto dir_at = [&](int aa, int bb) -> uint32_t {
-      const int g = (aa - 1) >> 5, l = (aa - 1) & 31;
-      const int64_t w = 2 * ((int64_t)g * T + bb + l - 1);
-      return ((dirs[w] >> l) & 1u) | (((dirs[w + 1] >> l) & 1u) << 1);
-    };
-    if (MODE == kNwMine) {
-      while (a > 0 && b > 0) {
-        const uint32_t d = dir_at(a, b);
-        if (d == 0u) {
-          const int i = N - a, j = M - b;
-          const double v = sim[(int64_t)i * ld + j];
-          if (v >= threshold) {
-            out[cnt].score = v;
-            out[cnt].i = i;
-            out[cnt].j = j;
-            ++cnt;
-          }
-          --a;
-          --b;
-        } else if (d == 1u) {
-          --a;
-        } else {
-          --b;
-        }
-      }
-    } else {
-      while (a > 0 && b > 0) {
-        const uint32_t d = dir_at(a, b);
-        steps[cnt++] = (uint8_t)d;
-        if (d == 0u) {
-          --a;
-          --b;
-        } else if (d == 1u) {
-          --a;
-        } else {
-          --b;
-        }
-      }
-      while (a > 0) {
-        steps[cnt++] = 1u;
-        --a;
-      }
-      while (b > 0) {
-        steps[cnt++] = 2u;
-        --b;
-      }
-    }
-    *count_out = (int32_t)cnt;
-    if (score_out) *score_out = last;
-  }
-  __syncwarp();
-}
-
-// direction words nw_solve2 needs for an N x M problem
-__host__ __device__ inline int64_t nw2_dir_words(int N, int M) { return 2 * (int64_t)((N + 31) / 32) * (M + 31); }
-
 template <int MODE>
 __device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *rowbuf) {
   const int64_t pair = q / A.n_settings;
@@ -401,12 +227,8 @@ __device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *r
   uint8_t *st = (MODE == kNwSteps) ? A.steps + A.step_off[q] : nullptr;
   int32_t *cnt = (MODE == kNwMine) ? A.counts + q : (MODE == kNwSteps) ? A.n_steps + q : nullptr;
   int32_t dummy;
-  if (MODE == kNwTable)
-    nw_solve<MODE, true>(A.sim + A.sim_off[pair], M, N, M, gap, A.mismatch, A.bonus, thr, A.table, dirs, rowbuf, out,
-                         st, cnt ? cnt : &dummy, A.score ? A.score + q : nullptr);
-  else
-    nw_solve2<MODE, true>(A.sim + A.sim_off[pair], M, N, M, gap, A.mismatch, A.bonus, thr, dirs, rowbuf, out, st,
-                          cnt ? cnt : &dummy, A.score ? A.score + q : nullptr);
+  nw_solve<MODE, true>(A.sim + A.sim_off[pair], M, N, M, gap, A.mismatch, A.bonus, thr, A.table, dirs, rowbuf, out,
+                       st, cnt ? cnt : &dummy, A.score ? A.score + q : nullptr);
 }
 
 // Warps loop over problems; each warp owns one direction area and one

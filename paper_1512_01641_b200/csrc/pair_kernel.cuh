@@ -91,7 +91,7 @@ struct PairSmem {
 // fused-NW scratch inside the overlay: sim tile [64][64] f64, row buffer, directions
 constexpr size_t kNwTileBytes = 64 * 64 * 8;
 constexpr size_t kNwRowBytes = 66 * 8;
-constexpr size_t kNwDirBytes = 2 * 2 * (64 + 31) * 4;  // nw2_dir_words(64, 64)
+constexpr size_t kNwDirBytes = 65 * 5 * 4;
 
 __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_u, int hash_bits, int cap_t,
                                                    PairSmem *s) {
@@ -544,9 +544,9 @@ __global__ void __launch_bounds__(kPairThreads, 3) pair_kernel(const PairArgs A)
   if (warp == 0) {
     double *rowbuf = (double *)(smem_raw + kNwTileBytes);
     uint32_t *dirs = (uint32_t *)(smem_raw + kNwTileBytes + kNwRowBytes);
-    nw_solve2<kNwMine, false>(tile, 64, N, M, A.gap, A.mismatch, A.bonus, A.threshold, dirs, rowbuf,
-                              A.nw_matches + A.nw_out_off[p], nullptr, A.nw_counts + p,
-                              A.nw_score ? A.nw_score + p : nullptr);
+    nw_solve<kNwMine, false>(tile, 64, N, M, A.gap, A.mismatch, A.bonus, A.threshold, nullptr, dirs, rowbuf,
+                             A.nw_matches + A.nw_out_off[p], nullptr, A.nw_counts + p,
+                             A.nw_score ? A.nw_score + p : nullptr);
   }
 }
 
