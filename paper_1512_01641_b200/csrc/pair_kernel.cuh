@@ -464,28 +464,43 @@ __global__ void __launch_bounds__(kPairThreads, 3) pair_kernel(const PairArgs A)
           // translations present in sentence j, added to the running sum
           // (adding +0.0 when absent leaves the non-negative sum unchanged)
           const uint32_t lbit = 1u << lane;  // bit of target jlo in the low word, jhi in the high word
-          int cs = 0;
-          for (int kk = 0; kk < cnt; ++kk) {
-            const uint64_t a = oany[kk];
-            const int n = on[kk];
-            if (a != 0ull) {
-              double bl, bh;
-              const uint64_t m0 = cm[cs];
-              const double p0 = cp[cs];
-              bl = ((uint32_t)m0 & lbit) ? p0 : 0.0;
-              bh = ((uint32_t)(m0 >> 32) & lbit) ? p0 : 0.0;
+          // per-occurrence records in registers of lane k: anyhit, first
+          // candidate, candidate range; only occurrences with a translation
+          // in the chunk are visited (in order)
+          const uint64_t my_any = in_seg ? oany[lane] : 0ull;
+          const int my_n = in_seg ? on[lane] : 0;
+          int my_cs = my_n;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, my_cs, o);
+            if (lane >= o) my_cs += y;
+          }
+          my_cs -= my_n;  // exclusive prefix: first candidate of occurrence `lane`
+          const uint64_t my_m0 = my_n ? cm[my_cs] : 0ull;
+          const double my_p0 = my_n ? cp[my_cs] : 0.0;
+          unsigned rel = __ballot_sync(kFull, my_any != 0ull);
+          while (rel) {
+            const int kk = __ffs(rel) - 1;
+            rel &= rel - 1u;
+            const uint64_t a = __shfl_sync(kFull, my_any, kk);
+            const int n = __shfl_sync(kFull, my_n, kk);
+            const uint64_t m0 = __shfl_sync(kFull, my_m0, kk);
+            const double p0 = __shfl_sync(kFull, my_p0, kk);
+            double bl = ((uint32_t)m0 & lbit) ? p0 : 0.0;
+            double bh = ((uint32_t)(m0 >> 32) & lbit) ? p0 : 0.0;
+            if (n > 1) {
+              const int cs = __shfl_sync(kFull, my_cs, kk);
               for (int c = cs + 1; c < cs + n; ++c) {
                 const uint64_t m = cm[c];
                 const double pr = cp[c];
                 if (((uint32_t)m & lbit) && pr > bl) bl = pr;
                 if (((uint32_t)(m >> 32) & lbit) && pr > bh) bh = pr;
               }
-              sum_lo = fadd(sum_lo, bl);
-              sum_hi = fadd(sum_hi, bh);
-              cov_lo += ((uint32_t)a & lbit) ? 1 : 0;
-              cov_hi += ((uint32_t)(a >> 32) & lbit) ? 1 : 0;
             }
-            cs += n;
+            sum_lo = fadd(sum_lo, bl);
+            sum_hi = fadd(sum_hi, bh);
+            cov_lo += ((uint32_t)a & lbit) ? 1 : 0;
+            cov_hi += ((uint32_t)(a >> 32) & lbit) ? 1 : 0;
           }
           __syncwarp();
           seg += cnt;
