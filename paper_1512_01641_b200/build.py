@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbimine_b200.so")
 SOURCES = ["abi.cu"]
-HEADERS = ["common.cuh", "glibc_exp.cuh", "exp_table.inc", "score_kernel.cuh", "nw_kernel.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".inc", ".h")))
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
