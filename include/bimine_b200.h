@@ -251,6 +251,28 @@ int bimine_mine_host(const bimine_dict *dict, const double *model,
                      int64_t capacity, int64_t *total_host, double *sim_host,
                      void *stream);
 
+/* ---- host tokenizer and joint vocabulary (text.py:97-104) ---------------
+ * A vocabulary maps token strings (UTF-8 bytes) to dense int32 ids; one
+ * vocabulary holds the dictionary's strings and every sentence token, so
+ * id equality is string equality.  bimine_tokenize_batch tokenises n
+ * sentences (buf[off[k] : off[k+1]]) with the reference's rules and
+ * appends their ids to tokens[] (capacity cap); per sentence it writes
+ * len(tokens), len(set(tokens)) and the byte length.  Sentences containing
+ * non-ASCII bytes get len_out = -1 and are left to the caller (Unicode
+ * lower()/split()); everything else is exact. */
+typedef struct bimine_vocab bimine_vocab;
+int bimine_vocab_create(bimine_vocab **out);
+int bimine_vocab_destroy(bimine_vocab *vocab);
+int64_t bimine_vocab_size(const bimine_vocab *vocab);
+int bimine_vocab_add_batch(bimine_vocab *vocab, const char *buf,
+                           const int64_t *off, int64_t n, int32_t *ids_out);
+int bimine_vocab_word(const bimine_vocab *vocab, int32_t id, const char **ptr,
+                      int64_t *len);
+int bimine_tokenize_batch(bimine_vocab *vocab, const char *buf,
+                          const int64_t *off, int64_t n, int32_t *tokens,
+                          int64_t cap, int64_t *n_tokens, int32_t *len_out,
+                          int32_t *uniq_out, int32_t *chars_out);
+
 /* ---- test hook -------------------------------------------------------
  * Device evaluation of the score_from_margin logistic's exp
  * (classifier.py:145-147, glibc __exp_fma restated) over n host doubles;

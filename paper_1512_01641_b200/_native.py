@@ -111,6 +111,13 @@ SIGNATURES = {
                                         ctypes.c_double, ctypes.c_double, _i32p, _vp, ctypes.c_int64, _i64p,
                                         _vp, _vp]),
     "bimine_exp_device": (ctypes.c_int, [_f64p, _f64p, ctypes.c_int64]),
+    "bimine_vocab_create": (ctypes.c_int, [ctypes.POINTER(_vp)]),
+    "bimine_vocab_destroy": (ctypes.c_int, [_vp]),
+    "bimine_vocab_size": (ctypes.c_int64, [_vp]),
+    "bimine_vocab_add_batch": (ctypes.c_int, [_vp, ctypes.c_char_p, _i64p, ctypes.c_int64, _i32p]),
+    "bimine_vocab_word": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_char_p), _i64p]),
+    "bimine_tokenize_batch": (ctypes.c_int, [_vp, ctypes.c_char_p, _i64p, ctypes.c_int64, _i32p, ctypes.c_int64,
+                                             _i64p, _i32p, _i32p, _i32p]),
 }
 
 _lib = None

@@ -109,12 +109,20 @@ def build_score_matrix(model, lexicon, source_sentences: Sequence[str], target_s
     if not source_sentences or not target_sentences:
         raise ValueError("both sentence sequences must be non-empty")
     ctx = _engine.lexicon_context(lexicon)
-    builder = BatchBuilder(ctx.vocab)
-    builder.add_pair(source_sentences, target_sentences)
-    batch = builder.build()
+    batch = _pack_one(ctx.vocab, source_sentences, target_sentences)
     dd = ctx.on(_engine.current_device())
     flat = _engine.score_host(dd, model_vector(model), batch)
     return flat.reshape(len(source_sentences), len(target_sentences))
+
+
+def _pack_one(vocab, source, target) -> PackedBatch:
+    """One pair through the (native) tokenizer; the reference's ValueError
+    messages (align.py:109-119) for empty or untokenizable input."""
+    builder = BatchBuilder(vocab)
+    [res] = builder.add_pairs([(source, target)])
+    if isinstance(res, str):
+        raise ValueError(res)
+    return builder.build()
 
 
 def _steps_from_codes(codes: np.ndarray) -> tuple[Step, ...]:
@@ -204,9 +212,8 @@ def align_pair_indices(model, lexicon, pair, config: MiningConfig, engine: str =
     src, tgt = pair.source.sentences, pair.target.sentences
     if not src or not tgt:
         raise ValueError("both sentence sequences must be non-empty")
-    builder = BatchBuilder(_engine.lexicon_context(lexicon).vocab)
-    builder.add_pair(src, tgt)
-    counts, matches = _mine_packed(model, lexicon, builder.build(), config)
+    batch = _pack_one(_engine.lexicon_context(lexicon).vocab, src, tgt)
+    counts, matches = _mine_packed(model, lexicon, batch, config)
     return [(float(r["score"]), int(r["i"]), int(r["j"])) for r in matches]
 
 
@@ -247,12 +254,12 @@ def mine_corpus(model, lexicon, pairs: Sequence, config: MiningConfig, engine: s
     builder = BatchBuilder(ctx.vocab)
     index_of: list[int] = []  # batch pair -> input pair
     errors: dict[int, str] = {}
-    for k, pair in enumerate(pairs):
-        try:
-            builder.add_pair(pair.source.sentences, pair.target.sentences)
+    results = builder.add_pairs([(p.source.sentences, p.target.sentences) for p in pairs])
+    for k, (pair, res) in enumerate(zip(pairs, results)):
+        if isinstance(res, str):
+            errors[k] = f"pair {pair.topic_id}: {res}"
+        else:
             index_of.append(k)
-        except Exception as exc:
-            errors[k] = f"pair {pair.topic_id}: {exc}" if isinstance(exc, ValueError) else str(exc)
     batch = builder.build()
     per_pair: list = [None] * len(pairs)
     if batch.n_pairs:

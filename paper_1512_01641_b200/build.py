@@ -17,7 +17,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbimine_b200.so")
-SOURCES = ["abi.cu"]
+SOURCES = ["abi.cu", "host_text.cpp"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".inc", ".h")))
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -649,7 +649,6 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     int rc = bimine_plan_batch(h, work.data(), work_cap, &plan);
     if (rc != BIMINE_OK) return rc;
   }
-  const int32_t max_n = plan.max_n, max_m = plan.max_m;
   int64_t cap = 0, cells = 0;
   for (int64_t p = 0; p < P; ++p) {
     const int32_t n = h->pair_n[p], m = h->pair_m[p];
@@ -671,14 +670,13 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
                o_schar = carve(4 * S), o_psrc = carve(8 * P), o_pn = carve(4 * P), o_ptgt = carve(8 * P),
                o_pm = carve(4 * P), o_psim = carve(8 * P), o_outoff = carve(8 * P), o_sim = carve(8 * cells),
                o_slots = carve(sizeof(bimine_match) * cap), o_counts = carve(4 * P), o_base = carve(8 * P),
-               o_comp = carve(sizeof(bimine_match) * cap), o_total = carve(8), o_par = carve(16),
+               o_comp = carve(sizeof(bimine_match) * cap), o_total = carve(8),
                o_work = carve(8 * plan.work_len);
   char *arena = nullptr;
   BIMINE_CUDA(cudaMallocAsync((void **)&arena, off, st));
   auto H2D = [&](size_t o, const void *src, size_t bytes) {
     return bytes ? cudaMemcpyAsync(arena + o, src, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
   };
-  double par[2] = {gap, threshold};
   cudaError_t e = cudaSuccess;
   e = e ? e : H2D(o_tok, h->tokens, 4 * T);
   e = e ? e : H2D(o_soff, h->sent_tok_off, 8 * S);
@@ -691,7 +689,6 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   e = e ? e : H2D(o_pm, h->pair_m, 4 * P);
   e = e ? e : H2D(o_psim, h->pair_sim_off, 8 * P);
   e = e ? e : H2D(o_outoff, out_off.data(), 8 * P);
-  e = e ? e : H2D(o_par, par, 16);
   e = e ? e : H2D(o_work, work.data(), 8 * plan.work_len);
   if (e != cudaSuccess) {
     cudaFreeAsync(arena, st);
@@ -713,8 +710,6 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   d.pair_sim_off = (const int64_t *)(arena + o_psim);
   double *sim = (double *)(arena + o_sim);
   plan.work = (const int64_t *)(arena + o_work);
-  const double *pd = (const double *)(arena + o_par);
-  (void)pd;
   int rc = bimine_mine_batch(dict, model, &d, &plan, gap, threshold, mismatch, bonus, sim,
                              (const int64_t *)(arena + o_outoff), (bimine_match *)(arena + o_slots),
                              (int32_t *)(arena + o_counts), nullptr, stream);

@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .packing import PackedBatch, Vocabulary, lexicon_arrays
+from .packing import PackedBatch, Vocabulary, lexicon_arrays, new_vocabulary
 
 
 def _torch():
@@ -74,7 +74,7 @@ def lexicon_context(lexicon) -> LexiconContext:
         hit = _contexts.get(key)
         if hit is not None and hit[0]() is lexicon:
             return hit[1]
-        vocab = Vocabulary()
+        vocab = new_vocabulary()
         coo = lexicon_arrays(lexicon.items(), vocab)
         ctx = LexiconContext(vocab=vocab, coo=coo, devices={})
         try:

@@ -21,9 +21,10 @@ from .text import tokenize
 
 
 class Vocabulary:
-    """str -> int32 id, grown on demand; one instance per Lexicon."""
+    """str -> int32 id, grown on demand; one instance per Lexicon (Python dict)."""
 
     __slots__ = ("ids", "words")
+    native = False
 
     def __init__(self) -> None:
         self.ids: dict[str, int] = {}
@@ -39,6 +40,102 @@ class Vocabulary:
             self.ids[word] = i
             self.words.append(word)
         return i
+
+    def add_many(self, words) -> np.ndarray:
+        return np.fromiter((self.get(w) for w in words), dtype=np.int32)
+
+
+def _utf8_offsets(strings: list[str]) -> tuple[bytes, np.ndarray]:
+    joined = "".join(strings)
+    data = joined.encode("utf-8", "surrogatepass")
+    off = np.zeros(len(strings) + 1, dtype=np.int64)
+    if len(data) == len(joined):  # all ASCII: byte offsets = character offsets
+        np.cumsum(np.fromiter(map(len, strings), dtype=np.int64, count=len(strings)), out=off[1:])
+    else:
+        np.cumsum(np.fromiter((len(x.encode("utf-8", "surrogatepass")) for x in strings), dtype=np.int64,
+                              count=len(strings)), out=off[1:])
+    return data, off
+
+
+class NativeVocabulary:
+    """The same mapping kept in libbimine_b200.so (bimine_vocab_*), with the
+    native tokenizer (bimine_tokenize_batch) for ASCII sentences."""
+
+    native = True
+
+    def __init__(self) -> None:
+        import ctypes
+
+        from . import _native as N
+
+        self._N = N
+        self._L = N.load(require_gpu=False)
+        h = ctypes.c_void_p()
+        N.check(self._L.bimine_vocab_create(ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                self._L.bimine_vocab_destroy(h)
+            except Exception:
+                pass
+
+    def __len__(self) -> int:
+        return int(self._L.bimine_vocab_size(self._h))
+
+    def add_many(self, words) -> np.ndarray:
+        words = list(words)
+        data, off = _utf8_offsets(words)
+        ids = np.empty(max(len(words), 1), dtype=np.int32)
+        N = self._N
+        N.check(self._L.bimine_vocab_add_batch(self._h, data, N.ptr(off, N._i64p), len(words), N.ptr(ids, N._i32p)))
+        return ids[: len(words)]
+
+    def get(self, word: str) -> int:
+        return int(self.add_many([word])[0])
+
+    def tokenize(self, sentences: list[str]):
+        """(tokens int32, len, uniq, chars) per sentence with the reference's
+        tokenize(); a sentence with no token has len 0."""
+        N = self._N
+        n = len(sentences)
+        data, off = _utf8_offsets(sentences)
+        cap = len(data) // 2 + n + 1
+        tokens = np.empty(cap, dtype=np.int32)
+        lens = np.empty(max(n, 1), dtype=np.int32)
+        uniq = np.empty(max(n, 1), dtype=np.int32)
+        chars = np.empty(max(n, 1), dtype=np.int32)
+        nt = np.zeros(1, dtype=np.int64)
+        N.check(self._L.bimine_tokenize_batch(self._h, data, N.ptr(off, N._i64p), n, N.ptr(tokens, N._i32p), cap,
+                                              N.ptr(nt, N._i64p), N.ptr(lens, N._i32p), N.ptr(uniq, N._i32p),
+                                              N.ptr(chars, N._i32p)))
+        tokens, lens, uniq, chars = tokens[: int(nt[0])], lens[:n], uniq[:n], chars[:n]
+        slow = np.flatnonzero(lens < 0)
+        if slow.size:  # non-ASCII sentences: Python's Unicode rules, same vocabulary
+            starts = np.zeros(n + 1, dtype=np.int64)
+            np.cumsum(np.maximum(lens, 0), out=starts[1:])
+            pieces = []
+            for k in range(n):
+                if lens[k] >= 0:
+                    pieces.append(tokens[starts[k] : starts[k] + lens[k]])
+                else:
+                    ids = self.add_many(tokenize(sentences[k]))
+                    pieces.append(ids)
+                    lens[k] = ids.shape[0]
+                    uniq[k] = len(set(ids.tolist()))
+                    chars[k] = len(sentences[k])
+            tokens = np.concatenate(pieces) if pieces else np.zeros(0, np.int32)
+        return tokens.astype(np.int32, copy=False), lens, uniq, chars
+
+
+def new_vocabulary():
+    """The native vocabulary when libbimine_b200.so is built, else the dict one."""
+    try:
+        return NativeVocabulary()
+    except Exception:
+        return Vocabulary()
 
 
 @dataclass
@@ -177,9 +274,9 @@ def profile_ids(sentence: str, vocab: Vocabulary) -> list[int]:
 class BatchBuilder:
     """Accumulates document pairs (as sentence strings) into a PackedBatch."""
 
-    def __init__(self, vocab: Vocabulary) -> None:
+    def __init__(self, vocab) -> None:
         self.vocab = vocab
-        self.tokens: list[int] = []
+        self.tok_chunks: list[np.ndarray] = []
         self.sent_len: list[int] = []
         self.sent_uniq: list[int] = []
         self.sent_chars: list[int] = []
@@ -207,7 +304,7 @@ class BatchBuilder:
         tgt = self._profiles(target, "target")
         first = len(self.sent_len)
         for ids, text in zip(src + tgt, list(source) + list(target)):
-            self.tokens.extend(ids)
+            self.tok_chunks.append(np.asarray(ids, dtype=np.int32))
             self.sent_len.append(len(ids))
             self.sent_uniq.append(len(set(ids)))
             self.sent_chars.append(len(text))
@@ -217,9 +314,58 @@ class BatchBuilder:
         self.pair_m.append(len(tgt))
         return len(self.pair_n) - 1
 
+    def add_pairs(self, pairs) -> list:
+        """Append many (source_sentences, target_sentences) at once.  Returns,
+        per input pair, its batch index or the ValueError message the
+        reference would raise for it (the pair is then not appended).
+        With a native vocabulary the sentences are tokenised in one call."""
+        if not getattr(self.vocab, "native", False):
+            out = []
+            for src, tgt in pairs:
+                try:
+                    out.append(self.add_pair(src, tgt))
+                except ValueError as exc:
+                    out.append(str(exc))
+            return out
+        if not pairs:
+            return []
+        pairs = [(list(src), list(tgt)) for src, tgt in pairs]
+        flat = [x for src, tgt in pairs for x in src + tgt]
+        tokens, lens, uniq, chars = self.vocab.tokenize(flat)
+        tstart = np.zeros(len(flat) + 1, dtype=np.int64)
+        np.cumsum(lens, out=tstart[1:])
+        out, k = [], 0
+        keep_tok, keep_sent = [], []
+        for src, tgt in pairs:
+            ns, nt = len(src), len(tgt)
+            span = range(k, k + ns + nt)
+            k += ns + nt
+            if not src or not tgt:
+                out.append("both sentence sequences must be non-empty")
+                continue
+            bad = next((x for x in span if lens[x] == 0), None)
+            if bad is not None:
+                side, index = ("source", bad - span.start) if bad - span.start < ns else ("target", bad - span.start - ns)
+                out.append(f"{side} sentence {index}: untokenizable sentence: {flat[bad]!r}")
+                continue
+            first = len(self.sent_len)
+            keep_sent.append(span)
+            keep_tok.append((tstart[span.start], tstart[span.stop]))
+            self.sent_len.extend(lens[span.start : span.stop].tolist())
+            self.sent_uniq.extend(uniq[span.start : span.stop].tolist())
+            self.sent_chars.extend(chars[span.start : span.stop].tolist())
+            self.pair_src.append(first)
+            self.pair_n.append(ns)
+            self.pair_tgt.append(first + ns)
+            self.pair_m.append(nt)
+            out.append(len(self.pair_n) - 1)
+        for a, b in keep_tok:
+            self.tok_chunks.append(tokens[a:b])
+        return out
+
     def build(self) -> PackedBatch:
         return PackedBatch.from_token_lengths(
-            np.asarray(self.tokens, dtype=np.int32),
+            np.concatenate(self.tok_chunks) if self.tok_chunks else np.zeros(0, np.int32),
             np.asarray(self.sent_len, dtype=np.int32),
             np.asarray(self.sent_chars, dtype=np.int32),
             np.asarray(self.pair_src, dtype=np.int64),
@@ -230,16 +376,17 @@ class BatchBuilder:
         )
 
 
-def lexicon_arrays(entries: Iterable[tuple[str, str, float]], vocab: Vocabulary):
+def lexicon_arrays(entries: Iterable[tuple[str, str, float]], vocab):
     """COO (src, tgt, prob) arrays of a lexicon in its iteration order."""
-    src, tgt, prob = [], [], []
-    get = vocab.get
+    ss, ts, ps = [], [], []
     for s, t, p in entries:
-        src.append(get(s))
-        tgt.append(get(t))
-        prob.append(float(p))
+        ss.append(s)
+        ts.append(t)
+        ps.append(float(p))
+    words = [w for pair in zip(ss, ts) for w in pair]
+    ids = vocab.add_many(words) if words else np.zeros(0, np.int32)
     return (
-        np.asarray(src, dtype=np.int32),
-        np.asarray(tgt, dtype=np.int32),
-        np.asarray(prob, dtype=np.float64),
+        np.ascontiguousarray(ids[0::2], dtype=np.int32),
+        np.ascontiguousarray(ids[1::2], dtype=np.int32),
+        np.asarray(ps, dtype=np.float64),
     )

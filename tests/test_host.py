@@ -176,3 +176,57 @@ def test_shard_bounds_cover_in_order():
         assert b[0][0] == 0 and b[-1][1] == len(w)
         assert all(x[1] == y[0] for x, y in zip(b, b[1:]))
         assert len(b) <= parts
+
+
+def _native_vocab():
+    from paper_1512_01641_b200 import build
+    from paper_1512_01641_b200.packing import NativeVocabulary
+
+    build.build()
+    return NativeVocabulary()
+
+
+def test_native_tokenizer_matches_python_rules():
+    """bimine_tokenize_batch == text.tokenize (text.py:97-104) on ASCII and,
+    through the Python path, on non-ASCII sentences; same vocabulary ids."""
+    import random
+
+    v = _native_vocab()
+    rng = random.Random(5)
+    alphabet = "abcXYZ019 .,;:!?'\"()[]-_\t\n\x0b\x0c\r\x1c\x1d\x1e\x1f\x00~`@#$%^&*+=<>/\\|{}"
+    sents = ["".join(rng.choice(alphabet) for _ in range(rng.randint(0, 40))) for _ in range(3000)]
+    sents += ["Żółw «ok» x", "ǅ ab", "naïve café.", " a　b\x85c", "İstanbul"]
+    tokens, lens, uniq, chars = v.tokenize(sents)
+    pos = 0
+    for s, L, U, C in zip(sents, lens.tolist(), uniq.tolist(), chars.tolist()):
+        want = tokenize(s)
+        got = tokens[pos : pos + L].tolist()
+        pos += L
+        assert [v.get(w) for w in want] == got, s
+        assert U == len(set(want)) and C == len(s)
+    assert pos == tokens.shape[0]
+
+
+def test_native_and_python_builders_agree():
+    from paper_1512_01641_b200.packing import BatchBuilder, Vocabulary
+
+    corpus = synth.make_config(2, n_pairs=4)
+    pairs = [corpus.pair_sentences(p) for p in range(4)]
+    pairs.insert(2, (["ok s1."], ["...", "t2"]))  # untokenizable target sentence
+    pairs.insert(3, ([], ["t2"]))
+    nb = BatchBuilder(_native_vocab())
+    pb = BatchBuilder(Vocabulary())
+    rn = nb.add_pairs(pairs)
+    rp = pb.add_pairs(pairs)
+    assert rn == rp
+    assert rn[2] == "target sentence 0: untokenizable sentence: '...'"
+    assert rn[3] == "both sentence sequences must be non-empty"
+    a, b = nb.build(), pb.build()
+    for f in ("sent_len", "sent_uniq", "sent_chars", "pair_src", "pair_n", "pair_tgt", "pair_m", "pair_sim_off"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    # ids differ between vocabularies only by renaming: compare token strings
+    pv = pb.vocab.words
+    inv = {}
+    for w in set(pv):
+        inv[nb.vocab.get(w)] = w
+    assert [inv[t] for t in a.tokens.tolist()] == [pv[t] for t in b.tokens.tolist()]
