@@ -145,6 +145,7 @@ typedef struct bimine_plan {
   int64_t n_long;              /* pairs for the fallback kernel           */
   int32_t long_max_n, long_max_m;
   int64_t n_large;             /* pairs not in the one-CTA-per-pair launch */
+  int64_t n_cells;             /* extent of sim: max pair_sim_off + N * M  */
   int64_t work_len;            /* 3 * n_tiles + n_long + n_large          */
   const int64_t *work;         /* device copy of work_host (set by caller)*/
 } bimine_plan;

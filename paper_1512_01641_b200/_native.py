@@ -77,6 +77,7 @@ class CPlan(ctypes.Structure):
         ("long_max_n", ctypes.c_int32),
         ("long_max_m", ctypes.c_int32),
         ("n_large", ctypes.c_int64),
+        ("n_cells", ctypes.c_int64),
         ("work_len", ctypes.c_int64),
         ("work", _vp),
     ]

@@ -195,6 +195,8 @@ int bimine_plan_batch(const bimine_batch *b, int64_t *work, int64_t work_cap, bi
   }
   std::vector<int64_t> longs, larges;
   int64_t t = 0;
+  for (int64_t p = 0; p < b->n_pairs; ++p)
+    P.n_cells = std::max(P.n_cells, b->pair_sim_off[p] + (int64_t)b->pair_n[p] * b->pair_m[p]);
   for (int64_t p = 0; p < b->n_pairs; ++p) {
     const int32_t n = b->pair_n[p], m = b->pair_m[p];
     if (n < 1 || m < 1) return fail(BIMINE_E_ARG, "bimine_plan_batch: empty document");
@@ -310,6 +312,9 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
     int rc = term_tables(model, st, &A.T);
     if (rc != BIMINE_OK) return rc;
     A.sim = sim_dev;
+    // per-cell counters scratch (L2 resident while a CTA works on it)
+    const int64_t cells = plan->n_cells;
+    BIMINE_CUDA(cudaMallocAsync((void **)&A.aux, sizeof(uint16_t) * std::max<int64_t>(cells, 1), st));
     A.cap_u = 1024;
     A.hash_bits = 11;
     A.cap_t = 2048;
@@ -335,7 +340,9 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
     const int64_t grid = plan->n_tiles + b->n_pairs;
     if (grid > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: too many CTAs");
     pair_kernel<<<(unsigned)grid, kPairThreads, smem, st>>>(A);
-    BIMINE_CUDA(cudaGetLastError());
+    const cudaError_t le = cudaGetLastError();
+    cudaFreeAsync(A.aux, st);
+    if (le != cudaSuccess) return fail(BIMINE_E_CUDA, std::string("pair_kernel: ") + cudaGetErrorString(le));
   }
   if (plan->n_long > 0) {
     ScoreArgs A;

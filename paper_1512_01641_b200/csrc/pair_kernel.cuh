@@ -51,6 +51,7 @@ struct PairArgs {
   Model md;
   TermTables T;
   double *sim;
+  uint16_t *aux;            // per-cell scratch, same layout as sim: covered | shared << 8
   const int64_t *tiles;     // (pair, i0, j0) per tile of the pairs larger than 64x64
   int64_t n_tiles;          // CTAs [0, n_tiles) are tiles, the rest one pair each
   int cap_u;                // distinct target tokens per chunk (dense arrays)
@@ -84,7 +85,7 @@ struct PairSmem {
   int32_t *misc;       // [8]: 0 distinct count, 1 chunk end, 2 D work counter, 3 C work counter
   int16_t *dense;      // [slots]
   int16_t *tgt_d;      // [cap_t]
-  uint8_t *cov, *covt, *shr;  // [64][64]
+  uint8_t *covt;       // [64][64]
   size_t overlay_bytes;  // bytes of the reusable region at the start
 };
 
@@ -129,9 +130,7 @@ __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_
   t.tgt_chars = (int32_t *)take(64 * 4, 4);
   t.tgt_occ0 = (int32_t *)take(65 * 4, 4);
   t.misc = (int32_t *)take(8 * 4, 4);
-  t.cov = (uint8_t *)take(64 * 64, 4);
   t.covt = (uint8_t *)take(64 * 64, 4);
-  t.shr = (uint8_t *)take(64 * 64, 4);
   if (s) *s = t;
   return (o + 15) / 16 * 16;
 }
@@ -190,7 +189,7 @@ __host__ __device__ inline bool pair_is_small(int n, int m, int max_len) {
   return n <= kPairMax && m <= kPairMax && max_len <= kPairMaxLen;
 }
 
-__global__ void __launch_bounds__(kPairThreads, 3) pair_kernel(const PairArgs A) {
+__global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // CTAs [0, n_tiles) take the 64x64 tiles of large pairs (first, so the
   // long pairs start early), the rest one pair each (pairs larger than
@@ -222,6 +221,7 @@ __global__ void __launch_bounds__(kPairThreads, 3) pair_kernel(const PairArgs A)
   const int hslots = 1 << hbits;
   // the block's cell (i, j) lives at out[i * Mfull + j]; also the running-sum scratch
   double *__restrict__ out = A.sim + A.b.pair_sim_off[p] + (int64_t)i0 * Mfull + j0;
+  uint16_t *__restrict__ aux = A.aux + A.b.pair_sim_off[p] + (int64_t)i0 * Mfull + j0;
 
   // ---- 0: tables and sentence metadata
   for (int k = tid; k < 256; k += kPairThreads) S.exp_tab[k] = kExpTableDev[k];
@@ -506,13 +506,11 @@ __global__ void __launch_bounds__(kPairThreads, 3) pair_kernel(const PairArgs A)
           seg += cnt;
         }
         if (jlo < nj) {
-          S.cov[i * kCellStride + jc0 + jlo] = (uint8_t)cov_lo;
-          S.shr[i * kCellStride + jc0 + jlo] = (uint8_t)sh_lo;
+          aux[(int64_t)i * Mfull + jc0 + jlo] = (uint16_t)(cov_lo | (sh_lo << 8));
           out[(int64_t)i * Mfull + jc0 + jlo] = sum_lo;
         }
         if (jhi < nj) {
-          S.cov[i * kCellStride + jc0 + jhi] = (uint8_t)cov_hi;
-          S.shr[i * kCellStride + jc0 + jhi] = (uint8_t)sh_hi;
+          aux[(int64_t)i * Mfull + jc0 + jhi] = (uint16_t)(cov_hi | (sh_hi << 8));
           out[(int64_t)i * Mfull + jc0 + jhi] = sum_hi;
         }
       }
@@ -547,8 +545,10 @@ __global__ void __launch_bounds__(kPairThreads, 3) pair_kernel(const PairArgs A)
     const int i = c / M, j = c - i * M;
     const int x = i * kCellStride + j;
     const int64_t o = (int64_t)i * Mfull + j;
+    const uint32_t ax = aux[o];
     const double v = cell_score_t(A.md, A.T, S.src_len[i], S.src_uniq[i], S.src_chars[i], S.tgt_len[j],
-                                  S.tgt_uniq[j], S.tgt_chars[j], S.cov[x], out[o], S.covt[x], S.shr[x], S.exp_tab);
+                                  S.tgt_uniq[j], S.tgt_chars[j], (int)(ax & 0xffu), out[o], S.covt[x],
+                                  (int)(ax >> 8), S.exp_tab);
     out[o] = v;
     if (fuse_nw) tile[i * 64 + j] = v;
   }
