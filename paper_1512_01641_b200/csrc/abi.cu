@@ -408,7 +408,27 @@ int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
     BIMINE_CUDA(cudaGetLastError());
     return BIMINE_OK;
   }
-  // global scratch: one slot per launched warp, bounded to ~2 GiB
+  if (MODE != kNwTable) {
+    // large problems: one CTA each, warps pipelined over row bands
+    const int64_t G = (max_n + 31) / 32, T = (int64_t)max_m + 31;
+    const int64_t stride = 2 * G * T;  // u32 direction words per problem (worst case)
+    const int64_t nprob = A.n_problems;
+    uint32_t *dirs = nullptr;
+    int64_t *offs = nullptr;
+    BIMINE_CUDA(cudaMallocAsync((void **)&dirs, sizeof(uint32_t) * stride * nprob, st));
+    BIMINE_CUDA(cudaMallocAsync((void **)&offs, sizeof(int64_t) * nprob, st));
+    std::vector<int64_t> h(nprob);
+    for (int64_t k = 0; k < nprob; ++k) h[k] = k * stride;
+    BIMINE_CUDA(cudaMemcpyAsync(offs, h.data(), sizeof(int64_t) * nprob, cudaMemcpyHostToDevice, st));
+    if (nprob > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "nw: too many large problems");
+    nw_big_kernel<MODE><<<(unsigned)nprob, kBigWarps * 32, 0, st>>>(A, dirs, offs);
+    const cudaError_t e = cudaGetLastError();
+    cudaFreeAsync(dirs, st);
+    cudaFreeAsync(offs, st);
+    if (e != cudaSuccess) return fail(BIMINE_E_CUDA, std::string("nw_big_kernel: ") + cudaGetErrorString(e));
+    return BIMINE_OK;
+  }
+  // table mode (B1 shim): global scratch, one slot per launched warp, bounded to ~2 GiB
   if (dir_w >= (1LL << 31)) return fail(BIMINE_E_LIMIT, "nw: alignment table too large");
   int64_t warps = std::min<int64_t>(A.n_problems, (int64_t)num_sms() * 16);
   warps = std::max<int64_t>(1, std::min<int64_t>(warps, (int64_t)((size_t)2 << 30) / (int64_t)per_warp));

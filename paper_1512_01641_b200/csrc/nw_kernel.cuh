@@ -413,3 +413,257 @@ __global__ void __launch_bounds__(128) agree_kernel(const AgreeArgs A) {
 }
 
 }  // namespace bimine
+
+namespace bimine {
+
+// ---- large problems: one CTA, warps pipelined over 32-row bands ----------
+//
+// For pairs too big for a warp's shared memory (C1 200x220, C3 4096x4096):
+// band g (rows 32g+1 .. 32g+32 of the reversed table) runs on warp g % W
+// with the same lane-per-row anti-diagonal sweep as nw_solve; the band's
+// upper boundary (row 32g) streams from the warp that owns band g-1
+// through a per-boundary shared-memory ring (producer/consumer positions,
+// monotonic across the bands that reuse the ring), so W bands advance
+// together a few columns apart.  Each lane prefetches its sim row into L1
+// a line ahead (prefetch.global.L1) and loads it 8 steps ahead into
+// registers.  Directions are stored per (band, step) as two ballot words
+// (bit l = lane l's cell), written coalesced; the traceback walks them on
+// lane 0 from a 64-step window staged by the whole warp, and the match
+// scores are gathered in parallel afterwards.
+constexpr int kBigWarps = 16;
+constexpr int kRing = 256;  // boundary values buffered per ring
+
+struct BigRing {
+  double v[kRing];
+  volatile long long prod;  // positions written  (gen * (M+1) + b, exclusive)
+  volatile long long cons;  // positions consumed
+};
+
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, uint32_t *g_dirs_all,
+                                                                 const int64_t *dir_off) {
+  __shared__ BigRing rings[kBigWarps];
+  __shared__ int band_done;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t q = A.problem_ids ? A.problem_ids[blockIdx.x] : (int64_t)blockIdx.x;
+  const int64_t pair = q / A.n_settings;
+  const int setting = (int)(q % A.n_settings);
+  const int N = A.pair_n[pair], M = A.pair_m[pair];
+  const double *__restrict__ sim = A.sim + A.sim_off[pair];
+  const double gap = A.gap_per_problem ? A.gap[q] : A.gap[setting];
+  const double ng = -gap, mismatch = A.mismatch, span = fsub(A.bonus, A.mismatch);
+  const int G = (N + 31) >> 5, T = M + 31;
+  uint32_t *dirs = g_dirs_all + dir_off[blockIdx.x];  // [G][T][2]
+  if (threadIdx.x < kBigWarps) {
+    rings[threadIdx.x].prod = 0;
+    rings[threadIdx.x].cons = 0;
+  }
+  if (threadIdx.x == 0) band_done = 0;
+  __syncthreads();
+  const long long W1 = (long long)M + 1;
+  double last = 0.0;
+  for (int g = warp, gen = 0; g < G; g += kBigWarps, ++gen) {
+    BigRing &in = rings[warp];                     // boundary row 32g (from band g-1)
+    BigRing &outr = rings[(warp + 1) % kBigWarps];  // boundary row 32g+32 (for band g+1)
+    const int out_gen = (g + 1) / kBigWarps;        // generation of band g+1 on its ring
+    const int a = 32 * g + 1 + lane;
+    const bool active = a <= N;
+    const double left0 = fmul(ng, (double)a);
+    double cur = left0;
+    // dp[32g][0] for lane 0's first diagonal, dp[a-1][0] for the others
+    double diag = __shfl_up_sync(kFull, left0, 1);
+    if (lane == 0) diag = fmul(ng, (double)(32 * g));
+    const double *srow = sim + (int64_t)(N - a) * M + (M - 1);
+    auto ldr = [&](int b) -> double {
+      return (active && b >= 1 && b <= M) ? __ldg(srow - (b - 1)) : 0.0;
+    };
+    double cur8[8], nxt8[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) nxt8[u] = ldr(u - lane + 1);
+    const int nsteps = M + 31;
+    for (int s0 = 0; s0 < nsteps; s0 += 8) {
+      if (active && ((s0 - lane + 1) & 15) < 8) prefetch_l1(srow - min(max(s0 - lane + 1 + 32, 0), M - 1));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) cur8[u] = nxt8[u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) nxt8[u] = ldr(s0 + 8 + u - lane + 1);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int s = s0 + u;
+        if (s >= nsteps) break;
+        const int b = s - lane + 1;
+        double up = __shfl_up_sync(kFull, cur, 1);
+        if (lane == 0 && b >= 1 && b <= M) {
+          // row 32g, columns b and b-1: kernels.py:46 for band 0, else the ring
+          if (g == 0) {
+            up = fmul(ng, (double)b);
+            diag = fmul(ng, (double)(b - 1));
+          } else {
+            const long long pos = (long long)gen * W1 + b;  // position of column b
+            while (in.prod <= pos) {
+            }
+            __threadfence_block();
+            up = in.v[pos % kRing];
+            if (b == 1) diag = fmul(ng, (double)(32 * g));
+            else diag = in.v[(pos - 1) % kRing];
+            if ((b & 15) == 0 || b == M) in.cons = pos;  // release ring space (keeps b-1's value)
+          }
+        }
+        uint32_t dir = 0u;
+        double best = 0.0;
+        const bool valid = active && b >= 1 && b <= M;
+        if (valid) {
+          const double c = fadd(mismatch, fmul(cur8[u], span));
+          best = fadd(diag, c);
+          double cand = fsub(up, gap);
+          if (cand > best) {
+            best = cand;
+            dir = 1u;
+          }
+          cand = fsub(cur, gap);
+          if (cand > best) {
+            best = cand;
+            dir = 2u;
+          }
+          cur = best;
+          if (a == N && b == M) last = best;
+        }
+        if (lane == 31 && valid && g + 1 < G) {
+          const long long pos = (long long)out_gen * W1 + b;
+          while (pos - outr.cons >= kRing - 1) {
+          }
+          outr.v[pos % kRing] = best;
+          __threadfence_block();
+          if ((b & 7) == 0 || b == M) outr.prod = pos + 1;
+        }
+        if (lane > 0) diag = up;
+        const uint32_t lo = __ballot_sync(kFull, valid && (dir & 1u));
+        const uint32_t hi = __ballot_sync(kFull, valid && (dir & 2u));
+        if (lane == 0) {
+          dirs[2 * ((int64_t)g * T + s)] = lo;
+          dirs[2 * ((int64_t)g * T + s) + 1] = hi;
+        }
+      }
+    }
+    if (lane == 0 && g > 0) in.cons = (long long)gen * W1 + M + 1;
+    if (lane == 31 && g + 1 < G) outr.prod = (long long)out_gen * W1 + M + 1;  // flush
+    __syncwarp();
+  }
+  // dp[N][M] from the lane owning row N (its warp)
+  const int owner_warp = ((N - 1) >> 5) % kBigWarps;
+  __shared__ double s_last;
+  if (warp == owner_warp && lane == ((N - 1) & 31)) s_last = last;
+  __syncthreads();
+  if (MODE == kNwTable) return;
+  // ---- traceback on warp 0: lane 0 walks, the warp stages 64 steps of the
+  // current band at a time
+  if (warp == 0) {
+    __shared__ uint32_t win[2][64];
+    __shared__ int win_g, win_t0;
+    int a = N, b = M;
+    int64_t cnt = 0;
+    bimine_match *outm = (MODE == kNwMine) ? A.matches + A.out_off[q] : nullptr;
+    uint8_t *st = (MODE == kNwSteps) ? A.steps + A.step_off[q] : nullptr;
+    if (lane == 0) {
+      win_g = -1;
+      win_t0 = 0;
+    }
+    __syncwarp();
+    while (true) {
+      // every lane agrees on (a, b): lane 0 broadcasts
+      a = __shfl_sync(kFull, a, 0);
+      b = __shfl_sync(kFull, b, 0);
+      if (!(a > 0 && b > 0)) break;
+      const int g = (a - 1) >> 5, l = (a - 1) & 31, t = b + l - 1;
+      const bool miss = !(g == win_g && t >= win_t0 && t < win_t0 + 64);
+      if (miss) {  // stage steps [t-63, t] of band g
+        const int t0 = max(0, t - 63);
+        for (int k = lane; k < 64; k += 32) {
+          const int tt = t0 + k;
+          const bool ok = tt < T;
+          win[0][k] = ok ? __ldcg(dirs + 2 * ((int64_t)g * T + tt)) : 0u;
+          win[1][k] = ok ? __ldcg(dirs + 2 * ((int64_t)g * T + tt) + 1) : 0u;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          win_g = g;
+          win_t0 = t0;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        // walk while inside the window
+        while (a > 0 && b > 0) {
+          const int gg = (a - 1) >> 5, ll = (a - 1) & 31, tt = b + ll - 1;
+          if (gg != win_g || tt < win_t0 || tt >= win_t0 + 64) break;
+          const uint32_t d = ((win[0][tt - win_t0] >> ll) & 1u) | (((win[1][tt - win_t0] >> ll) & 1u) << 1);
+          if (d == 0u) {
+            if (MODE == kNwMine) {
+              outm[cnt].i = N - a;  // score filled below
+              outm[cnt].j = M - b;
+              ++cnt;
+            } else {
+              st[cnt++] = 0u;
+            }
+            --a;
+            --b;
+          } else if (d == 1u) {
+            if (MODE == kNwSteps) st[cnt++] = 1u;
+            --a;
+          } else {
+            if (MODE == kNwSteps) st[cnt++] = 2u;
+            --b;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    cnt = __shfl_sync(kFull, cnt, 0);
+    if (MODE == kNwSteps) {
+      if (lane == 0) {
+        while (a > 0) {
+          st[cnt++] = 1u;
+          --a;
+        }
+        while (b > 0) {
+          st[cnt++] = 2u;
+          --b;
+        }
+        A.n_steps[q] = (int32_t)cnt;
+      }
+    } else {
+      // gather the scores in parallel, keep those at or above the threshold
+      const double thr = A.threshold[setting];
+      int64_t kept = 0;
+      for (int64_t base = 0; base < cnt; base += 32) {
+        const int64_t c = base + lane;
+        double v = 0.0;
+        int32_t i = 0, j = 0;
+        if (c < cnt) {
+          i = outm[c].i;
+          j = outm[c].j;
+          v = sim[(int64_t)i * M + j];
+        }
+        const bool keep = c < cnt && v >= thr;
+        const unsigned bal = __ballot_sync(kFull, keep);
+        __syncwarp();
+        if (keep) {
+          bimine_match &o = outm[kept + __popc(bal & ((1u << lane) - 1u))];
+          o.score = v;
+          o.i = i;
+          o.j = j;
+        }
+        kept += __popc(bal);
+        __syncwarp();
+      }
+      if (lane == 0) A.counts[q] = (int32_t)kept;
+    }
+    if (lane == 0 && A.score) A.score[q] = s_last;
+  }
+}
+
+}  // namespace bimine

@@ -413,3 +413,16 @@ def test_fused_nw_tail_matches_standalone(monkeypatch):
     res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-2000:]
+
+
+@pytest.mark.parametrize("shape", [(1500, 1700), (2100, 97), (96, 2100)])
+def test_nw_large_problems_band_pipeline(shape):
+    """Problems handled by the CTA-per-problem band pipeline (ring buffers
+    between warps): steps, score and mined matches equal the oracle."""
+    rng = np.random.default_rng(shape[0])
+    sims = [rng.random(shape), (rng.random(shape) > 0.7).astype(np.float64)]
+    out = E.nw_steps_host(sims, [1.3, 0.5], -1.0, 1.0)
+    for sim, g, (codes, score) in zip(sims, [1.3, 0.5], out):
+        want, _, _, want_score = oracle.nw_align(sim, -1.0, 1.0, g)
+        assert np.array_equal(codes, want)
+        assert bits_equal(score, want_score)
