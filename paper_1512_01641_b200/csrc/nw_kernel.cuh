@@ -447,7 +447,6 @@ template <int MODE>
 __global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, uint32_t *g_dirs_all,
                                                                  const int64_t *dir_off) {
   __shared__ BigRing rings[kBigWarps];
-  __shared__ int band_done;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q = A.problem_ids ? A.problem_ids[blockIdx.x] : (int64_t)blockIdx.x;
   const int64_t pair = q / A.n_settings;
@@ -458,13 +457,15 @@ __global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, 
   const double ng = -gap, mismatch = A.mismatch, span = fsub(A.bonus, A.mismatch);
   const int G = (N + 31) >> 5, T = M + 31;
   uint32_t *dirs = g_dirs_all + dir_off[blockIdx.x];  // [G][T][2]
+  const long long W1 = (long long)M + 1;
   if (threadIdx.x < kBigWarps) {
     rings[threadIdx.x].prod = 0;
-    rings[threadIdx.x].cons = 0;
+    // band 0 takes its boundary from kernels.py:46 and never reads ring 0, so
+    // ring 0's generation 0 starts consumed (else band kBigWarps-1 would
+    // wait for space forever)
+    rings[threadIdx.x].cons = threadIdx.x == 0 ? W1 : 0;
   }
-  if (threadIdx.x == 0) band_done = 0;
   __syncthreads();
-  const long long W1 = (long long)M + 1;
   double last = 0.0;
   for (int g = warp, gen = 0; g < G; g += kBigWarps, ++gen) {
     BigRing &in = rings[warp];                     // boundary row 32g (from band g-1)
