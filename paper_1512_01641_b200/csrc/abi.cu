@@ -387,13 +387,15 @@ namespace {
 template <int MODE>
 int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
   if (A.n_problems == 0) return BIMINE_OK;
-  const int row_d = ((max_m + 1) + 1) & ~1;                      // doubles, even
-  const int64_t dir_w = (int64_t)(max_n + 1) * ((max_m >> 4) + 1);  // u32 words
+  const int row_d = ((max_m + 1) + 1) & ~1;  // doubles, even
+  const int64_t dir_w = (MODE == kNwTable) ? 0 : (lean_dir_words16(max_n, max_m) + 1) / 2;  // u32 words
   const size_t per_warp = (size_t)row_d * 8 + (size_t)dir_w * 4;
   A.row_doubles_per_warp = row_d;
   if (MODE == kNwTable) A.dir_words_per_warp = 0;
   const size_t per_block = per_warp * kNwWarpsPerBlock;
-  if (MODE != kNwTable && dir_w < (1LL << 31) && per_block <= kNwSmemPerBlockMax) {
+  // one warp per problem for small problems; problems taller than 64 rows
+  // go to the band pipeline (one CTA each)
+  if (MODE != kNwTable && max_n <= 64 && dir_w < (1LL << 31) && per_block <= kNwSmemPerBlockMax) {
     A.dir_words_per_warp = (int)dir_w;
     A.g_dirs = nullptr;
     A.g_rows = nullptr;
@@ -410,8 +412,7 @@ int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
   }
   if (MODE != kNwTable) {
     // large problems: one CTA each, warps pipelined over row bands
-    const int64_t G = (max_n + 31) / 32, T = (int64_t)max_m + 31;
-    const int64_t stride = 2 * G * T;  // u32 direction words per problem (worst case)
+    const int64_t stride = (lean_dir_words16(max_n, max_m) + 1) / 2;  // u32 words per problem (worst case)
     const int64_t nprob = A.n_problems;
     uint32_t *dirs = nullptr;
     int64_t *offs = nullptr;

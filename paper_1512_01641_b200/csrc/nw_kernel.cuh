@@ -216,6 +216,199 @@ __device__ __forceinline__ void nw_solve(const double *__restrict__ sim, int ld,
   __syncwarp();
 }
 
+// ---- the lean band sweep -------------------------------------------------
+//
+// One 32-row band (rows a0+1 .. a0+32 of the reversed table, lane l owns
+// row a0+1+l) swept over all columns: at step s lane l computes column
+// b = s - l + 1.  Everything that does not depend on the neighbour's
+// value is prepared once per group of 8 steps, off the dependency chain:
+// the 8 R values (loaded 8 steps ahead), c = mismatch + R * span, the
+// valid-step mask and lane 0's 9 boundary values dp[a0][s0 .. s0+8]
+// (from `top`, which may wait for a producer).  A step is then a shuffle,
+// three adds, two compares and selects.  Directions: per lane and group
+// one u16 (2 bits per step), dirs_band[group * 32 + lane] -- coalesced.
+// The band's last row (lane 31) goes to `bot` one value per step.
+// Returns the lane's final value dp[row][M] (cur after the sweep).
+__host__ __device__ inline int nw_groups(int M) { return (M + 31 + 7) >> 3; }
+
+template <bool kGlobal, class Top, class Bot>
+__device__ __forceinline__ double band_sweep(const double *__restrict__ sim, int ld, int N, int M, int a0, double gap,
+                                             double mismatch, double span, Top &top, Bot &bot,
+                                             uint16_t *__restrict__ dirs_band) {
+  const int lane = threadIdx.x & 31;
+  const int a = a0 + 1 + lane;
+  const bool active = a <= N;
+  const double ng = -gap;
+  const double left0 = fmul(ng, (double)a);  // dp[a][0] (kernels.py:47)
+  double cur = left0;
+  double diag = __shfl_up_sync(kFull, left0, 1);  // dp[a-1][0] for lanes > 0
+  const double *srow = sim + (int64_t)(N - (active ? a : N)) * ld + (M - 1);
+  auto ldr = [&](int b) -> double {
+    if (!(active && b >= 1 && b <= M)) return 0.0;
+    const double *q = srow - (b - 1);
+    return kGlobal ? __ldg(q) : *q;
+  };
+  const int nsteps = M + 31;
+  double nxt[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) nxt[u] = ldr(u - lane + 1);
+  for (int s0 = 0, grp = 0; s0 < nsteps; s0 += 8, ++grp) {
+    double c[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) c[u] = fadd(mismatch, fmul(nxt[u], span));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) nxt[u] = ldr(s0 + 8 + u - lane + 1);
+    // steps s0+u with 1 <= b <= M for this lane
+    const int lo = max(lane - s0, 0), hi = min(lane + M - 1 - s0, 7);
+    const uint32_t vmask = (active && lo <= hi) ? (((2u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
+    double rb[9];
+    top.load9(s0, rb);  // lane 0: dp[a0][s0 .. s0+8]
+    uint32_t bits = 0u;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      double up = __shfl_up_sync(kFull, cur, 1);
+      if (lane == 0) {
+        up = rb[u + 1];
+        diag = rb[u];
+      }
+      double best = fadd(diag, c[u]);
+      const double t1 = fsub(up, gap);
+      const bool p1 = t1 > best;
+      best = p1 ? t1 : best;
+      const double t2 = fsub(cur, gap);
+      const bool p2 = t2 > best;
+      best = p2 ? t2 : best;
+      const bool v = (vmask >> u) & 1u;
+      cur = v ? best : cur;
+      bits |= (p2 ? 2u : (p1 ? 1u : 0u)) << (2 * u);
+      bot.put(s0 + u, v, best);  // lane 31's cell of row a0+32, column s0+u-30
+      diag = up;
+    }
+    dirs_band[grp * 32 + lane] = (uint16_t)bits;
+  }
+  return cur;
+}
+
+// traceback direction of reversed cell (a, b) from band-sweep directions
+__device__ __forceinline__ uint32_t lean_dir(const uint16_t *dirs, int G8, int a, int b) {
+  const int g = (a - 1) >> 5, l = (a - 1) & 31, s = b + l - 1;
+  return ((uint32_t)dirs[((int64_t)g * G8 + (s >> 3)) * 32 + l] >> (2 * (s & 7))) & 3u;
+}
+
+// boundary providers / consumers for band_sweep
+struct TopAnalytic {  // row 0: -gap * b (kernels.py:46)
+  double ng;
+  __device__ void load9(int s0, double *rb) const {
+#pragma unroll
+    for (int u = 0; u < 9; ++u) rb[u] = fmul(ng, (double)(s0 + u));
+  }
+};
+struct TopRow {  // a row buffer rowbuf[0..M] (the previous band's last row)
+  const double *row;
+  int M;
+  __device__ void load9(int s0, double *rb) const {
+#pragma unroll
+    for (int u = 0; u < 9; ++u) rb[u] = row[min(s0 + u, M)];
+  }
+};
+struct BotRow {  // lane 31 writes row[b] for the next band
+  double *row;
+  int M;
+  bool on;
+  __device__ void put(int s, bool v, double best) const {
+    if (on && v && (threadIdx.x & 31) == 31) row[s - 30] = best;
+  }
+};
+struct BotNone {
+  __device__ void put(int, bool, double) const {}
+};
+
+// Single-warp solve of a problem that fits one warp's scratch: bands in
+// sequence through a row buffer (M+1 doubles); directions in dirs
+// (G * nw_groups(M) * 32 u16).
+template <int MODE, bool kGlobal>
+__device__ __forceinline__ void nw_solve_lean(const double *__restrict__ sim, int ld, int N, int M, double gap,
+                                              double mismatch, double bonus, double threshold, uint16_t *dirs,
+                                              double *rowbuf, bimine_match *out, uint8_t *steps, int32_t *count_out,
+                                              double *score_out) {
+  const int lane = threadIdx.x & 31;
+  const double ng = -gap, span = fsub(bonus, mismatch);
+  const int G = (N + 31) >> 5, G8 = nw_groups(M);
+  double last = 0.0;
+  for (int g = 0; g < G; ++g) {
+    BotRow bot{rowbuf, M, g + 1 < G};
+    double fin;
+    if (g == 0) {
+      TopAnalytic top{ng};
+      fin = band_sweep<kGlobal>(sim, ld, N, M, 0, gap, mismatch, span, top, bot, dirs);
+    } else {
+      TopRow top{rowbuf, M};
+      // the band reads rowbuf[b] before lane 31 of the same sweep could
+      // overwrite it: reads of column s0+8 happen at group s0, writes of
+      // column s0+u-30 later -- never the same column within a group
+      fin = band_sweep<kGlobal>(sim, ld, N, M, 32 * g, gap, mismatch, span, top, bot, dirs + (int64_t)g * G8 * 32);
+    }
+    if (32 * g + 1 + lane == N) last = fin;
+    __syncwarp();
+    if (lane == 31 && g + 1 < G) rowbuf[0] = fmul(ng, (double)(32 * g + 32));  // dp[32g+32][0]
+    __syncwarp();
+  }
+  last = __shfl_sync(kFull, last, (N - 1) & 31);
+  if (lane == 0) {
+    int a = N, b = M;
+    int64_t cnt = 0;
+    if (MODE == kNwMine) {
+      while (a > 0 && b > 0) {
+        const uint32_t d = lean_dir(dirs, G8, a, b);
+        if (d == 0u) {
+          const int i = N - a, j = M - b;
+          const double v = sim[(int64_t)i * ld + j];
+          if (v >= threshold) {
+            out[cnt].score = v;
+            out[cnt].i = i;
+            out[cnt].j = j;
+            ++cnt;
+          }
+          --a;
+          --b;
+        } else if (d == 1u) {
+          --a;
+        } else {
+          --b;
+        }
+      }
+    } else {
+      while (a > 0 && b > 0) {
+        const uint32_t d = lean_dir(dirs, G8, a, b);
+        steps[cnt++] = (uint8_t)d;
+        if (d == 0u) {
+          --a;
+          --b;
+        } else if (d == 1u) {
+          --a;
+        } else {
+          --b;
+        }
+      }
+      while (a > 0) {
+        steps[cnt++] = 1u;
+        --a;
+      }
+      while (b > 0) {
+        steps[cnt++] = 2u;
+        --b;
+      }
+    }
+    *count_out = (int32_t)cnt;
+    if (score_out) *score_out = last;
+  }
+  __syncwarp();
+}
+
+__host__ __device__ inline int64_t lean_dir_words16(int N, int M) {
+  return (int64_t)((N + 31) >> 5) * nw_groups(M) * 32;
+}
+
 template <int MODE>
 __device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *rowbuf) {
   const int64_t pair = q / A.n_settings;
@@ -227,8 +420,12 @@ __device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *r
   uint8_t *st = (MODE == kNwSteps) ? A.steps + A.step_off[q] : nullptr;
   int32_t *cnt = (MODE == kNwMine) ? A.counts + q : (MODE == kNwSteps) ? A.n_steps + q : nullptr;
   int32_t dummy;
-  nw_solve<MODE, true>(A.sim + A.sim_off[pair], M, N, M, gap, A.mismatch, A.bonus, thr, A.table, dirs, rowbuf, out,
-                       st, cnt ? cnt : &dummy, A.score ? A.score + q : nullptr);
+  if (MODE == kNwTable)
+    nw_solve<MODE, true>(A.sim + A.sim_off[pair], M, N, M, gap, A.mismatch, A.bonus, thr, A.table, dirs, rowbuf, out,
+                         st, cnt ? cnt : &dummy, A.score ? A.score + q : nullptr);
+  else
+    nw_solve_lean<MODE, true>(A.sim + A.sim_off[pair], M, N, M, gap, A.mismatch, A.bonus, thr, (uint16_t *)dirs,
+                              rowbuf, out, st, cnt ? cnt : &dummy, A.score ? A.score + q : nullptr);
 }
 
 // Warps loop over problems; each warp owns one direction area and one
@@ -439,14 +636,50 @@ struct BigRing {
   volatile long long cons;  // positions consumed
 };
 
-__device__ __forceinline__ void prefetch_l1(const void *p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
+// ring-backed boundary provider: lane 0 of band g waits for the columns
+// its group needs, then releases what it will not read again
+struct TopRing {
+  BigRing *in;
+  long long base;  // position of column 0 of this band's generation
+  int M;
+  double row0;     // dp[32g][0]
+  __device__ void load9(int s0, double *rb) const {
+    if ((threadIdx.x & 31) != 0) return;
+    const int need = min(s0 + 8, M);
+    while (in->prod <= base + need) {
+    }
+    __threadfence_block();
+#pragma unroll
+    for (int u = 0; u < 9; ++u) {
+      const int b = min(s0 + u, M);
+      rb[u] = (b == 0) ? row0 : in->v[(base + b) % kRing];
+    }
+    in->cons = base + min(s0 + 8, M);  // columns below s0+8 are not read again
+  }
+};
+
+struct BotRing {
+  BigRing *out;
+  long long base;
+  int M;
+  bool on;
+  __device__ void put(int s, bool v, double best) const {
+    if (!(on && v && (threadIdx.x & 31) == 31)) return;
+    const int b = s - 30;
+    const long long pos = base + b;
+    while (pos - out->cons >= kRing - 1) {
+    }
+    out->v[pos % kRing] = best;
+    __threadfence_block();
+    if ((b & 7) == 0 || b == M) out->prod = pos + 1;
+  }
+};
 
 template <int MODE>
 __global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, uint32_t *g_dirs_all,
                                                                  const int64_t *dir_off) {
   __shared__ BigRing rings[kBigWarps];
+  __shared__ double s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q = A.problem_ids ? A.problem_ids[blockIdx.x] : (int64_t)blockIdx.x;
   const int64_t pair = q / A.n_settings;
@@ -455,8 +688,8 @@ __global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, 
   const double *__restrict__ sim = A.sim + A.sim_off[pair];
   const double gap = A.gap_per_problem ? A.gap[q] : A.gap[setting];
   const double ng = -gap, mismatch = A.mismatch, span = fsub(A.bonus, A.mismatch);
-  const int G = (N + 31) >> 5, T = M + 31;
-  uint32_t *dirs = g_dirs_all + dir_off[blockIdx.x];  // [G][T][2]
+  const int G = (N + 31) >> 5, G8 = nw_groups(M);
+  uint16_t *dirs = (uint16_t *)(g_dirs_all + dir_off[blockIdx.x]);  // [G][G8][32]
   const long long W1 = (long long)M + 1;
   if (threadIdx.x < kBigWarps) {
     rings[threadIdx.x].prod = 0;
@@ -466,142 +699,59 @@ __global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, 
     rings[threadIdx.x].cons = threadIdx.x == 0 ? W1 : 0;
   }
   __syncthreads();
-  double last = 0.0;
   for (int g = warp, gen = 0; g < G; g += kBigWarps, ++gen) {
-    BigRing &in = rings[warp];                     // boundary row 32g (from band g-1)
-    BigRing &outr = rings[(warp + 1) % kBigWarps];  // boundary row 32g+32 (for band g+1)
-    const int out_gen = (g + 1) / kBigWarps;        // generation of band g+1 on its ring
-    const int a = 32 * g + 1 + lane;
-    const bool active = a <= N;
-    const double left0 = fmul(ng, (double)a);
-    double cur = left0;
-    // dp[32g][0] for lane 0's first diagonal, dp[a-1][0] for the others
-    double diag = __shfl_up_sync(kFull, left0, 1);
-    if (lane == 0) diag = fmul(ng, (double)(32 * g));
-    const double *srow = sim + (int64_t)(N - a) * M + (M - 1);
-    auto ldr = [&](int b) -> double {
-      return (active && b >= 1 && b <= M) ? __ldg(srow - (b - 1)) : 0.0;
-    };
-    double cur8[8], nxt8[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) nxt8[u] = ldr(u - lane + 1);
-    const int nsteps = M + 31;
-    for (int s0 = 0; s0 < nsteps; s0 += 8) {
-      if (active && ((s0 - lane + 1) & 15) < 8) prefetch_l1(srow - min(max(s0 - lane + 1 + 32, 0), M - 1));
-#pragma unroll
-      for (int u = 0; u < 8; ++u) cur8[u] = nxt8[u];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) nxt8[u] = ldr(s0 + 8 + u - lane + 1);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int s = s0 + u;
-        if (s >= nsteps) break;
-        const int b = s - lane + 1;
-        double up = __shfl_up_sync(kFull, cur, 1);
-        if (lane == 0 && b >= 1 && b <= M) {
-          // row 32g, columns b and b-1: kernels.py:46 for band 0, else the ring
-          if (g == 0) {
-            up = fmul(ng, (double)b);
-            diag = fmul(ng, (double)(b - 1));
-          } else {
-            const long long pos = (long long)gen * W1 + b;  // position of column b
-            while (in.prod <= pos) {
-            }
-            __threadfence_block();
-            up = in.v[pos % kRing];
-            if (b == 1) diag = fmul(ng, (double)(32 * g));
-            else diag = in.v[(pos - 1) % kRing];
-            if ((b & 15) == 0 || b == M) in.cons = pos;  // release ring space (keeps b-1's value)
-          }
-        }
-        uint32_t dir = 0u;
-        double best = 0.0;
-        const bool valid = active && b >= 1 && b <= M;
-        if (valid) {
-          const double c = fadd(mismatch, fmul(cur8[u], span));
-          best = fadd(diag, c);
-          double cand = fsub(up, gap);
-          if (cand > best) {
-            best = cand;
-            dir = 1u;
-          }
-          cand = fsub(cur, gap);
-          if (cand > best) {
-            best = cand;
-            dir = 2u;
-          }
-          cur = best;
-          if (a == N && b == M) last = best;
-        }
-        if (lane == 31 && valid && g + 1 < G) {
-          const long long pos = (long long)out_gen * W1 + b;
-          while (pos - outr.cons >= kRing - 1) {
-          }
-          outr.v[pos % kRing] = best;
-          __threadfence_block();
-          if ((b & 7) == 0 || b == M) outr.prod = pos + 1;
-        }
-        if (lane > 0) diag = up;
-        const uint32_t lo = __ballot_sync(kFull, valid && (dir & 1u));
-        const uint32_t hi = __ballot_sync(kFull, valid && (dir & 2u));
-        if (lane == 0) {
-          dirs[2 * ((int64_t)g * T + s)] = lo;
-          dirs[2 * ((int64_t)g * T + s) + 1] = hi;
-        }
-      }
+    BotRing bot{&rings[(warp + 1) % kBigWarps], (long long)((g + 1) / kBigWarps) * W1, M, g + 1 < G};
+    double fin;
+    if (g == 0) {
+      TopAnalytic top{ng};
+      fin = band_sweep<true>(sim, M, N, M, 0, gap, mismatch, span, top, bot, dirs);
+    } else {
+      TopRing top{&rings[warp], (long long)gen * W1, M, fmul(ng, (double)(32 * g))};
+      fin = band_sweep<true>(sim, M, N, M, 32 * g, gap, mismatch, span, top, bot, dirs + (int64_t)g * G8 * 32);
+      if (lane == 0) rings[warp].cons = (long long)(gen + 1) * W1;  // generation done
     }
-    if (lane == 0 && g > 0) in.cons = (long long)gen * W1 + M + 1;
-    if (lane == 31 && g + 1 < G) outr.prod = (long long)out_gen * W1 + M + 1;  // flush
+    if (32 * g + 1 + lane == N) s_last = fin;
     __syncwarp();
   }
-  // dp[N][M] from the lane owning row N (its warp)
-  const int owner_warp = ((N - 1) >> 5) % kBigWarps;
-  __shared__ double s_last;
-  if (warp == owner_warp && lane == ((N - 1) & 31)) s_last = last;
   __syncthreads();
   if (MODE == kNwTable) return;
-  // ---- traceback on warp 0: lane 0 walks, the warp stages 64 steps of the
-  // current band at a time
+  // ---- traceback on warp 0: lane 0 walks, the warp stages 16 direction
+  // groups (128 steps) of the current band at a time
   if (warp == 0) {
-    __shared__ uint32_t win[2][64];
-    __shared__ int win_g, win_t0;
+    __shared__ uint16_t win[16 * 32];
+    __shared__ int win_g, win_k0;
     int a = N, b = M;
     int64_t cnt = 0;
     bimine_match *outm = (MODE == kNwMine) ? A.matches + A.out_off[q] : nullptr;
     uint8_t *st = (MODE == kNwSteps) ? A.steps + A.step_off[q] : nullptr;
     if (lane == 0) {
       win_g = -1;
-      win_t0 = 0;
+      win_k0 = 0;
     }
     __syncwarp();
     while (true) {
-      // every lane agrees on (a, b): lane 0 broadcasts
       a = __shfl_sync(kFull, a, 0);
       b = __shfl_sync(kFull, b, 0);
       if (!(a > 0 && b > 0)) break;
-      const int g = (a - 1) >> 5, l = (a - 1) & 31, t = b + l - 1;
-      const bool miss = !(g == win_g && t >= win_t0 && t < win_t0 + 64);
-      if (miss) {  // stage steps [t-63, t] of band g
-        const int t0 = max(0, t - 63);
-        for (int k = lane; k < 64; k += 32) {
-          const int tt = t0 + k;
-          const bool ok = tt < T;
-          win[0][k] = ok ? __ldcg(dirs + 2 * ((int64_t)g * T + tt)) : 0u;
-          win[1][k] = ok ? __ldcg(dirs + 2 * ((int64_t)g * T + tt) + 1) : 0u;
+      const int g = (a - 1) >> 5, l = (a - 1) & 31, k = (b + l - 1) >> 3;
+      if (!(g == win_g && k >= win_k0 && k < win_k0 + 16)) {
+        const int k0 = max(0, k - 15);
+        for (int x = lane; x < 16 * 32; x += 32) {
+          const int kk = k0 + (x >> 5);
+          win[x] = kk < G8 ? __ldcg(dirs + ((int64_t)g * G8 + kk) * 32 + (x & 31)) : (uint16_t)0;
         }
         __syncwarp();
         if (lane == 0) {
           win_g = g;
-          win_t0 = t0;
+          win_k0 = k0;
         }
         __syncwarp();
       }
       if (lane == 0) {
-        // walk while inside the window
         while (a > 0 && b > 0) {
-          const int gg = (a - 1) >> 5, ll = (a - 1) & 31, tt = b + ll - 1;
-          if (gg != win_g || tt < win_t0 || tt >= win_t0 + 64) break;
-          const uint32_t d = ((win[0][tt - win_t0] >> ll) & 1u) | (((win[1][tt - win_t0] >> ll) & 1u) << 1);
+          const int gg = (a - 1) >> 5, ll = (a - 1) & 31, ss = b + ll - 1, kk = ss >> 3;
+          if (gg != win_g || kk < win_k0 || kk >= win_k0 + 16) break;
+          const uint32_t d = ((uint32_t)win[(kk - win_k0) * 32 + ll] >> (2 * (ss & 7))) & 3u;
           if (d == 0u) {
             if (MODE == kNwMine) {
               outm[cnt].i = N - a;  // score filled below
