@@ -628,15 +628,34 @@ namespace bimine {
 // lane 0 from a 64-step window staged by the whole warp, and the match
 // scores are gathered in parallel afterwards.
 constexpr int kBigWarps = 16;
-constexpr int kRing = 256;  // boundary values buffered per ring
+constexpr int kRing = 128;  // boundary values buffered per ring
 
+// A ring slot carries its value and the position it holds, written by one
+// 16-byte shared-memory store, so a consumer polling the slot's position
+// sees a consistent value without any fence (a __threadfence_block per step
+// would wait for the warp's outstanding global direction stores).
 struct BigRing {
-  double v[kRing];
-  volatile long long prod;  // positions written  (gen * (M+1) + b, exclusive)
-  volatile long long cons;  // positions consumed
+  double2 slot[kRing];      // .x = value, .y = position bits (as double bits)
+  volatile long long cons;  // positions consumed (capacity hint for the producer)
 };
 
-// ring-backed boundary provider: lane 0 of band g waits for the columns
+__device__ __forceinline__ void ring_put(double2 *slot, double v, long long pos) {
+  asm volatile("st.volatile.shared.v2.f64 [%0], {%1, %2};" ::"r"((unsigned)__cvta_generic_to_shared(slot)), "d"(v),
+               "d"(__longlong_as_double(pos))
+               : "memory");
+}
+
+__device__ __forceinline__ double ring_get(const double2 *slot, long long pos) {
+  double v, t;
+  do {
+    asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v), "=d"(t)
+                 : "r"((unsigned)__cvta_generic_to_shared(slot))
+                 : "memory");
+  } while (__double_as_longlong(t) != pos);
+  return v;
+}
+
+// ring-backed boundary provider: lane 0 of band g waits for each column
 // its group needs, then releases what it will not read again
 struct TopRing {
   BigRing *in;
@@ -645,14 +664,10 @@ struct TopRing {
   double row0;     // dp[32g][0]
   __device__ void load9(int s0, double *rb) const {
     if ((threadIdx.x & 31) != 0) return;
-    const int need = min(s0 + 8, M);
-    while (in->prod <= base + need) {
-    }
-    __threadfence_block();
 #pragma unroll
     for (int u = 0; u < 9; ++u) {
       const int b = min(s0 + u, M);
-      rb[u] = (b == 0) ? row0 : in->v[(base + b) % kRing];
+      rb[u] = (b == 0) ? row0 : ring_get(&in->slot[(base + b) % kRing], base + b);
     }
     in->cons = base + min(s0 + 8, M);  // columns below s0+8 are not read again
   }
@@ -665,13 +680,10 @@ struct BotRing {
   bool on;
   __device__ void put(int s, bool v, double best) const {
     if (!(on && v && (threadIdx.x & 31) == 31)) return;
-    const int b = s - 30;
-    const long long pos = base + b;
+    const long long pos = base + (s - 30);
     while (pos - out->cons >= kRing - 1) {
     }
-    out->v[pos % kRing] = best;
-    __threadfence_block();
-    if ((b & 7) == 0 || b == M) out->prod = pos + 1;
+    ring_put(&out->slot[pos % kRing], best, pos);
   }
 };
 
@@ -691,8 +703,9 @@ __global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, 
   const int G = (N + 31) >> 5, G8 = nw_groups(M);
   uint16_t *dirs = (uint16_t *)(g_dirs_all + dir_off[blockIdx.x]);  // [G][G8][32]
   const long long W1 = (long long)M + 1;
+  for (int k = threadIdx.x; k < kBigWarps * kRing; k += blockDim.x)
+    rings[k / kRing].slot[k % kRing] = make_double2(0.0, __longlong_as_double(-1ll));
   if (threadIdx.x < kBigWarps) {
-    rings[threadIdx.x].prod = 0;
     // band 0 takes its boundary from kernels.py:46 and never reads ring 0, so
     // ring 0's generation 0 starts consumed (else band kBigWarps-1 would
     // wait for space forever)
