@@ -422,7 +422,8 @@ int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
     for (int64_t k = 0; k < nprob; ++k) h[k] = k * stride;
     BIMINE_CUDA(cudaMemcpyAsync(offs, h.data(), sizeof(int64_t) * nprob, cudaMemcpyHostToDevice, st));
     if (nprob > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "nw: too many large problems");
-    nw_big_kernel<MODE><<<(unsigned)nprob, kBigWarps * 32, 0, st>>>(A, dirs, offs);
+    BIMINE_CUDA(cudaFuncSetAttribute(nw_big_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem));
+    nw_big_kernel<MODE><<<(unsigned)nprob, kBigWarps * 32, kBigSmem, st>>>(A, dirs, offs);
     const cudaError_t e = cudaGetLastError();
     cudaFreeAsync(dirs, st);
     cudaFreeAsync(offs, st);

@@ -687,10 +687,22 @@ struct BotRing {
   }
 };
 
+// Rings: two per warp slot, by generation parity.  Band g (warp g % W,
+// generation g / W) reads ring (g % W, gen & 1) and writes ring
+// ((g+1) % W, ((g+1)/W) & 1).  A producer of generation k+2 can only wait
+// on the consumer of generation k -- a band that depends on strictly
+// earlier bands only -- so the waits are acyclic; with a single ring per
+// slot the producer of k+1 would wait on the consumer of k, which waits
+// (through the chain of slots) on that same producer once M is large.
+// A consumer that finishes its band marks the ring empty for the next
+// generation of the same parity (cons = (gen + 2) * (M + 1)).
+constexpr size_t kBigSmem = 2 * kBigWarps * sizeof(BigRing);
+
 template <int MODE>
 __global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, uint32_t *g_dirs_all,
                                                                  const int64_t *dir_off) {
-  __shared__ BigRing rings[kBigWarps];
+  extern __shared__ __align__(16) unsigned char big_smem[];
+  BigRing *rings = (BigRing *)big_smem;  // [kBigWarps][2]
   __shared__ double s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q = A.problem_ids ? A.problem_ids[blockIdx.x] : (int64_t)blockIdx.x;
@@ -703,25 +715,28 @@ __global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, 
   const int G = (N + 31) >> 5, G8 = nw_groups(M);
   uint16_t *dirs = (uint16_t *)(g_dirs_all + dir_off[blockIdx.x]);  // [G][G8][32]
   const long long W1 = (long long)M + 1;
-  for (int k = threadIdx.x; k < kBigWarps * kRing; k += blockDim.x)
+  for (int k = threadIdx.x; k < 2 * kBigWarps * kRing; k += blockDim.x)
     rings[k / kRing].slot[k % kRing] = make_double2(0.0, __longlong_as_double(-1ll));
-  if (threadIdx.x < kBigWarps) {
-    // band 0 takes its boundary from kernels.py:46 and never reads ring 0, so
-    // ring 0's generation 0 starts consumed (else band kBigWarps-1 would
-    // wait for space forever)
-    rings[threadIdx.x].cons = threadIdx.x == 0 ? W1 : 0;
+  if (threadIdx.x < 2 * kBigWarps) {
+    // ring (slot, parity) first holds generation `parity`; band 0 (slot 0,
+    // generation 0) takes its boundary from kernels.py:46, so that ring
+    // starts empty for generation 2
+    const int slot = threadIdx.x >> 1, par = threadIdx.x & 1;
+    rings[threadIdx.x].cons = (slot == 0 && par == 0) ? 2 * W1 : par * W1;
   }
   __syncthreads();
   for (int g = warp, gen = 0; g < G; g += kBigWarps, ++gen) {
-    BotRing bot{&rings[(warp + 1) % kBigWarps], (long long)((g + 1) / kBigWarps) * W1, M, g + 1 < G};
+    const int ogen = (g + 1) / kBigWarps;
+    BotRing bot{&rings[2 * ((warp + 1) % kBigWarps) + (ogen & 1)], (long long)ogen * W1, M, g + 1 < G};
     double fin;
     if (g == 0) {
       TopAnalytic top{ng};
       fin = band_sweep<true>(sim, M, N, M, 0, gap, mismatch, span, top, bot, dirs);
     } else {
-      TopRing top{&rings[warp], (long long)gen * W1, M, fmul(ng, (double)(32 * g))};
+      BigRing *in = &rings[2 * warp + (gen & 1)];
+      TopRing top{in, (long long)gen * W1, M, fmul(ng, (double)(32 * g))};
       fin = band_sweep<true>(sim, M, N, M, 32 * g, gap, mismatch, span, top, bot, dirs + (int64_t)g * G8 * 32);
-      if (lane == 0) rings[warp].cons = (long long)(gen + 1) * W1;  // generation done
+      if (lane == 0) in->cons = (long long)(gen + 2) * W1;  // empty: free for generation gen + 2
     }
     if (32 * g + 1 + lane == N) s_last = fin;
     __syncwarp();
