@@ -422,11 +422,17 @@ int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
     for (int64_t k = 0; k < nprob; ++k) h[k] = k * stride;
     BIMINE_CUDA(cudaMemcpyAsync(offs, h.data(), sizeof(int64_t) * nprob, cudaMemcpyHostToDevice, st));
     if (nprob > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "nw: too many large problems");
+    // wrap-around boundary rows: [2][max_m + 1] tagged slots per problem, tags -1
+    const int64_t rows_stride = 2 * ((int64_t)max_m + 1);
+    double2 *rows = nullptr;
+    BIMINE_CUDA(cudaMallocAsync((void **)&rows, sizeof(double2) * rows_stride * nprob, st));
+    BIMINE_CUDA(cudaMemsetAsync(rows, 0xff, sizeof(double2) * rows_stride * nprob, st));
     BIMINE_CUDA(cudaFuncSetAttribute(nw_big_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem));
-    nw_big_kernel<MODE><<<(unsigned)nprob, kBigWarps * 32, kBigSmem, st>>>(A, dirs, offs);
+    nw_big_kernel<MODE><<<(unsigned)nprob, kBigWarps * 32, kBigSmem, st>>>(A, dirs, offs, rows, rows_stride);
     const cudaError_t e = cudaGetLastError();
     cudaFreeAsync(dirs, st);
     cudaFreeAsync(offs, st);
+    cudaFreeAsync(rows, st);
     if (e != cudaSuccess) return fail(BIMINE_E_CUDA, std::string("nw_big_kernel: ") + cudaGetErrorString(e));
     return BIMINE_OK;
   }

@@ -263,6 +263,8 @@ __device__ __forceinline__ double band_sweep(const double *__restrict__ sim, int
     const uint32_t vmask = (active && lo <= hi) ? (((2u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
     double rb[9];
     top.load9(s0, rb);  // lane 0: dp[a0][s0 .. s0+8]
+    bot.reserve(s0);    // whole warp: room for this group's boundary values
+    __syncwarp();       // reconverge before the shuffles of the step loop
     uint32_t bits = 0u;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -315,11 +317,13 @@ struct BotRow {  // lane 31 writes row[b] for the next band
   double *row;
   int M;
   bool on;
+  __device__ void reserve(int) const {}
   __device__ void put(int s, bool v, double best) const {
     if (on && v && (threadIdx.x & 31) == 31) row[s - 30] = best;
   }
 };
 struct BotNone {
+  __device__ void reserve(int) const {}
   __device__ void put(int, bool, double) const {}
 };
 
@@ -655,21 +659,78 @@ __device__ __forceinline__ double ring_get(const double2 *slot, long long pos) {
   return v;
 }
 
-// ring-backed boundary provider: lane 0 of band g waits for each column
-// its group needs, then releases what it will not read again
-struct TopRing {
-  BigRing *in;
-  long long base;  // position of column 0 of this band's generation
+// Tagged-slot boundary provider (lane 0 of band g).  kShared: the slots
+// are a shared-memory ring; the group's 9 slots are read together and those
+// whose tag is not yet the wanted position re-read until the producer has
+// written them; then `cons` releases what will not be read again.  Else a
+// full global row (L2 round trips): the next group's slots are prefetched
+// while the current group computes, and checked at the next group start.  Tags compare on their
+// low 32 bits -- stale tags are at most a ring or two generations old.
+template <bool kShared>
+struct TopTagged {
+  const double2 *buf;
+  volatile long long *cons;  // ring only
+  long long base;            // position of column 0 of this band's generation
   int M;
-  double row0;     // dp[32g][0]
-  __device__ void load9(int s0, double *rb) const {
-    if ((threadIdx.x & 31) != 0) return;
+  double row0;               // dp[32g][0]
+  double pv[9];
+  int pt[9];
+  __device__ __forceinline__ void ld(int b, double &v, int &t) const {
+    double td;
+    if (kShared) {
+      const double2 *q = buf + ((base + b) & (kRing - 1));
+      asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v), "=d"(td)
+                   : "r"((unsigned)__cvta_generic_to_shared(q))
+                   : "memory");
+    } else {
+      asm volatile("ld.volatile.global.v2.f64 {%0, %1}, [%2];" : "=d"(v), "=d"(td) : "l"(buf + b) : "memory");
+    }
+    t = __double2loint(td);
+  }
+  __device__ __forceinline__ void fetch(int s0) {
 #pragma unroll
     for (int u = 0; u < 9; ++u) {
       const int b = min(s0 + u, M);
-      rb[u] = (b == 0) ? row0 : ring_get(&in->slot[(base + b) % kRing], base + b);
+      if (b == 0) {
+        pv[u] = row0;
+        pt[u] = (int)base;
+      } else {
+        ld(b, pv[u], pt[u]);
+      }
     }
-    in->cons = base + min(s0 + 8, M);  // columns below s0+8 are not read again
+  }
+  __device__ __forceinline__ void load9(int s0, double *rb) {
+    if ((threadIdx.x & 31) != 0) return;
+    if (kShared) {  // shared ring: ~30-cycle round trip, no prefetch state kept
+#pragma unroll
+      for (int u = 0; u < 9; ++u) {
+        const int b = min(s0 + u, M);
+        int t;
+        if (b == 0) {
+          rb[u] = row0;
+          t = (int)base;
+        } else {
+          ld(b, rb[u], t);
+        }
+        pt[u] = t;
+      }
+#pragma unroll
+      for (int u = 0; u < 9; ++u) {
+        const int b = min(s0 + u, M);
+        while (pt[u] != (int)(base + b)) ld(b, rb[u], pt[u]);
+      }
+      *cons = base + min(s0 + 8, M);  // columns below s0+8 are not read again
+      return;
+    }
+    if (s0 == 0) fetch(0);
+#pragma unroll
+    for (int u = 0; u < 9; ++u) {
+      const int b = min(s0 + u, M);
+      const int want = (int)(base + b);
+      while (pt[u] != want) ld(b, pv[u], pt[u]);
+      rb[u] = pv[u];
+    }
+    fetch(s0 + 8);
   }
 };
 
@@ -678,31 +739,51 @@ struct BotRing {
   long long base;
   int M;
   bool on;
+  // warp-uniform wait (every lane reads the same `cons`): the group's
+  // stores, positions up to base + s0 + 7 - 30, must not lap the consumer
+  __device__ void reserve(int s0) const {
+    if (!on) return;
+    const long long last = base + (s0 + 7 - 30);
+    while (last - out->cons >= kRing - 1) {
+    }
+  }
   __device__ void put(int s, bool v, double best) const {
     if (!(on && v && (threadIdx.x & 31) == 31)) return;
     const long long pos = base + (s - 30);
-    while (pos - out->cons >= kRing - 1) {
-    }
-    ring_put(&out->slot[pos % kRing], best, pos);
+    ring_put(&out->slot[pos & (kRing - 1)], best, pos);
   }
 };
 
-// Rings: two per warp slot, by generation parity.  Band g (warp g % W,
-// generation g / W) reads ring (g % W, gen & 1) and writes ring
-// ((g+1) % W, ((g+1)/W) & 1).  A producer of generation k+2 can only wait
-// on the consumer of generation k -- a band that depends on strictly
-// earlier bands only -- so the waits are acyclic; with a single ring per
-// slot the producer of k+1 would wait on the consumer of k, which waits
-// (through the chain of slots) on that same producer once M is large.
-// A consumer that finishes its band marks the ring empty for the next
-// generation of the same parity (cons = (gen + 2) * (M + 1)).
-constexpr size_t kBigSmem = 2 * kBigWarps * sizeof(BigRing);
+// Boundaries between bands of the same round (warp w-1 -> warp w, w >= 1)
+// stream through a shared-memory ring; the wrap-around boundary (warp W-1
+// -> warp 0's next band) goes through a full row of tagged slots in global
+// memory, double-buffered by generation parity: warp 0 starts that band only
+// after finishing its previous one, so a bounded buffer there would tie band
+// 0's progress to its own successors (a wait cycle once M exceeds the
+// chain's total buffering).  With the wrap row never full, every wait points
+// to a lower band or to a band of the same round further right -- acyclic.
+struct BotRowG {  // lane 31 writes tagged slots of a global row
+  double2 *row;
+  long long base;
+  bool on;
+  __device__ void reserve(int) const {}
+  __device__ void put(int s, bool v, double best) const {
+    if (!(on && v && (threadIdx.x & 31) == 31)) return;
+    const int b = s - 30;
+    asm volatile("st.volatile.global.v2.f64 [%0], {%1, %2};" ::"l"(row + b), "d"(best),
+                 "d"(__longlong_as_double(base + b))
+                 : "memory");
+  }
+};
+
+constexpr size_t kBigSmem = kBigWarps * sizeof(BigRing);
 
 template <int MODE>
 __global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, uint32_t *g_dirs_all,
-                                                                 const int64_t *dir_off) {
+                                                                 const int64_t *dir_off, double2 *g_rows,
+                                                                 int64_t rows_stride) {
   extern __shared__ __align__(16) unsigned char big_smem[];
-  BigRing *rings = (BigRing *)big_smem;  // [kBigWarps][2]
+  BigRing *rings = (BigRing *)big_smem;  // [kBigWarps], slot w feeds warp w (w >= 1)
   __shared__ double s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q = A.problem_ids ? A.problem_ids[blockIdx.x] : (int64_t)blockIdx.x;
@@ -714,29 +795,40 @@ __global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, 
   const double ng = -gap, mismatch = A.mismatch, span = fsub(A.bonus, A.mismatch);
   const int G = (N + 31) >> 5, G8 = nw_groups(M);
   uint16_t *dirs = (uint16_t *)(g_dirs_all + dir_off[blockIdx.x]);  // [G][G8][32]
+  double2 *wrap = g_rows + (int64_t)blockIdx.x * rows_stride;      // [2][M+1] tagged, pre-filled with tag -1
   const long long W1 = (long long)M + 1;
-  for (int k = threadIdx.x; k < 2 * kBigWarps * kRing; k += blockDim.x)
+  for (int k = threadIdx.x; k < kBigWarps * kRing; k += blockDim.x)
     rings[k / kRing].slot[k % kRing] = make_double2(0.0, __longlong_as_double(-1ll));
-  if (threadIdx.x < 2 * kBigWarps) {
-    // ring (slot, parity) first holds generation `parity`; band 0 (slot 0,
-    // generation 0) takes its boundary from kernels.py:46, so that ring
-    // starts empty for generation 2
-    const int slot = threadIdx.x >> 1, par = threadIdx.x & 1;
-    rings[threadIdx.x].cons = (slot == 0 && par == 0) ? 2 * W1 : par * W1;
-  }
+  if (threadIdx.x < kBigWarps) rings[threadIdx.x].cons = 0;
   __syncthreads();
   for (int g = warp, gen = 0; g < G; g += kBigWarps, ++gen) {
     const int ogen = (g + 1) / kBigWarps;
-    BotRing bot{&rings[2 * ((warp + 1) % kBigWarps) + (ogen & 1)], (long long)ogen * W1, M, g + 1 < G};
+    const bool out_wrap = (warp + 1) == kBigWarps;
     double fin;
+    // output side
+    BotRing bring{&rings[(warp + 1) % kBigWarps], (long long)ogen * W1, M, g + 1 < G && !out_wrap};
+    BotRowG brow{wrap + (ogen & 1) * W1, (long long)ogen * W1, g + 1 < G && out_wrap};
+    struct Bot2 {
+      const BotRing &r;
+      const BotRowG &w;
+      __device__ void reserve(int s0) const { r.reserve(s0); }
+      __device__ void put(int s_, bool v, double best) const {
+        r.put(s_, v, best);
+        w.put(s_, v, best);
+      }
+    } bot{bring, brow};
+    uint16_t *dband = dirs + (int64_t)g * G8 * 32;
     if (g == 0) {
       TopAnalytic top{ng};
-      fin = band_sweep<true>(sim, M, N, M, 0, gap, mismatch, span, top, bot, dirs);
+      fin = band_sweep<true>(sim, M, N, M, 0, gap, mismatch, span, top, bot, dband);
+    } else if (warp == 0) {
+      TopTagged<false> top{wrap + (gen & 1) * W1, nullptr, (long long)gen * W1, M, fmul(ng, (double)(32 * g))};
+      fin = band_sweep<true>(sim, M, N, M, 32 * g, gap, mismatch, span, top, bot, dband);
     } else {
-      BigRing *in = &rings[2 * warp + (gen & 1)];
-      TopRing top{in, (long long)gen * W1, M, fmul(ng, (double)(32 * g))};
-      fin = band_sweep<true>(sim, M, N, M, 32 * g, gap, mismatch, span, top, bot, dirs + (int64_t)g * G8 * 32);
-      if (lane == 0) in->cons = (long long)(gen + 2) * W1;  // empty: free for generation gen + 2
+      BigRing *in = &rings[warp];
+      TopTagged<true> top{in->slot, &in->cons, (long long)gen * W1, M, fmul(ng, (double)(32 * g))};
+      fin = band_sweep<true>(sim, M, N, M, 32 * g, gap, mismatch, span, top, bot, dband);
+      if (lane == 0) in->cons = (long long)(gen + 1) * W1;  // generation done
     }
     if (32 * g + 1 + lane == N) s_last = fin;
     __syncwarp();
