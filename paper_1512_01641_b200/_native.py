@@ -15,7 +15,8 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbimine_b200.so")
+# BIMINE_LIB: load another build of the library (A/B kernel experiments)
+LIB_PATH = os.environ.get("BIMINE_LIB") or os.path.join(HERE, "libbimine_b200.so")
 
 _i64p = ctypes.POINTER(ctypes.c_int64)
 _i32p = ctypes.POINTER(ctypes.c_int32)

@@ -341,11 +341,29 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
       double *cp = S.c_p + warp * kSegItems;
       const int jlo = lane, jhi = lane + 32;
       const unsigned lt_mask = (1u << lane) - 1u;
-      while (true) {
-        int i = 0;
-        if (lane == 0) i = atomicAdd(&S.misc[2], 1);
-        i = __shfl_sync(kFull, i, 0);
-        if (i >= N) break;
+      // software pipeline: the next segment's window (token, dictionary row)
+      // is loaded while the current one is processed, and the next
+      // sentence is claimed one sentence ahead
+      auto claim = [&]() -> int {
+        int v = 0;
+        if (lane == 0) v = atomicAdd(&S.misc[2], 1);
+        return __shfl_sync(kFull, v, 0);
+      };
+      auto load_tok = [&](int si, int pos) -> int32_t {
+        if (si >= N) return -1;
+        const int k = pos + lane;
+        return k < S.src_len[si] ? tokens[S.src_off[si] + k] : -1;
+      };
+      int i = claim();
+      int i_nxt = i < N ? claim() : N;
+      int32_t s_w = load_tok(i, 0);
+      int64_t e0_w = 0;
+      int rl_w = 0;
+      if (s_w >= 0 && s_w < n_rows) {
+        e0_w = row_ptr[s_w];
+        rl_w = (int)(row_ptr[s_w + 1] - e0_w);
+      }
+      while (i < N) {
         const int64_t off = S.src_off[i];
         const int L = S.src_len[i];
         const unsigned long long ibit = 1ull << i;
@@ -354,13 +372,9 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
         for (int seg = 0; seg < L;) {
           const int k = seg + lane;
           const bool valid = k < L;
-          const int32_t s = valid ? tokens[off + k] : -1;
-          int64_t e0 = 0;
-          int rl = 0;
-          if (valid && s >= 0 && s < n_rows) {
-            e0 = row_ptr[s];
-            rl = (int)(row_ptr[s + 1] - e0);
-          }
+          const int32_t s = s_w;  // tokens[off + k] or -1
+          const int64_t e0 = e0_w;
+          const int rl = rl_w;
           // segment: the longest prefix of occurrences whose rows total
           // <= kSegItems entries (at least one occurrence)
           int x = rl;
@@ -374,6 +388,9 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           const bool in_seg = lane < cnt;
           const int items = min(kSegItems, __shfl_sync(kFull, x, cnt - 1));
           const int ofs = x - rl;  // exclusive prefix: first item of this occurrence
+          // next window: the rest of this sentence, else the next sentence
+          const bool more = seg + cnt < L;
+          const int32_t tok_nx = more ? load_tok(i, seg + cnt) : load_tok(i_nxt, 0);
           // shared tokens: first occurrence of a source token that is a chunk token
           const int ds = in_seg ? pk_find_f(S.bloom, S.keys, S.dense, hbits, s) : -1;
           const unsigned peers = __match_any_sync(kFull, in_seg ? s : -1);
@@ -420,7 +437,14 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
               cov_lo += (int)((a >> jlo) & 1ull);
               cov_hi += (int)((a >> jhi) & 1ull);
             }
-            seg += 1;
+            s_w = tok_nx;
+            e0_w = 0;
+            rl_w = 0;
+            if (s_w >= 0 && s_w < n_rows) {
+              e0_w = row_ptr[s_w];
+              rl_w = (int)(row_ptr[s_w + 1] - e0_w);
+            }
+            seg += 1;  // cnt == 1 here
             continue;
           }
           oany[lane] = 0ull;
@@ -441,10 +465,12 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
             const int64_t oe0 = __shfl_sync(kFull, e0, owner);
             const int oofs = __shfl_sync(kFull, ofs, owner);
             int d = -1;
-            int64_t e = 0;
+            double pr = 0.0;
             if (live) {
-              e = oe0 + (it - oofs);
-              d = pk_find_f(S.bloom, S.keys, S.dense, hbits, dtgt[e]);
+              const int64_t e = oe0 + (it - oofs);
+              const int32_t t = dtgt[e];
+              pr = dprob[e];  // issued with the id load: no second round trip for hits
+              d = pk_find_f(S.bloom, S.keys, S.dense, hbits, t);
             }
             const bool pres = d >= 0;
             const unsigned bal = __ballot_sync(kFull, pres);
@@ -452,12 +478,20 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
               const uint64_t m = S.colmask[d];
               const int pos = ncand + __popc(bal & lt_mask);
               cm[pos] = m;
-              cp[pos] = dprob[e];
+              cp[pos] = pr;
               atomicOr((unsigned long long *)&S.reachcol[d], ibit);
               atomicOr((unsigned long long *)&oany[owner], m);
               atomicAdd(&on[owner], 1);
             }
             ncand += __popc(bal);
+          }
+          // the next window's dictionary rows (its tokens arrived during the walk)
+          s_w = tok_nx;
+          e0_w = 0;
+          rl_w = 0;
+          if (s_w >= 0 && s_w < n_rows) {
+            e0_w = row_ptr[s_w];
+            rl_w = (int)(row_ptr[s_w + 1] - e0_w);
           }
           __syncwarp();
           // occurrence-major, in order: max p over the occurrence's
@@ -513,6 +547,17 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           aux[(int64_t)i * Mfull + jc0 + jhi] = (uint16_t)(cov_hi | (sh_hi << 8));
           out[(int64_t)i * Mfull + jc0 + jhi] = sum_hi;
         }
+        if (L == 0) {  // (the builder rejects empty sentences; keep the pipeline consistent anyway)
+          s_w = load_tok(i_nxt, 0);
+          e0_w = 0;
+          rl_w = 0;
+          if (s_w >= 0 && s_w < n_rows) {
+            e0_w = row_ptr[s_w];
+            rl_w = (int)(row_ptr[s_w + 1] - e0_w);
+          }
+        }
+        i = i_nxt;  // its first window is already loaded
+        if (i < N) i_nxt = claim();
       }
     }
     __syncthreads();
