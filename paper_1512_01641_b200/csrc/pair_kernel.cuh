@@ -184,6 +184,14 @@ __device__ __forceinline__ void pk_insert(int32_t *keys, int bits, int32_t key) 
   }
 }
 
+// 64-bit OR into shared memory as native 32-bit ORs of the nonzero halves
+// (a 64-bit shared atomicOr compiles to a compare-and-swap loop)
+__device__ __forceinline__ void or64(uint64_t *w, uint64_t m) {
+  uint32_t *h = (uint32_t *)w;
+  if ((uint32_t)m) atomicOr(h, (uint32_t)m);
+  if ((uint32_t)(m >> 32)) atomicOr(h + 1, (uint32_t)(m >> 32));
+}
+
 // Is the pair handled by pair_kernel?  (host and device agree on this rule)
 __host__ __device__ inline bool pair_is_small(int n, int m, int max_len) {
   return n <= kPairMax && m <= kPairMax && max_len <= kPairMaxLen;
@@ -329,7 +337,7 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
       for (int k = lane; k < L; k += 32) {
         const int d = pk_find(S.keys, S.dense, hbits, tokens[off + k]);
         S.tgt_d[q0 + k] = (int16_t)d;
-        atomicOr((unsigned long long *)&S.colmask[d], 1ull << jj);
+        or64(&S.colmask[d], 1ull << jj);
       }
     }
     __syncthreads();
@@ -419,7 +427,7 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
               if (it < rl0) d = pk_find_f(S.bloom, S.keys, S.dense, hbits, dtgt[r0 + it]);
               const uint64_t m = d >= 0 ? S.colmask[d] : 0ull;
               const double pr = d >= 0 ? dprob[r0 + it] : 0.0;
-              if (d >= 0) atomicOr((unsigned long long *)&S.reachcol[d], ibit);
+              if (d >= 0) or64(&S.reachcol[d], ibit);
               unsigned bal = __ballot_sync(kFull, d >= 0);
               while (bal) {
                 const int src = __ffs(bal) - 1;
@@ -479,8 +487,8 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
               const int pos = ncand + __popc(bal & lt_mask);
               cm[pos] = m;
               cp[pos] = pr;
-              atomicOr((unsigned long long *)&S.reachcol[d], ibit);
-              atomicOr((unsigned long long *)&oany[owner], m);
+              or64(&S.reachcol[d], ibit);
+              or64(&oany[owner], m);
               atomicAdd(&on[owner], 1);
             }
             ncand += __popc(bal);
@@ -586,8 +594,10 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
   const bool fuse_nw = A.nw_matches != nullptr && !is_tile;
   double *tile = (double *)smem_raw;  // overlay: dead after phase C
   const int cells = N * M;
+  // cell c = i * M + j, stepped without integer division
+  const int di = kPairThreads / M, dj = kPairThreads - di * M;
+  int i = tid / M, j = tid - (tid / M) * M;
   for (int c = tid; c < cells; c += kPairThreads) {
-    const int i = c / M, j = c - i * M;
     const int x = i * kCellStride + j;
     const int64_t o = (int64_t)i * Mfull + j;
     const uint32_t ax = aux[o];
@@ -596,6 +606,12 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
                                   (int)(ax >> 8), S.exp_tab);
     out[o] = v;
     if (fuse_nw) tile[i * 64 + j] = v;
+    i += di;
+    j += dj;
+    if (j >= M) {
+      j -= M;
+      ++i;
+    }
   }
   if (!fuse_nw) return;
   __syncthreads();
