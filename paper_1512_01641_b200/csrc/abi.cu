@@ -16,6 +16,7 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/bimine_b200.h"
@@ -411,28 +412,118 @@ int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
     return BIMINE_OK;
   }
   if (MODE != kNwTable) {
-    // large problems: one CTA each, warps pipelined over row bands
+    // large problems: K CTAs each (16 warps pipelined over row bands per CTA);
+    // K > 1 only while every CTA of the launch can be resident at once
     const int64_t stride = (lean_dir_words16(max_n, max_m) + 1) / 2;  // u32 words per problem (worst case)
     const int64_t nprob = A.n_problems;
+    if (nprob > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "nw: too many large problems");
+    const int gmax = (max_n + 31) / 32;
+    int kc = std::max(1, std::min(16, (gmax + kBigW - 1) / kBigW));  // CTAs per cluster (= per problem)
+    constexpr size_t smem = big_smem_bytes<kBigW>();
+    auto kern = nw_big_kernel<MODE, kBigW>;
+    BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    cfg.blockDim = dim3(kBigW * 32, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    while (kc > 1) {  // the largest cluster the device schedules for this kernel
+      attr[0].val.clusterDim.x = (unsigned)kc;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3((unsigned)kc, 1, 1);
+      int ok = 0;
+      if (cudaOccupancyMaxActiveClusters(&ok, kern, &cfg) == cudaSuccess && ok > 0) break;
+      cudaGetLastError();
+      --kc;
+    }
+    attr[0].val.clusterDim.x = (unsigned)kc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    if (nprob * kc > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "nw: too many large problems");
+    cfg.gridDim = dim3((unsigned)(nprob * kc), 1, 1);
+    // diagonal layout of every distinct pair among the problems
+    std::vector<int64_t> ids(nprob);
+    if (A.problem_ids) {
+      BIMINE_CUDA(cudaMemcpyAsync(ids.data(), A.problem_ids, sizeof(int64_t) * nprob, cudaMemcpyDeviceToHost, st));
+      BIMINE_CUDA(cudaStreamSynchronize(st));
+    } else {
+      for (int64_t k = 0; k < nprob; ++k) ids[k] = k;
+    }
+    std::vector<int64_t> dpairs, dslot(nprob), doff;
+    {
+      std::unordered_map<int64_t, int64_t> seen;
+      for (int64_t k = 0; k < nprob; ++k) {
+        const int64_t pr = ids[k] / A.n_settings;
+        auto it = seen.find(pr);
+        if (it == seen.end()) it = seen.emplace(pr, (int64_t)dpairs.size()).first, dpairs.push_back(pr);
+        dslot[k] = it->second;
+      }
+    }
+    std::vector<int32_t> pn(dpairs.size()), pm(dpairs.size());
+    for (size_t k = 0; k < dpairs.size(); ++k) {
+      BIMINE_CUDA(cudaMemcpyAsync(&pn[k], A.pair_n + dpairs[k], sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      BIMINE_CUDA(cudaMemcpyAsync(&pm[k], A.pair_m + dpairs[k], sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    }
+    BIMINE_CUDA(cudaStreamSynchronize(st));
+    int64_t dtotal = 0;
+    int gmax_d = 1;
+    std::vector<int64_t> pair_doff(dpairs.size());
+    for (size_t k = 0; k < dpairs.size(); ++k) {
+      pair_doff[k] = dtotal;
+      const int g = (pn[k] + 31) / 32;
+      gmax_d = std::max(gmax_d, g);
+      dtotal += (int64_t)g * nw_diag_steps(pm[k]) * 32;
+    }
+    doff.resize(nprob);
+    for (int64_t k = 0; k < nprob; ++k) doff[k] = pair_doff[dslot[k]];
+    if (gmax_d > 65535 || (int64_t)dpairs.size() > 65535) return fail(BIMINE_E_LIMIT, "nw: large problem too tall");
+    double *diag = nullptr;
+    int64_t *d_pairs = nullptr, *d_pair_doff = nullptr, *d_doff = nullptr;
+    BIMINE_CUDA(cudaMallocAsync((void **)&diag, sizeof(double) * std::max<int64_t>(dtotal, 1), st));
+    BIMINE_CUDA(cudaMallocAsync((void **)&d_pairs, sizeof(int64_t) * dpairs.size(), st));
+    BIMINE_CUDA(cudaMallocAsync((void **)&d_pair_doff, sizeof(int64_t) * dpairs.size(), st));
+    BIMINE_CUDA(cudaMallocAsync((void **)&d_doff, sizeof(int64_t) * nprob, st));
+    BIMINE_CUDA(cudaMemcpyAsync(d_pairs, dpairs.data(), sizeof(int64_t) * dpairs.size(), cudaMemcpyHostToDevice, st));
+    BIMINE_CUDA(cudaMemcpyAsync(d_pair_doff, pair_doff.data(), sizeof(int64_t) * dpairs.size(), cudaMemcpyHostToDevice, st));
+    BIMINE_CUDA(cudaMemcpyAsync(d_doff, doff.data(), sizeof(int64_t) * nprob, cudaMemcpyHostToDevice, st));
+    {
+      const int mmax = *std::max_element(pm.begin(), pm.end());
+      const int64_t per_band = nw_diag_steps(mmax) * 32;
+      const dim3 grid((unsigned)std::min<int64_t>((per_band + 255) / 256, 64), (unsigned)gmax_d, (unsigned)dpairs.size());
+      nw_diag_kernel<<<grid, 256, 0, st>>>(A.sim, A.sim_off, A.pair_n, A.pair_m, d_pairs, d_pair_doff, A.mismatch,
+                                           A.bonus - A.mismatch, diag);  // one IEEE subtraction, as fsub on the device
+      BIMINE_CUDA(cudaGetLastError());
+    }
     uint32_t *dirs = nullptr;
     int64_t *offs = nullptr;
+    double *lastv = nullptr;
     BIMINE_CUDA(cudaMallocAsync((void **)&dirs, sizeof(uint32_t) * stride * nprob, st));
     BIMINE_CUDA(cudaMallocAsync((void **)&offs, sizeof(int64_t) * nprob, st));
+    BIMINE_CUDA(cudaMallocAsync((void **)&lastv, sizeof(double) * nprob, st));
     std::vector<int64_t> h(nprob);
     for (int64_t k = 0; k < nprob; ++k) h[k] = k * stride;
     BIMINE_CUDA(cudaMemcpyAsync(offs, h.data(), sizeof(int64_t) * nprob, cudaMemcpyHostToDevice, st));
-    if (nprob > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "nw: too many large problems");
-    // wrap-around boundary rows: [2][max_m + 1] tagged slots per problem, tags -1
+    // wrap-around rows: [2][max_m + 1] tagged slots per problem, tags -1
     const int64_t rows_stride = 2 * ((int64_t)max_m + 1);
     double2 *rows = nullptr;
     BIMINE_CUDA(cudaMallocAsync((void **)&rows, sizeof(double2) * rows_stride * nprob, st));
     BIMINE_CUDA(cudaMemsetAsync(rows, 0xff, sizeof(double2) * rows_stride * nprob, st));
-    BIMINE_CUDA(cudaFuncSetAttribute(nw_big_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem));
-    nw_big_kernel<MODE><<<(unsigned)nprob, kBigWarps * 32, kBigSmem, st>>>(A, dirs, offs, rows, rows_stride);
+    BIMINE_CUDA(cudaLaunchKernelEx(&cfg, kern, A, dirs, (const int64_t *)offs, rows, rows_stride, lastv, (const double *)diag,
+                                   (const int64_t *)d_doff));
     const cudaError_t e = cudaGetLastError();
     cudaFreeAsync(dirs, st);
     cudaFreeAsync(offs, st);
     cudaFreeAsync(rows, st);
+    cudaFreeAsync(lastv, st);
+    cudaFreeAsync(diag, st);
+    cudaFreeAsync(d_pairs, st);
+    cudaFreeAsync(d_pair_doff, st);
+    cudaFreeAsync(d_doff, st);
     if (e != cudaSuccess) return fail(BIMINE_E_CUDA, std::string("nw_big_kernel: ") + cudaGetErrorString(e));
     return BIMINE_OK;
   }

@@ -231,7 +231,10 @@ __device__ __forceinline__ void nw_solve(const double *__restrict__ sim, int ld,
 // Returns the lane's final value dp[row][M] (cur after the sweep).
 __host__ __device__ inline int nw_groups(int M) { return (M + 31 + 7) >> 3; }
 
-template <bool kGlobal, class Top, class Bot>
+// kDiag: `sim` is the band's block of the diagonal layout (nw_diag_kernel):
+// entry [s][lane] = the lane's match/mismatch term c at step s, so a step
+// reads 32 consecutive doubles (zeros outside the table)
+template <bool kGlobal, class Top, class Bot, bool kDiag = false>
 __device__ __forceinline__ double band_sweep(const double *__restrict__ sim, int ld, int N, int M, int a0, double gap,
                                              double mismatch, double span, Top &top, Bot &bot,
                                              uint16_t *__restrict__ dirs_band) {
@@ -251,13 +254,14 @@ __device__ __forceinline__ double band_sweep(const double *__restrict__ sim, int
   const int nsteps = M + 31;
   double nxt[8];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) nxt[u] = ldr(u - lane + 1);
+  for (int u = 0; u < 8; ++u) nxt[u] = kDiag ? __ldg(sim + u * 32 + lane) : ldr(u - lane + 1);
   for (int s0 = 0, grp = 0; s0 < nsteps; s0 += 8, ++grp) {
     double c[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) c[u] = fadd(mismatch, fmul(nxt[u], span));
+    for (int u = 0; u < 8; ++u) c[u] = kDiag ? nxt[u] : fadd(mismatch, fmul(nxt[u], span));
 #pragma unroll
-    for (int u = 0; u < 8; ++u) nxt[u] = ldr(s0 + 8 + u - lane + 1);
+    for (int u = 0; u < 8; ++u)
+      nxt[u] = kDiag ? __ldg(sim + (int64_t)(s0 + 8 + u) * 32 + lane) : ldr(s0 + 8 + u - lane + 1);
     // steps s0+u with 1 <= b <= M for this lane
     const int lo = max(lane - s0, 0), hi = min(lane + M - 1 - s0, 7);
     const uint32_t vmask = (active && lo <= hi) ? (((2u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
@@ -631,13 +635,22 @@ namespace bimine {
 // (bit l = lane l's cell), written coalesced; the traceback walks them on
 // lane 0 from a 64-step window staged by the whole warp, and the match
 // scores are gathered in parallel afterwards.
-constexpr int kBigWarps = 16;
+#ifndef BIMINE_BIG_W
+#define BIMINE_BIG_W 8
+#endif
+constexpr int kBigW = BIMINE_BIG_W;  // warps per CTA of the band pipeline (one per SM sub-partition)
 constexpr int kRing = 128;  // boundary values buffered per ring
 
 // A ring slot carries its value and the position it holds, written by one
 // 16-byte shared-memory store, so a consumer polling the slot's position
 // sees a consistent value without any fence (a __threadfence_block per step
 // would wait for the warp's outstanding global direction stores).
+#ifndef BIMINE_SPIN_NS
+#define BIMINE_SPIN_NS 0
+#endif
+constexpr unsigned kSpinNs = BIMINE_SPIN_NS;  // back-off of the band pipeline's spin waits (0: none;
+                                              // measured: any back-off slows the pipeline)
+
 struct BigRing {
   double2 slot[kRing];      // .x = value, .y = position bits (as double bits)
   volatile long long cons;  // positions consumed (capacity hint for the producer)
@@ -683,7 +696,7 @@ struct TopTagged {
                    : "r"((unsigned)__cvta_generic_to_shared(q))
                    : "memory");
     } else {
-      asm volatile("ld.volatile.global.v2.f64 {%0, %1}, [%2];" : "=d"(v), "=d"(td) : "l"(buf + b) : "memory");
+      asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v), "=d"(td) : "l"(buf + b) : "memory");
     }
     t = __double2loint(td);
   }
@@ -717,7 +730,10 @@ struct TopTagged {
 #pragma unroll
       for (int u = 0; u < 9; ++u) {
         const int b = min(s0 + u, M);
-        while (pt[u] != (int)(base + b)) ld(b, rb[u], pt[u]);
+        while (pt[u] != (int)(base + b)) {
+          if (kSpinNs) __nanosleep(kSpinNs);
+          ld(b, rb[u], pt[u]);
+        }
       }
       *cons = base + min(s0 + 8, M);  // columns below s0+8 are not read again
       return;
@@ -727,7 +743,10 @@ struct TopTagged {
     for (int u = 0; u < 9; ++u) {
       const int b = min(s0 + u, M);
       const int want = (int)(base + b);
-      while (pt[u] != want) ld(b, pv[u], pt[u]);
+      while (pt[u] != want) {
+        if (kSpinNs) __nanosleep(kSpinNs);
+        ld(b, pv[u], pt[u]);
+      }
       rb[u] = pv[u];
     }
     fetch(s0 + 8);
@@ -744,8 +763,8 @@ struct BotRing {
   __device__ void reserve(int s0) const {
     if (!on) return;
     const long long last = base + (s0 + 7 - 30);
-    while (last - out->cons >= kRing - 1) {
-    }
+    while (last - out->cons >= kRing - 1)
+      if (kSpinNs) __nanosleep(kSpinNs);
   }
   __device__ void put(int s, bool v, double best) const {
     if (!(on && v && (threadIdx.x & 31) == 31)) return;
@@ -770,23 +789,116 @@ struct BotRowG {  // lane 31 writes tagged slots of a global row
   __device__ void put(int s, bool v, double best) const {
     if (!(on && v && (threadIdx.x & 31) == 31)) return;
     const int b = s - 30;
-    asm volatile("st.volatile.global.v2.f64 [%0], {%1, %2};" ::"l"(row + b), "d"(best),
+    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(row + b), "d"(best),
                  "d"(__longlong_as_double(base + b))
                  : "memory");
   }
 };
 
-constexpr size_t kBigSmem = kBigWarps * sizeof(BigRing);
+template <int W>
+constexpr size_t big_smem_bytes() { return W * sizeof(BigRing); }
 
-template <int MODE>
-__global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, uint32_t *g_dirs_all,
-                                                                 const int64_t *dir_off, double2 *g_rows,
-                                                                 int64_t rows_stride) {
+// Diagonal layout of a problem's band g: steps s = 0 .. nw_diag_steps(M)-1
+// (M + 31 rounded up to the group size, plus one prefetch group), 32 lanes.
+__host__ __device__ inline int64_t nw_diag_steps(int M) { return (int64_t)((M + 31 + 7) & ~7) + 8; }
+
+// One pass per large pair: c = mismatch + R[a-1][b-1] * (bonus - mismatch)
+// (the sweep's two IEEE ops, kernels.py:47-52 / _nwcore.pyx:27) stored at
+// [g][s][l] for reversed row a = 32g + 1 + l, column b = s - l + 1, so a
+// warp step of the sweep reads 32 consecutive doubles.
+__global__ void __launch_bounds__(256) nw_diag_kernel(const double *__restrict__ sim_all,
+                                                       const int64_t *__restrict__ sim_off,
+                                                       const int32_t *__restrict__ pair_n,
+                                                       const int32_t *__restrict__ pair_m,
+                                                       const int64_t *__restrict__ pairs,
+                                                       const int64_t *__restrict__ diag_off, double mismatch,
+                                                       double span, double *__restrict__ diag_all) {
+  const int64_t ps = blockIdx.z;
+  const int g = blockIdx.y;
+  const int64_t pair = pairs[ps];
+  const int N = pair_n[pair], M = pair_m[pair];
+  if (32 * g >= N) return;
+  const double *__restrict__ sim = sim_all + sim_off[pair];
+  const int64_t S = nw_diag_steps(M);
+  double *__restrict__ out = diag_all + diag_off[ps] + (int64_t)g * S * 32;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < S * 32; x += (int64_t)gridDim.x * blockDim.x) {
+    const int l = (int)(x & 31);
+    const int64_t st = x >> 5;
+    const int a = 32 * g + 1 + l;
+    const int64_t b = st - l + 1;
+    double v = 0.0;
+    if (a <= N && b >= 1 && b <= M) v = fadd(mismatch, fmul(sim[(int64_t)(N - a) * M + (M - b)], span));
+    out[x] = v;
+  }
+}
+
+// Large problems: one thread-block cluster of K CTAs x W warps per problem.
+// Band g runs on CTA (g / W) mod K, warp g mod W, round g / (W K).  The
+// boundary into warp w of a CTA is that CTA's shared-memory ring w: rings
+// 1..W-1 are written by the CTA's own warps, ring 0 by the last warp of the
+// previous CTA of the cluster through distributed shared memory
+// (st.shared::cluster; the producer polls the consumer's remote `cons`).
+// The wrap-around boundary (last warp of CTA K-1 -> warp 0 of CTA 0, next
+// round) is a full global row of tagged slots, double-buffered by round
+// parity.  Every capacity wait points to a band of the same round further
+// right and ends at the wrap row, which never waits, and every data wait to
+// a lower band: the wait graph is acyclic for any N, M, K.  A cluster is
+// co-scheduled, so all of a problem's CTAs are resident together.  After a
+// cluster barrier, CTA 0 walks the traceback.
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same shared-memory object in CTA `rank`
+__device__ __forceinline__ unsigned cluster_addr(const void *p, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(rank));
+  return r;
+}
+
+struct BotRemote {  // lane 31 writes ring 0 of the next CTA of the cluster
+  unsigned slot0;   // shared::cluster address of its slot[0]
+  unsigned cons;    // shared::cluster address of its cons
+  long long base;
+  bool on;
+  __device__ void reserve(int s0) const {
+    if (!on) return;
+    const long long last = base + (s0 + 7 - 30);
+    while (true) {
+      long long c;
+      asm volatile("ld.relaxed.cluster.shared::cluster.b64 %0, [%1];" : "=l"(c) : "r"(cons) : "memory");
+      if (last - c < kRing - 1) break;
+      if (kSpinNs) __nanosleep(kSpinNs);
+    }
+  }
+  __device__ void put(int s, bool v, double best) const {
+    if (!(on && v && (threadIdx.x & 31) == 31)) return;
+    const long long pos = base + (s - 30);
+    asm volatile("st.relaxed.cluster.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(slot0 + (unsigned)((pos & (kRing - 1)) * 16)),
+                 "d"(best), "d"(__longlong_as_double(pos))
+                 : "memory");
+  }
+};
+
+template <int MODE, int W>
+__global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t *g_dirs_all, const int64_t *dir_off,
+                                                        double2 *g_rows, int64_t rows_stride, double *last_val,
+                                                        const double *diag_all, const int64_t *diag_off) {
   extern __shared__ __align__(16) unsigned char big_smem[];
-  BigRing *rings = (BigRing *)big_smem;  // [kBigWarps], slot w feeds warp w (w >= 1)
-  __shared__ double s_last;
+  BigRing *rings = (BigRing *)big_smem;  // [W], ring w feeds warp w
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t q = A.problem_ids ? A.problem_ids[blockIdx.x] : (int64_t)blockIdx.x;
+  const int crank = (int)cluster_rank(), K = (int)cluster_size();
+  const int64_t slot = blockIdx.x / K;
+  const int64_t q = A.problem_ids ? A.problem_ids[slot] : slot;
   const int64_t pair = q / A.n_settings;
   const int setting = (int)(q % A.n_settings);
   const int N = A.pair_n[pair], M = A.pair_m[pair];
@@ -794,46 +906,77 @@ __global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, 
   const double gap = A.gap_per_problem ? A.gap[q] : A.gap[setting];
   const double ng = -gap, mismatch = A.mismatch, span = fsub(A.bonus, A.mismatch);
   const int G = (N + 31) >> 5, G8 = nw_groups(M);
-  uint16_t *dirs = (uint16_t *)(g_dirs_all + dir_off[blockIdx.x]);  // [G][G8][32]
-  double2 *wrap = g_rows + (int64_t)blockIdx.x * rows_stride;      // [2][M+1] tagged, pre-filled with tag -1
+  uint16_t *dirs = (uint16_t *)(g_dirs_all + dir_off[slot]);  // [G][G8][32]
+  double2 *wrap = g_rows + slot * rows_stride;                // [2][M+1] tagged, pre-filled with tag -1
   const long long W1 = (long long)M + 1;
-  for (int k = threadIdx.x; k < kBigWarps * kRing; k += blockDim.x)
+  const int per_round = W * K;
+  const double *__restrict__ diag = diag_all + diag_off[slot];  // [G][nw_diag_steps(M)][32]
+  const int64_t dstride = nw_diag_steps(M) * 32;
+  for (int k = threadIdx.x; k < W * kRing; k += blockDim.x)
     rings[k / kRing].slot[k % kRing] = make_double2(0.0, __longlong_as_double(-1ll));
-  if (threadIdx.x < kBigWarps) rings[threadIdx.x].cons = 0;
+  if (threadIdx.x < W) rings[threadIdx.x].cons = 0;
   __syncthreads();
-  for (int g = warp, gen = 0; g < G; g += kBigWarps, ++gen) {
-    const int ogen = (g + 1) / kBigWarps;
-    const bool out_wrap = (warp + 1) == kBigWarps;
+  cluster_barrier();  // every ring initialised before any remote write
+#ifdef BIMINE_NW_PROFILE
+  if (threadIdx.x == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    printf("prof start cta %d ns %llu\n", crank, gt);
+  }
+#endif
+  const bool has_next = crank + 1 < K;
+  const unsigned r_slot0 = has_next ? cluster_addr(&rings[0].slot[0], crank + 1) : 0u;
+  const unsigned r_cons = has_next ? cluster_addr((const void *)&rings[0].cons, crank + 1) : 0u;
+  for (int g = crank * W + warp, gen = 0; g < G; g += per_round, ++gen) {
     double fin;
-    // output side
-    BotRing bring{&rings[(warp + 1) % kBigWarps], (long long)ogen * W1, M, g + 1 < G && !out_wrap};
-    BotRowG brow{wrap + (ogen & 1) * W1, (long long)ogen * W1, g + 1 < G && out_wrap};
-    struct Bot2 {
+    const bool last_warp = warp + 1 == W;
+    const int ogr = (g + 1) / per_round;  // round of the consumer band
+    BotRing bring{&rings[(warp + 1) % W], (long long)gen * W1, M, g + 1 < G && !last_warp};
+    BotRemote brem{r_slot0, r_cons, (long long)gen * W1, g + 1 < G && last_warp && has_next};
+    BotRowG brow{wrap + (ogr & 1) * W1, (long long)(g + 1) * W1, g + 1 < G && last_warp && !has_next};
+    struct Bot3 {
       const BotRing &r;
+      const BotRemote &x;
       const BotRowG &w;
-      __device__ void reserve(int s0) const { r.reserve(s0); }
+      __device__ void reserve(int s0) const {
+        r.reserve(s0);
+        x.reserve(s0);
+      }
       __device__ void put(int s_, bool v, double best) const {
         r.put(s_, v, best);
+        x.put(s_, v, best);
         w.put(s_, v, best);
       }
-    } bot{bring, brow};
+    } bot{bring, brem, brow};
     uint16_t *dband = dirs + (int64_t)g * G8 * 32;
+    const double *dg = diag + g * dstride;
     if (g == 0) {
       TopAnalytic top{ng};
-      fin = band_sweep<true>(sim, M, N, M, 0, gap, mismatch, span, top, bot, dband);
-    } else if (warp == 0) {
-      TopTagged<false> top{wrap + (gen & 1) * W1, nullptr, (long long)gen * W1, M, fmul(ng, (double)(32 * g))};
-      fin = band_sweep<true>(sim, M, N, M, 32 * g, gap, mismatch, span, top, bot, dband);
+      fin = band_sweep<true, TopAnalytic, Bot3, true>(dg, M, N, M, 0, gap, mismatch, span, top, bot, dband);
+    } else if (warp == 0 && crank == 0) {
+      TopTagged<false> top{wrap + (gen & 1) * W1, nullptr, (long long)g * W1, M, fmul(ng, (double)(32 * g))};
+      fin = band_sweep<true, TopTagged<false>, Bot3, true>(dg, M, N, M, 32 * g, gap, mismatch, span, top, bot, dband);
     } else {
       BigRing *in = &rings[warp];
       TopTagged<true> top{in->slot, &in->cons, (long long)gen * W1, M, fmul(ng, (double)(32 * g))};
-      fin = band_sweep<true>(sim, M, N, M, 32 * g, gap, mismatch, span, top, bot, dband);
+      fin = band_sweep<true, TopTagged<true>, Bot3, true>(dg, M, N, M, 32 * g, gap, mismatch, span, top, bot, dband);
       if (lane == 0) in->cons = (long long)(gen + 1) * W1;  // generation done
     }
-    if (32 * g + 1 + lane == N) s_last = fin;
+    if (32 * g + 1 + lane == N) last_val[slot] = fin;
     __syncwarp();
+#ifdef BIMINE_NW_PROFILE
+    if (lane == 0) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      printf("prof band %d cta %d end_ns %llu\n", g, crank, gt);
+    }
+#endif
   }
+  // all bands of the problem are done (and no remote access is pending)
   __syncthreads();
+  cluster_barrier();
+  if (crank != 0) return;
+  const double s_last = __ldcg(&last_val[slot]);
   if (MODE == kNwTable) return;
   // ---- traceback on warp 0: lane 0 walks, the warp stages 16 direction
   // groups (128 steps) of the current band at a time
@@ -934,6 +1077,13 @@ __global__ void __launch_bounds__(kBigWarps * 32) nw_big_kernel(const NwArgs A, 
       if (lane == 0) A.counts[q] = (int32_t)kept;
     }
     if (lane == 0 && A.score) A.score[q] = s_last;
+#ifdef BIMINE_NW_PROFILE
+    if (lane == 0) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      printf("prof traceback end_ns %llu\n", gt);
+    }
+#endif
   }
 }
 
