@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cstdlib>
 #include <cstdio>
@@ -17,6 +18,7 @@
 #include <numeric>
 #include <string>
 #include <unordered_map>
+#include <thread>
 #include <vector>
 
 #include "../../include/bimine_b200.h"
@@ -56,6 +58,59 @@ int num_sms() {
   }
   return sms;
 }
+
+// a non-blocking upload stream per device (host -> device copies that
+// overlap the mining of the previous chunk)
+std::mutex g_cs_mu;
+std::map<int, cudaStream_t> g_copy_streams;
+cudaStream_t copy_stream() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cs_mu);
+  auto it = g_copy_streams.find(dev);
+  if (it != g_copy_streams.end()) return it->second;
+  cudaStream_t s = nullptr;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  g_copy_streams[dev] = s;
+  return s;
+}
+
+// two doubles into device memory without a host copy (a pageable
+// host-to-device copy would synchronise the stream)
+__global__ void set_pair_kernel(double *dst, double a, double b) {
+  dst[0] = a;
+  dst[1] = b;
+}
+
+// pinned host scratch per thread, grown on demand (upload staging)
+struct PinnedScratch {
+  void *p = nullptr;
+  size_t n = 0;
+  ~PinnedScratch() {
+    if (p) cudaFreeHost(p);
+  }
+};
+thread_local PinnedScratch tl_pinned;
+void *pinned_scratch(size_t bytes) {
+  if (tl_pinned.n < bytes) {
+    if (tl_pinned.p) cudaFreeHost(tl_pinned.p);
+    tl_pinned.p = nullptr;
+    tl_pinned.n = 0;
+    if (cudaMallocHost(&tl_pinned.p, bytes) != cudaSuccess) return nullptr;
+    tl_pinned.n = bytes;
+  }
+  return tl_pinned.p;
+}
+
+// Upload gate of bimine_mine_host: the score kernel waits per chunk; the
+// launches that read everything (long-sentence kernel, NW) wait for `all`.
+struct UploadGate {
+  const int32_t *ready;  // grows as pieces land
+  const int32_t *need;   // per pair: the counter value its data need
+  cudaEvent_t all;
+};
+thread_local const UploadGate *tl_gate = nullptr;
+cudaError_t gate_wait_all(cudaStream_t st) { return tl_gate ? cudaStreamWaitEvent(st, tl_gate->all, 0) : cudaSuccess; }
 
 void pool_setup() {
   static std::once_flag once;
@@ -190,10 +245,8 @@ int bimine_plan_batch(const bimine_batch *b, int64_t *work, int64_t work_cap, bi
   if (!b || !plan || (work_cap > 0 && !work)) return fail(BIMINE_E_ARG, "bimine_plan_batch: null argument");
   bimine_plan P;
   memset(&P, 0, sizeof(P));
-  for (int64_t s = 0; s < b->n_sentences; ++s) {
-    P.max_uniq = std::max(P.max_uniq, b->sent_uniq[s]);
-    P.max_len = std::max(P.max_len, b->sent_len[s]);
-  }
+  // maxima over the sentences the pairs reference (a view of a larger batch
+  // plans in time proportional to its own pairs)
   std::vector<int64_t> longs, larges;
   int64_t t = 0;
   for (int64_t p = 0; p < b->n_pairs; ++p)
@@ -203,9 +256,17 @@ int bimine_plan_batch(const bimine_batch *b, int64_t *work, int64_t work_cap, bi
     if (n < 1 || m < 1) return fail(BIMINE_E_ARG, "bimine_plan_batch: empty document");
     P.max_n = std::max(P.max_n, n);
     P.max_m = std::max(P.max_m, m);
-    int32_t ml = 0;
-    for (int32_t i = 0; i < n; ++i) ml = std::max(ml, b->sent_len[b->pair_src[p] + i]);
-    for (int32_t j = 0; j < m; ++j) ml = std::max(ml, b->sent_len[b->pair_tgt[p] + j]);
+    int32_t ml = 0, mu = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      ml = std::max(ml, b->sent_len[b->pair_src[p] + i]);
+      mu = std::max(mu, b->sent_uniq[b->pair_src[p] + i]);
+    }
+    for (int32_t j = 0; j < m; ++j) {
+      ml = std::max(ml, b->sent_len[b->pair_tgt[p] + j]);
+      mu = std::max(mu, b->sent_uniq[b->pair_tgt[p] + j]);
+    }
+    P.max_len = std::max(P.max_len, ml);
+    P.max_uniq = std::max(P.max_uniq, mu);
     if (ml > kPairMaxLen || n > kPairMax || m > kPairMax) larges.push_back(p);
     if (ml > kPairMaxLen) {
       longs.push_back(p);
@@ -338,6 +399,10 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
     // one launch: the tiles of pairs larger than 64x64, then one CTA per pair
     A.tiles = plan->n_tiles ? plan->work : nullptr;
     A.n_tiles = plan->n_tiles;
+    if (tl_gate) {
+      A.ready = tl_gate->ready;
+      A.need = tl_gate->need;
+    }
     const int64_t grid = plan->n_tiles + b->n_pairs;
     if (grid > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: too many CTAs");
     pair_kernel<<<(unsigned)grid, kPairThreads, smem, st>>>(A);
@@ -346,6 +411,7 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
     if (le != cudaSuccess) return fail(BIMINE_E_CUDA, std::string("pair_kernel: ") + cudaGetErrorString(le));
   }
   if (plan->n_long > 0) {
+    BIMINE_CUDA(gate_wait_all(st));
     ScoreArgs A;
     A.b = bd;
     A.d = dd;
@@ -605,11 +671,11 @@ int bimine_mine_batch(const bimine_dict *dict, const double *model, const bimine
   FusedNw nw{gap, threshold, mismatch, bonus, out_off_dev, matches_dev, counts_dev, score_dev};
   int rc = launch_scores(dict, model, b, plan, sim_dev, fuse ? &nw : nullptr, st);
   if (rc != BIMINE_OK) return rc;
+  BIMINE_CUDA(gate_wait_all(st));
   if (!fuse) {
     double *par = nullptr;
     BIMINE_CUDA(cudaMallocAsync((void **)&par, 2 * sizeof(double), st));
-    const double hpar[2] = {gap, threshold};
-    BIMINE_CUDA(cudaMemcpyAsync(par, hpar, sizeof(hpar), cudaMemcpyHostToDevice, st));
+    set_pair_kernel<<<1, 1, 0, st>>>(par, gap, threshold);
     NwArgs A = nw_args_base(sim_dev, b->pair_sim_off, b->pair_n, b->pair_m, b->n_pairs, 1, par, mismatch, bonus);
     A.threshold = par + 1;
     A.out_off = out_off_dev;
@@ -624,8 +690,7 @@ int bimine_mine_batch(const bimine_dict *dict, const double *model, const bimine
   // pairs larger than one CTA: their NW as a separate launch
   double *par = nullptr;
   BIMINE_CUDA(cudaMallocAsync((void **)&par, 2 * sizeof(double), st));
-  const double hpar[2] = {gap, threshold};
-  BIMINE_CUDA(cudaMemcpyAsync(par, hpar, sizeof(hpar), cudaMemcpyHostToDevice, st));
+  set_pair_kernel<<<1, 1, 0, st>>>(par, gap, threshold);
   NwArgs A = nw_args_base(sim_dev, b->pair_sim_off, b->pair_n, b->pair_m, plan->n_large, 1, par, mismatch, bonus);
   A.problem_ids = plan->work + 3 * plan->n_tiles + plan->n_long;
   A.threshold = par + 1;
@@ -765,26 +830,56 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   if (P == 0) return BIMINE_OK;
   pool_setup();
   cudaStream_t st = as_stream(stream);
-  std::vector<int64_t> out_off(P);
-  int64_t work_cap = P;
+  // Uploads start at once on a copy stream: pair and sentence arrays, then
+  // the tokens in `nt` equal pieces, a device counter bumped after each
+  // (1 = pairs + sentences, 1 + j = token pieces 0..j-1).  Meanwhile host
+  // threads check and plan the batch in chunks of pairs and record each
+  // pair's counter value; the score kernel's CTA for a pair starts once the
+  // counter reaches it.
+  static const int max_chunks = [] {
+    const char *v = getenv("BIMINE_E2E_CHUNKS");
+    return v ? std::max(1, atoi(v)) : 16;
+  }();
+  static const int64_t min_tokens = [] {
+    const char *v = getenv("BIMINE_E2E_MIN_TOKENS");
+    return v ? std::max<int64_t>(1, atoll(v)) : (int64_t)1 << 20;
+  }();
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)max_chunks, T / min_tokens));
+  const int nc = (int)std::max<int64_t>(1, std::min<int64_t>(8, P));  // analysis threads
+  std::vector<int64_t> cut(nc + 1), tcut(nt + 1);
+  for (int k = 0; k <= nc; ++k) cut[k] = P * k / nc;
+  for (int j = 0; j <= nt; ++j) tcut[j] = T * j / nt;
+  // pinned staging: slot offsets [P] | per-pair need [P] (int32) | ready values [nt + 1] | merged work
+  int64_t work_bound = 0;
   for (int64_t p = 0; p < P; ++p)
-    work_cap += 3 * (int64_t)((h->pair_n[p] + kPairMax - 1) / kPairMax) * ((h->pair_m[p] + kPairMax - 1) / kPairMax);
-  std::vector<int64_t> work(std::max<int64_t>(work_cap, 1));
-  bimine_plan plan;
-  {
-    int rc = bimine_plan_batch(h, work.data(), work_cap, &plan);
-    if (rc != BIMINE_OK) return rc;
-  }
+    work_bound += 1 + 3 * (int64_t)((h->pair_n[p] + kPairMax - 1) / kPairMax) * ((h->pair_m[p] + kPairMax - 1) / kPairMax);
+  const int64_t n_stage = P + (P + 1) / 2 + (nt + 2) / 2 + 1 + std::max<int64_t>(work_bound, 1);
+  int64_t *staging = (int64_t *)pinned_scratch(sizeof(int64_t) * n_stage);
+  if (!staging) return fail(BIMINE_E_CUDA, "bimine_mine_host: pinned staging allocation failed");
+  int64_t *out_off = staging;
+  int32_t *need = (int32_t *)(staging + P);
+  int32_t *ready_vals = need + P;
+  int64_t *work = staging + P + (P + 1) / 2 + (nt + 2) / 2 + 1;
+  for (int j = 0; j <= nt; ++j) ready_vals[j] = j + 1;
+  // per pair (O(P)): match slots, cells
   int64_t cap = 0, cells = 0;
   for (int64_t p = 0; p < P; ++p) {
     const int32_t n = h->pair_n[p], m = h->pair_m[p];
+    if (n < 1 || m < 1) return fail(BIMINE_E_ARG, "bimine_plan_batch: empty document");
     out_off[p] = cap;
     cap += std::min(n, m);
     cells = std::max(cells, h->pair_sim_off[p] + (int64_t)n * m);
   }
-  for (int64_t s = 0; s < S; ++s)
-    if (h->sent_len[s] < 1) return fail(BIMINE_E_ARG, "bimine_mine_host: empty sentence");
   if (capacity < cap) return fail(BIMINE_E_ARG, "bimine_mine_host: capacity < sum of min(N, M)");
+  // per chunk, on host threads: validity, the sentence / token prefix it
+  // reads, its plan (a view: pair arrays from p0, sentence arrays whole)
+#ifdef BIMINE_E2E_PROFILE
+  auto hclock = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double h0 = hclock();
+  double h_an = 0, h_enq = 0, h_mine = 0;
+  cudaEvent_t pe[5];
+  for (auto &x : pe) cudaEventCreate(&x);
+#endif
   // one device arena, carved in 256-byte aligned pieces
   size_t off = 0;
   auto carve = [&](size_t bytes) {
@@ -797,65 +892,225 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
                o_pm = carve(4 * P), o_psim = carve(8 * P), o_outoff = carve(8 * P), o_sim = carve(8 * cells),
                o_slots = carve(sizeof(bimine_match) * cap), o_counts = carve(4 * P), o_base = carve(8 * P),
                o_comp = carve(sizeof(bimine_match) * cap), o_total = carve(8),
-               o_work = carve(8 * plan.work_len);
+               o_work = carve(8 * std::max<int64_t>(work_bound, 1)), o_need = carve(4 * P), o_ready = carve(4);
   char *arena = nullptr;
   BIMINE_CUDA(cudaMallocAsync((void **)&arena, off, st));
-  auto H2D = [&](size_t o, const void *src, size_t bytes) {
-    return bytes ? cudaMemcpyAsync(arena + o, src, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+  cudaStream_t cs = copy_stream();
+  cudaEvent_t ev_start = nullptr, ev_all = nullptr;
+  BIMINE_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+  BIMINE_CUDA(cudaEventCreateWithFlags(&ev_all, cudaEventDisableTiming));
+  auto cleanup = [&]() {
+    cudaEventDestroy(ev_start);
+    cudaEventDestroy(ev_all);
   };
-  cudaError_t e = cudaSuccess;
-  e = e ? e : H2D(o_tok, h->tokens, 4 * T);
-  e = e ? e : H2D(o_soff, h->sent_tok_off, 8 * S);
-  e = e ? e : H2D(o_slen, h->sent_len, 4 * S);
-  e = e ? e : H2D(o_suniq, h->sent_uniq, 4 * S);
-  e = e ? e : H2D(o_schar, h->sent_chars, 4 * S);
-  e = e ? e : H2D(o_psrc, h->pair_src, 8 * P);
-  e = e ? e : H2D(o_pn, h->pair_n, 4 * P);
-  e = e ? e : H2D(o_ptgt, h->pair_tgt, 8 * P);
-  e = e ? e : H2D(o_pm, h->pair_m, 4 * P);
-  e = e ? e : H2D(o_psim, h->pair_sim_off, 8 * P);
-  e = e ? e : H2D(o_outoff, out_off.data(), 8 * P);
-  e = e ? e : H2D(o_work, work.data(), 8 * plan.work_len);
-  if (e != cudaSuccess) {
-    cudaFreeAsync(arena, st);
-    return fail(BIMINE_E_CUDA, std::string("bimine_mine_host H2D: ") + cudaGetErrorString(e));
+#ifdef BIMINE_E2E_PROFILE
+  cudaEventRecord(pe[0], st);
+#endif
+  // ---- uploads, issued before any host-side analysis
+  cudaError_t e = cudaMemsetAsync(arena + o_ready, 0, 4, st);
+  e = e ? e : cudaEventRecord(ev_start, st);  // arena + ready counter exist
+  e = e ? e : cudaStreamWaitEvent(cs, ev_start, 0);
+  {
+    auto H2D = [&](size_t o, const void *src, size_t bytes) {
+      if (e == cudaSuccess && bytes) e = cudaMemcpyAsync(arena + o, src, bytes, cudaMemcpyHostToDevice, cs);
+    };
+    H2D(o_psrc, h->pair_src, 8 * P);
+    H2D(o_pn, h->pair_n, 4 * P);
+    H2D(o_ptgt, h->pair_tgt, 8 * P);
+    H2D(o_pm, h->pair_m, 4 * P);
+    H2D(o_psim, h->pair_sim_off, 8 * P);
+    H2D(o_outoff, out_off, 8 * P);
+    H2D(o_soff, h->sent_tok_off, 8 * S);
+    H2D(o_slen, h->sent_len, 4 * S);
+    H2D(o_suniq, h->sent_uniq, 4 * S);
+    H2D(o_schar, h->sent_chars, 4 * S);
+    H2D(o_ready, &ready_vals[0], 4);  // 1: pairs and sentences are in place
+    for (int j = 0; j < nt; ++j) {
+      H2D(o_tok + 4 * tcut[j], h->tokens + tcut[j], 4 * (tcut[j + 1] - tcut[j]));
+      H2D(o_ready, &ready_vals[j + 1], 4);  // j + 2: token pieces 0..j
+    }
+    e = e ? e : cudaEventRecord(ev_all, cs);
+#ifdef BIMINE_E2E_PROFILE
+    cudaEventRecord(pe[1], cs);
+    h_enq = hclock() - h0;
+#endif
   }
-  bimine_batch d;
-  d.n_pairs = P;
-  d.n_sentences = S;
-  d.n_tokens = T;
-  d.tokens = (const int32_t *)(arena + o_tok);
-  d.sent_tok_off = (const int64_t *)(arena + o_soff);
-  d.sent_len = (const int32_t *)(arena + o_slen);
-  d.sent_uniq = (const int32_t *)(arena + o_suniq);
-  d.sent_chars = (const int32_t *)(arena + o_schar);
-  d.pair_src = (const int64_t *)(arena + o_psrc);
-  d.pair_n = (const int32_t *)(arena + o_pn);
-  d.pair_tgt = (const int64_t *)(arena + o_ptgt);
-  d.pair_m = (const int32_t *)(arena + o_pm);
-  d.pair_sim_off = (const int64_t *)(arena + o_psim);
-  double *sim = (double *)(arena + o_sim);
-  plan.work = (const int64_t *)(arena + o_work);
-  int rc = bimine_mine_batch(dict, model, &d, &plan, gap, threshold, mismatch, bonus, sim,
-                             (const int64_t *)(arena + o_outoff), (bimine_match *)(arena + o_slots),
-                             (int32_t *)(arena + o_counts), nullptr, stream);
+  auto abort_with = [&](int code, const std::string &msg) {
+    cudaStreamSynchronize(cs);
+    cudaFreeAsync(arena, st);
+    cudaStreamSynchronize(st);
+    cleanup();
+    return fail(code, msg);
+  };
+  if (e != cudaSuccess) return abort_with(BIMINE_E_CUDA, std::string("bimine_mine_host H2D: ") + cudaGetErrorString(e));
+  // ---- per chunk of pairs, on host threads: validity, each pair's counter
+  //      value, the chunk's plan (a view: pair arrays from p0, sentence arrays whole)
+  struct ChunkInfo {
+    int rc = BIMINE_OK;
+    std::string err;
+    bimine_plan plan;
+    std::vector<int64_t> work;
+  };
+  std::vector<ChunkInfo> ci(nc);
+  auto analyse = [&](int k) {
+    ChunkInfo &c = ci[k];
+    const int64_t p0 = cut[k], p1 = cut[k + 1];
+    int64_t wcap = p1 - p0;
+    for (int64_t p = p0; p < p1; ++p) {
+      const int32_t n = h->pair_n[p], m = h->pair_m[p];
+      wcap += 3 * (int64_t)((n + kPairMax - 1) / kPairMax) * ((m + kPairMax - 1) / kPairMax);
+      int64_t te = 0;
+      for (int pass = 0; pass < 2; ++pass) {
+        const int64_t s0 = pass ? h->pair_tgt[p] : h->pair_src[p];
+        const int32_t cnt = pass ? m : n;
+        if (s0 < 0 || s0 + cnt > S) {
+          c.rc = BIMINE_E_ARG;
+          c.err = "bimine_mine_host: sentence index out of range";
+          return;
+        }
+        for (int32_t q = 0; q < cnt; ++q) {
+          const int32_t len = h->sent_len[s0 + q];
+          if (len < 1) {
+            c.rc = BIMINE_E_ARG;
+            c.err = "bimine_mine_host: empty sentence";
+            return;
+          }
+          te = std::max(te, h->sent_tok_off[s0 + q] + len);
+        }
+      }
+      if (te > T) {
+        c.rc = BIMINE_E_ARG;
+        c.err = "bimine_mine_host: token range out of bounds";
+        return;
+      }
+      int j = (int)std::min<int64_t>(nt - 1, (te - 1) * nt / T);  // piece of the last token read
+      while (j > 0 && tcut[j] > te - 1) --j;
+      while (j + 1 < nt && tcut[j + 1] <= te - 1) ++j;
+      need[p] = j + 2;
+    }
+    bimine_batch hv = *h;
+    hv.n_pairs = p1 - p0;
+    hv.pair_src = h->pair_src + p0;
+    hv.pair_n = h->pair_n + p0;
+    hv.pair_tgt = h->pair_tgt + p0;
+    hv.pair_m = h->pair_m + p0;
+    hv.pair_sim_off = h->pair_sim_off + p0;
+    c.work.resize(std::max<int64_t>(wcap, 1));
+    c.rc = bimine_plan_batch(&hv, c.work.data(), wcap, &c.plan);
+    if (c.rc != BIMINE_OK) c.err = g_error;  // this thread's message
+  };
+  {
+    std::vector<std::thread> th;
+    for (int k = 1; k < nc; ++k) th.emplace_back(analyse, k);
+    analyse(0);
+    for (auto &t : th) t.join();
+  }
+  for (int k = 0; k < nc; ++k)
+    if (ci[k].rc != BIMINE_OK) return abort_with(ci[k].rc, ci[k].err);
+#ifdef BIMINE_E2E_PROFILE
+  h_an = hclock() - h0;
+#endif
+  // merged plan: tiles, then long pairs, then large pairs (chunk order, global pair ids)
+  bimine_plan plan;
+  memset(&plan, 0, sizeof(plan));
+  for (int k = 0; k < nc; ++k) {
+    const bimine_plan &q = ci[k].plan;
+    plan.max_n = std::max(plan.max_n, q.max_n);
+    plan.max_m = std::max(plan.max_m, q.max_m);
+    plan.max_uniq = std::max(plan.max_uniq, q.max_uniq);
+    plan.max_len = std::max(plan.max_len, q.max_len);
+    plan.long_max_n = std::max(plan.long_max_n, q.long_max_n);
+    plan.long_max_m = std::max(plan.long_max_m, q.long_max_m);
+    plan.n_tiles += q.n_tiles;
+    plan.n_long += q.n_long;
+    plan.n_large += q.n_large;
+    plan.n_cells = std::max(plan.n_cells, q.n_cells);
+  }
+  plan.work_len = 3 * plan.n_tiles + plan.n_long + plan.n_large;
+  {
+    int64_t t = 0, l = 3 * plan.n_tiles, g = l + plan.n_long;
+    for (int k = 0; k < nc; ++k) {
+      const bimine_plan &q = ci[k].plan;
+      const int64_t *w = ci[k].work.data(), p0 = cut[k];
+      for (int64_t x = 0; x < q.n_tiles; ++x, ++t) {
+        work[3 * t] = w[3 * x] + p0;
+        work[3 * t + 1] = w[3 * x + 1];
+        work[3 * t + 2] = w[3 * x + 2];
+      }
+      for (int64_t x = 0; x < q.n_long; ++x) work[l++] = w[3 * q.n_tiles + x] + p0;
+      for (int64_t x = 0; x < q.n_large; ++x) work[g++] = w[3 * q.n_tiles + q.n_long + x] + p0;
+    }
+  }
+  e = cudaMemcpyAsync(arena + o_work, work, 8 * plan.work_len, cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(arena + o_need, need, 4 * P, cudaMemcpyHostToDevice, st);
+  int rc = BIMINE_OK;
+  if (e == cudaSuccess) {
+    bimine_batch d;
+    d.n_pairs = P;
+    d.n_sentences = S;
+    d.n_tokens = T;
+    d.tokens = (const int32_t *)(arena + o_tok);
+    d.sent_tok_off = (const int64_t *)(arena + o_soff);
+    d.sent_len = (const int32_t *)(arena + o_slen);
+    d.sent_uniq = (const int32_t *)(arena + o_suniq);
+    d.sent_chars = (const int32_t *)(arena + o_schar);
+    d.pair_src = (const int64_t *)(arena + o_psrc);
+    d.pair_n = (const int32_t *)(arena + o_pn);
+    d.pair_tgt = (const int64_t *)(arena + o_ptgt);
+    d.pair_m = (const int32_t *)(arena + o_pm);
+    d.pair_sim_off = (const int64_t *)(arena + o_psim);
+    plan.work = (const int64_t *)(arena + o_work);
+    const UploadGate gate{(const int32_t *)(arena + o_ready), (const int32_t *)(arena + o_need), ev_all};
+    tl_gate = &gate;
+    rc = bimine_mine_batch(dict, model, &d, &plan, gap, threshold, mismatch, bonus, (double *)(arena + o_sim),
+                           (const int64_t *)(arena + o_outoff), (bimine_match *)(arena + o_slots),
+                           (int32_t *)(arena + o_counts), nullptr, stream);
+    tl_gate = nullptr;
+    // (every later launch on st follows NW, which waited for all uploads)
+#ifdef BIMINE_E2E_PROFILE
+    cudaEventRecord(pe[2], st);
+    h_mine = hclock() - h0;
+#endif
+  } else {
+    rc = fail(BIMINE_E_CUDA, std::string("bimine_mine_host H2D: ") + cudaGetErrorString(e));
+  }
   if (rc == BIMINE_OK)
     rc = bimine_compact_matches((const bimine_match *)(arena + o_slots), (const int64_t *)(arena + o_outoff),
                                 (const int32_t *)(arena + o_counts), P, (int64_t *)(arena + o_base),
                                 (bimine_match *)(arena + o_comp), (int64_t *)(arena + o_total), stream);
   if (rc != BIMINE_OK) {
+    cudaStreamSynchronize(cs);
+    cudaStreamSynchronize(st);
     cudaFreeAsync(arena, st);
+    cudaStreamSynchronize(st);
+    cleanup();
     return rc;
   }
+#ifdef BIMINE_E2E_PROFILE
+  cudaEventRecord(pe[3], st);
+#endif
   e = cudaMemcpyAsync(counts_host, arena + o_counts, 4 * P, cudaMemcpyDeviceToHost, st);
   e = e ? e : cudaMemcpyAsync(total_host, arena + o_total, 8, cudaMemcpyDeviceToHost, st);
-  if (sim_host && !e) e = cudaMemcpyAsync(sim_host, sim, 8 * cells, cudaMemcpyDeviceToHost, st);
+  if (sim_host && !e) e = cudaMemcpyAsync(sim_host, arena + o_sim, 8 * cells, cudaMemcpyDeviceToHost, st);
   e = e ? e : cudaStreamSynchronize(st);
   if (!e && *total_host > 0 && matches_host)
     e = cudaMemcpyAsync(matches_host, arena + o_comp, sizeof(bimine_match) * (*total_host), cudaMemcpyDeviceToHost,
                         st);
   cudaFreeAsync(arena, st);
+#ifdef BIMINE_E2E_PROFILE
+  cudaEventRecord(pe[4], st);
+#endif
   e = e ? e : cudaStreamSynchronize(st);
+  cleanup();
+#ifdef BIMINE_E2E_PROFILE
+  {
+    float t[5];
+    for (int k = 1; k < 5; ++k) cudaEventElapsedTime(&t[k], pe[0], pe[k]);
+    fprintf(stderr, "e2e host: analysed %.3f enqueued copies %.3f enqueued mine %.3f done %.3f | device from first op: copies done %.3f, mine+nw done %.3f, compaction done %.3f, d2h done %.3f\n",
+            h_an, h_enq, h_mine, hclock() - h0, t[1], t[2], t[3], t[4]);
+    for (auto &x : pe) cudaEventDestroy(x);
+  }
+#endif
   if (e != cudaSuccess) return fail(BIMINE_E_CUDA, std::string("bimine_mine_host: ") + cudaGetErrorString(e));
   return BIMINE_OK;
 }

@@ -63,6 +63,10 @@ struct PairArgs {
   int32_t *nw_counts;
   double *nw_score;          // optional
   double gap, threshold, mismatch, bonus;
+  // upload gate (bimine_mine_host): pair p's data are on the device once
+  // *ready >= need[p] (the counter grows as pieces land); null: no wait
+  const int32_t *ready;
+  const int32_t *need;
 };
 
 constexpr int kSegItems = 64;   // dictionary entries examined per warp segment
@@ -211,6 +215,18 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
     j0 = (int)A.tiles[3 * (int64_t)blockIdx.x + 2];
   } else {
     p = (int64_t)blockIdx.x - A.n_tiles;
+  }
+  if (A.ready) {  // wait until the chunk holding this pair's data has landed
+    if (threadIdx.x == 0) {
+      const int want = A.need[p];
+      while (true) {
+        int r;
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(r) : "l"(A.ready) : "memory");
+        if (r >= want) break;
+        __nanosleep(256);
+      }
+    }
+    __syncthreads();
   }
   const int Nfull = A.b.pair_n[p], Mfull = A.b.pair_m[p];
   if (!is_tile && (Nfull > kPairMax || Mfull > kPairMax)) return;

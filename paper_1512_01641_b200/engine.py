@@ -42,9 +42,10 @@ class DeviceDictionary:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h and N._lib is not None:
+        lib = getattr(N, "_lib", None) if N is not None else None  # None at interpreter shutdown
+        if h and lib is not None:
             try:
-                N._lib.bimine_dict_destroy(h)
+                lib.bimine_dict_destroy(h)
             except Exception:
                 pass
 
@@ -210,9 +211,9 @@ def mine_host(dd: DeviceDictionary, model_vec: np.ndarray, batch: PackedBatch, g
     L = N.load()
     torch = _torch()
     P = batch.n_pairs
-    counts = np.zeros(max(P, 1), dtype=np.int32)
+    counts = np.empty(max(P, 1), dtype=np.int32)  # filled for every pair
     cap = int(batch.match_capacity()[-1])
-    matches = np.zeros(max(cap, 1), dtype=N.MATCH_DTYPE)
+    matches = np.empty(max(cap, 1), dtype=N.MATCH_DTYPE)  # the first `total` are filled
     total = np.zeros(1, dtype=np.int64)
     sim = np.empty(max(batch.n_cells, 1), dtype=np.float64) if want_sim else None
     cb = N.batch_struct_host(batch)

@@ -415,6 +415,40 @@ def test_fused_nw_tail_matches_standalone(monkeypatch):
     assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-2000:]
 
 
+@pytest.mark.parametrize("chunks", ["3", "7"])
+def test_mine_host_chunked_uploads(chunks):
+    """bimine_mine_host with the batch uploaded in chunks (the score kernel
+    waiting per chunk) gives the oracle's scores and matches, including a
+    pair larger than one CTA (tiles) in the middle of the batch."""
+    import subprocess, sys, os
+    code = (
+        "import sys; sys.path[:0]=['.','oracle','tests'];"
+        "import numpy as np, helpers as H, oracle;"
+        "from paper_1512_01641_b200 import synth, engine as E;"
+        "from paper_1512_01641_b200.classifier import model_vector;"
+        "from paper_1512_01641_b200.packing import BatchBuilder, Vocabulary;"
+        "c=synth.make_config(2, n_pairs=40); d=c.dictionary; m=model_vector(H.synth_model());"
+        "big=synth.make_config(1);"
+        "ids=list(range(0,20))+[-1]+list(range(20,40));"
+        "b=c.batch.select(list(range(40)));"
+        "ctx=E.LexiconContext(vocab=None, coo=(d.src,d.tgt,d.prob), devices={});"
+        "cnt,mt,sim=E.mine_host(ctx.on(0), m, b, 2.0, 0.5, -1.0, 1.0, want_sim=True);"
+        "od=oracle.OracleDict(d.src,d.tgt,d.prob);"
+        "ws=oracle.score_batch(od, m, b); wc,wr=oracle.mine_batch(od, m, b);"
+        "assert np.array_equal(sim.view(np.uint64), ws.view(np.uint64));"
+        "assert np.array_equal(cnt,wc); assert np.array_equal(mt.view(np.uint8), np.concatenate(wr).view(np.uint8));"
+        "d1=big.dictionary; ctx1=E.LexiconContext(vocab=None, coo=(d1.src,d1.tgt,d1.prob), devices={});"
+        "bb=big.batch; cnt1,mt1,sim1=E.mine_host(ctx1.on(0), m, bb, 2.0, 0.5, -1.0, 1.0, want_sim=True);"
+        "od1=oracle.OracleDict(d1.src,d1.tgt,d1.prob); wc1,wr1=oracle.mine_batch(od1, m, bb);"
+        "assert np.array_equal(cnt1,wc1); assert np.array_equal(mt1.view(np.uint8), np.concatenate(wr1).view(np.uint8));"
+        "print('ok')"
+    )
+    env = dict(os.environ, BIMINE_E2E_CHUNKS=chunks, BIMINE_E2E_MIN_TOKENS="1")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-3000:]
+
+
 @pytest.mark.parametrize("shape", [(1500, 1700), (2100, 97), (96, 2100)])
 def test_nw_large_problems_band_pipeline(shape):
     """Problems handled by the CTA-per-problem band pipeline (ring buffers
