@@ -303,8 +303,77 @@ def tuning_fixture():
     print("tuning fixture:", result)
 
 
+def cli_fixture():
+    """The reference CLI's `mine` and `tune` (cli.py:129-230) on a small
+    synthetic corpus directory: the bitext bytes, printed lines, exit codes
+    and tuning report a file-level drop-in must reproduce.  The corpus has a
+    topic id with a backslash, a title with a tab (field escaping) and one
+    pair with an untokenizable sentence (failure path, exit status 1)."""
+    import contextlib
+    import io
+    import shutil
+    import tempfile
+
+    from bimine import cli as ref_cli
+    from bimine.corpus import save_corpus
+    from bimine.lexicon import write_lexicon
+
+    out_dir = os.path.join(HERE, "cli")
+    shutil.rmtree(out_dir, ignore_errors=True)
+    os.makedirs(out_dir)
+    d = synth.make_dictionary(np.random.default_rng(777), 1000)
+    corpus = synth.make_corpus(778, 10, 1000, dictionary=d)
+    pairs = []
+    for p in range(10):
+        src, tgt = corpus.pair_sentences(p)
+        topic = f"cli-{p}" if p != 3 else "cli\\3"
+        title = f"title {p}" if p != 5 else "tab\there"
+        if p == 7:
+            tgt = tgt[:4] + ["..."] + tgt[4:]
+        pairs.append(DocumentPair(
+            topic_id=topic,
+            source=Document(id=f"s{p}", lang="pl", title=title, sentences=tuple(src)),
+            target=Document(id=f"t{p}", lang="en", title=title, sentences=tuple(tgt)),
+        ))
+    corpus_dir = os.path.join(out_dir, "corpus")
+    save_corpus(pairs, corpus_dir)
+    lex_path = os.path.join(out_dir, "lexicon.tsv")
+    write_lexicon(Lexicon(d.table()), lex_path)
+    model_path = os.path.join(HERE, "synth_model.json")
+    with open(os.path.join(out_dir, "reference.tsv"), "w", encoding="utf-8") as fh:
+        for p in (0, 1, 2, 4):
+            for i, j in corpus.reference[p]:
+                fh.write(f"{pairs[p].topic_id}\t{i}\t{j}\n")
+
+    def run(argv):
+        so, se = io.StringIO(), io.StringIO()
+        with contextlib.redirect_stdout(so), contextlib.redirect_stderr(se):
+            rc = ref_cli.main(argv)
+        return rc, so.getvalue(), se.getvalue()
+
+    expect = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, extra in (("default", []), ("strict", ["--threshold", "0.8", "--gap-penalty", "1.5"])):
+            out = os.path.join(tmp, f"mined_{name}.tsv")
+            rc, so, se = run(["mine", corpus_dir, model_path, lex_path, out, *extra])
+            shutil.copy(out, os.path.join(out_dir, f"mined_{name}.tsv"))
+            expect[f"mine_{name}"] = {"argv": extra, "rc": rc, "stdout": so, "stderr": se}
+        rep = os.path.join(tmp, "report.json")
+        good = os.path.join(tmp, "good")
+        save_corpus([p for k, p in enumerate(pairs) if k != 7], good)
+        rc, so, se = run(["tune", good, model_path, lex_path, os.path.join(out_dir, "reference.tsv"),
+                          "--budget", "8", "--seed", "3", "--out", rep])
+        with open(rep) as fh:
+            expect["tune"] = {"rc": rc, "stdout": so, "stderr": se, "report": json.load(fh)}
+    with open(os.path.join(out_dir, "expect.json"), "w") as fh:
+        json.dump(expect, fh, indent=1)
+    print("cli fixture:", {k: (v["rc"], v["stdout"].strip()[:80]) for k, v in expect.items()})
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["toy", "synth", "nw", "exp", "tune"]
+    which = sys.argv[1:] or ["toy", "synth", "nw", "exp", "tune", "cli"]
+    if "cli" in which:
+        cli_fixture()
     if "toy" in which:
         toy_fixture()
     if "synth" in which:
