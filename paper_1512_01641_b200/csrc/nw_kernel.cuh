@@ -362,42 +362,27 @@ __device__ __forceinline__ void nw_solve_lean(const double *__restrict__ sim, in
     __syncwarp();
   }
   last = __shfl_sync(kFull, last, (N - 1) & 31);
+  // the walk (lane 0): branch-free position updates; mine mode only records
+  // the Match cells -- their similarities are gathered by the whole warp
+  // afterwards, so no global load sits on the walk's dependency chain
+  int cnt = 0;
   if (lane == 0) {
     int a = N, b = M;
-    int64_t cnt = 0;
-    if (MODE == kNwMine) {
-      while (a > 0 && b > 0) {
-        const uint32_t d = lean_dir(dirs, G8, a, b);
+    while (a > 0 && b > 0) {
+      const uint32_t d = lean_dir(dirs, G8, a, b);
+      if (MODE == kNwMine) {
         if (d == 0u) {
-          const int i = N - a, j = M - b;
-          const double v = sim[(int64_t)i * ld + j];
-          if (v >= threshold) {
-            out[cnt].score = v;
-            out[cnt].i = i;
-            out[cnt].j = j;
-            ++cnt;
-          }
-          --a;
-          --b;
-        } else if (d == 1u) {
-          --a;
-        } else {
-          --b;
+          out[cnt].i = N - a;
+          out[cnt].j = M - b;
+          ++cnt;
         }
-      }
-    } else {
-      while (a > 0 && b > 0) {
-        const uint32_t d = lean_dir(dirs, G8, a, b);
+      } else {
         steps[cnt++] = (uint8_t)d;
-        if (d == 0u) {
-          --a;
-          --b;
-        } else if (d == 1u) {
-          --a;
-        } else {
-          --b;
-        }
       }
+      a -= (d != 2u);
+      b -= (d != 1u);
+    }
+    if (MODE != kNwMine) {
       while (a > 0) {
         steps[cnt++] = 1u;
         --a;
@@ -407,6 +392,35 @@ __device__ __forceinline__ void nw_solve_lean(const double *__restrict__ sim, in
         --b;
       }
     }
+  }
+  cnt = __shfl_sync(kFull, cnt, 0);
+  __syncwarp();
+  if (MODE == kNwMine) {  // keep matches with sim >= threshold, in order (align.py:323-332)
+    int kept = 0;
+    for (int base = 0; base < cnt; base += 32) {
+      const int c = base + lane;
+      double v = 0.0;
+      int32_t i = 0, j = 0;
+      if (c < cnt) {
+        i = out[c].i;
+        j = out[c].j;
+        v = sim[(int64_t)i * ld + j];
+      }
+      const bool keep = c < cnt && v >= threshold;
+      const unsigned bal = __ballot_sync(kFull, keep);
+      __syncwarp();
+      if (keep) {
+        bimine_match &o = out[kept + __popc(bal & ((1u << lane) - 1u))];
+        o.score = v;
+        o.i = i;
+        o.j = j;
+      }
+      kept += __popc(bal);
+      __syncwarp();
+    }
+    cnt = kept;
+  }
+  if (lane == 0) {
     *count_out = (int32_t)cnt;
     if (score_out) *score_out = last;
   }
@@ -1015,23 +1029,17 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
           const int gg = (a - 1) >> 5, ll = (a - 1) & 31, ss = b + ll - 1, kk = ss >> 3;
           if (gg != win_g || kk < win_k0 || kk >= win_k0 + 16) break;
           const uint32_t d = ((uint32_t)win[(kk - win_k0) * 32 + ll] >> (2 * (ss & 7))) & 3u;
-          if (d == 0u) {
-            if (MODE == kNwMine) {
+          if (MODE == kNwMine) {
+            if (d == 0u) {
               outm[cnt].i = N - a;  // score filled below
               outm[cnt].j = M - b;
               ++cnt;
-            } else {
-              st[cnt++] = 0u;
             }
-            --a;
-            --b;
-          } else if (d == 1u) {
-            if (MODE == kNwSteps) st[cnt++] = 1u;
-            --a;
           } else {
-            if (MODE == kNwSteps) st[cnt++] = 2u;
-            --b;
+            st[cnt++] = (uint8_t)d;
           }
+          a -= (d != 2u);
+          b -= (d != 1u);
         }
       }
       __syncwarp();
