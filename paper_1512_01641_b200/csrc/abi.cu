@@ -512,78 +512,87 @@ int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     if (nprob * kc > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "nw: too many large problems");
     cfg.gridDim = dim3((unsigned)(nprob * kc), 1, 1);
-    // diagonal layout of every distinct pair among the problems
-    std::vector<int64_t> ids(nprob);
-    if (A.problem_ids) {
-      BIMINE_CUDA(cudaMemcpyAsync(ids.data(), A.problem_ids, sizeof(int64_t) * nprob, cudaMemcpyDeviceToHost, st));
-      BIMINE_CUDA(cudaStreamSynchronize(st));
-    } else {
-      for (int64_t k = 0; k < nprob; ++k) ids[k] = k;
-    }
-    std::vector<int64_t> dpairs, dslot(nprob), doff;
-    {
-      std::unordered_map<int64_t, int64_t> seen;
-      for (int64_t k = 0; k < nprob; ++k) {
-        const int64_t pr = ids[k] / A.n_settings;
-        auto it = seen.find(pr);
-        if (it == seen.end()) it = seen.emplace(pr, (int64_t)dpairs.size()).first, dpairs.push_back(pr);
-        dslot[k] = it->second;
-      }
-    }
-    std::vector<int32_t> pn(dpairs.size()), pm(dpairs.size());
-    for (size_t k = 0; k < dpairs.size(); ++k) {
-      BIMINE_CUDA(cudaMemcpyAsync(&pn[k], A.pair_n + dpairs[k], sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-      BIMINE_CUDA(cudaMemcpyAsync(&pm[k], A.pair_m + dpairs[k], sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    }
-    BIMINE_CUDA(cudaStreamSynchronize(st));
-    int64_t dtotal = 0;
-    int gmax_d = 1;
-    std::vector<int64_t> pair_doff(dpairs.size());
-    for (size_t k = 0; k < dpairs.size(); ++k) {
-      pair_doff[k] = dtotal;
-      const int g = (pn[k] + 31) / 32;
-      gmax_d = std::max(gmax_d, g);
-      dtotal += (int64_t)g * nw_diag_steps(pm[k]) * 32;
-    }
-    doff.resize(nprob);
-    for (int64_t k = 0; k < nprob; ++k) doff[k] = pair_doff[dslot[k]];
-    if (gmax_d > 65535 || (int64_t)dpairs.size() > 65535) return fail(BIMINE_E_LIMIT, "nw: large problem too tall");
+    // diagonal layout of every distinct pair among the problems: without a
+    // problem list (problems = pairs x settings, in order) at a uniform
+    // per-pair stride and without any host round trip; with one, the
+    // distinct pairs are gathered on the host
+    const int64_t dstride_u = (int64_t)gmax * nw_diag_steps(max_m) * 32;
+    const int64_t npairs_u = nprob / A.n_settings;
+    const bool uniform = !A.problem_ids && npairs_u * dstride_u <= ((int64_t)1 << 29);  // <= 4 GiB
     double *diag = nullptr;
     int64_t *d_pairs = nullptr, *d_pair_doff = nullptr, *d_doff = nullptr;
-    BIMINE_CUDA(cudaMallocAsync((void **)&diag, sizeof(double) * std::max<int64_t>(dtotal, 1), st));
-    BIMINE_CUDA(cudaMallocAsync((void **)&d_pairs, sizeof(int64_t) * dpairs.size(), st));
-    BIMINE_CUDA(cudaMallocAsync((void **)&d_pair_doff, sizeof(int64_t) * dpairs.size(), st));
-    BIMINE_CUDA(cudaMallocAsync((void **)&d_doff, sizeof(int64_t) * nprob, st));
-    BIMINE_CUDA(cudaMemcpyAsync(d_pairs, dpairs.data(), sizeof(int64_t) * dpairs.size(), cudaMemcpyHostToDevice, st));
-    BIMINE_CUDA(cudaMemcpyAsync(d_pair_doff, pair_doff.data(), sizeof(int64_t) * dpairs.size(), cudaMemcpyHostToDevice, st));
-    BIMINE_CUDA(cudaMemcpyAsync(d_doff, doff.data(), sizeof(int64_t) * nprob, cudaMemcpyHostToDevice, st));
-    {
+    int64_t diag_stride = 0;
+    if (uniform) {
+      if (npairs_u > 65535 || gmax > 65535) return fail(BIMINE_E_LIMIT, "nw: large problem too tall");
+      BIMINE_CUDA(cudaMallocAsync((void **)&diag, sizeof(double) * std::max<int64_t>(npairs_u * dstride_u, 1), st));
+      diag_stride = dstride_u;
+      const int64_t per_band = nw_diag_steps(max_m) * 32;
+      const dim3 grid((unsigned)std::min<int64_t>((per_band + 255) / 256, 64), (unsigned)gmax, (unsigned)npairs_u);
+      nw_diag_kernel<<<grid, 256, 0, st>>>(A.sim, A.sim_off, A.pair_n, A.pair_m, nullptr, nullptr, dstride_u,
+                                           A.mismatch, A.bonus - A.mismatch, diag);  // one IEEE subtraction, as fsub
+      BIMINE_CUDA(cudaGetLastError());
+    } else {
+      std::vector<int64_t> ids(nprob);
+      if (A.problem_ids) {
+        BIMINE_CUDA(cudaMemcpyAsync(ids.data(), A.problem_ids, sizeof(int64_t) * nprob, cudaMemcpyDeviceToHost, st));
+        BIMINE_CUDA(cudaStreamSynchronize(st));
+      } else {
+        for (int64_t k = 0; k < nprob; ++k) ids[k] = k;
+      }
+      std::vector<int64_t> dpairs, dslot(nprob);
+      {
+        std::unordered_map<int64_t, int64_t> seen;
+        for (int64_t k = 0; k < nprob; ++k) {
+          const int64_t pr = ids[k] / A.n_settings;
+          auto it = seen.find(pr);
+          if (it == seen.end()) it = seen.emplace(pr, (int64_t)dpairs.size()).first, dpairs.push_back(pr);
+          dslot[k] = it->second;
+        }
+      }
+      std::vector<int32_t> pn(dpairs.size()), pm(dpairs.size());
+      for (size_t k = 0; k < dpairs.size(); ++k) {
+        BIMINE_CUDA(cudaMemcpyAsync(&pn[k], A.pair_n + dpairs[k], sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        BIMINE_CUDA(cudaMemcpyAsync(&pm[k], A.pair_m + dpairs[k], sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      }
+      BIMINE_CUDA(cudaStreamSynchronize(st));
+      int64_t dtotal = 0;
+      int gmax_d = 1;
+      std::vector<int64_t> pair_doff(dpairs.size()), doff(nprob);
+      for (size_t k = 0; k < dpairs.size(); ++k) {
+        pair_doff[k] = dtotal;
+        const int g = (pn[k] + 31) / 32;
+        gmax_d = std::max(gmax_d, g);
+        dtotal += (int64_t)g * nw_diag_steps(pm[k]) * 32;
+      }
+      for (int64_t k = 0; k < nprob; ++k) doff[k] = pair_doff[dslot[k]];
+      if (gmax_d > 65535 || (int64_t)dpairs.size() > 65535) return fail(BIMINE_E_LIMIT, "nw: large problem too tall");
+      BIMINE_CUDA(cudaMallocAsync((void **)&diag, sizeof(double) * std::max<int64_t>(dtotal, 1), st));
+      BIMINE_CUDA(cudaMallocAsync((void **)&d_pairs, sizeof(int64_t) * dpairs.size(), st));
+      BIMINE_CUDA(cudaMallocAsync((void **)&d_pair_doff, sizeof(int64_t) * dpairs.size(), st));
+      BIMINE_CUDA(cudaMallocAsync((void **)&d_doff, sizeof(int64_t) * nprob, st));
+      BIMINE_CUDA(cudaMemcpyAsync(d_pairs, dpairs.data(), sizeof(int64_t) * dpairs.size(), cudaMemcpyHostToDevice, st));
+      BIMINE_CUDA(cudaMemcpyAsync(d_pair_doff, pair_doff.data(), sizeof(int64_t) * dpairs.size(), cudaMemcpyHostToDevice, st));
+      BIMINE_CUDA(cudaMemcpyAsync(d_doff, doff.data(), sizeof(int64_t) * nprob, cudaMemcpyHostToDevice, st));
       const int mmax = *std::max_element(pm.begin(), pm.end());
       const int64_t per_band = nw_diag_steps(mmax) * 32;
       const dim3 grid((unsigned)std::min<int64_t>((per_band + 255) / 256, 64), (unsigned)gmax_d, (unsigned)dpairs.size());
-      nw_diag_kernel<<<grid, 256, 0, st>>>(A.sim, A.sim_off, A.pair_n, A.pair_m, d_pairs, d_pair_doff, A.mismatch,
-                                           A.bonus - A.mismatch, diag);  // one IEEE subtraction, as fsub on the device
+      nw_diag_kernel<<<grid, 256, 0, st>>>(A.sim, A.sim_off, A.pair_n, A.pair_m, d_pairs, d_pair_doff, 0, A.mismatch,
+                                           A.bonus - A.mismatch, diag);  // one IEEE subtraction, as fsub
       BIMINE_CUDA(cudaGetLastError());
     }
     uint32_t *dirs = nullptr;
-    int64_t *offs = nullptr;
     double *lastv = nullptr;
     BIMINE_CUDA(cudaMallocAsync((void **)&dirs, sizeof(uint32_t) * stride * nprob, st));
-    BIMINE_CUDA(cudaMallocAsync((void **)&offs, sizeof(int64_t) * nprob, st));
     BIMINE_CUDA(cudaMallocAsync((void **)&lastv, sizeof(double) * nprob, st));
-    std::vector<int64_t> h(nprob);
-    for (int64_t k = 0; k < nprob; ++k) h[k] = k * stride;
-    BIMINE_CUDA(cudaMemcpyAsync(offs, h.data(), sizeof(int64_t) * nprob, cudaMemcpyHostToDevice, st));
     // wrap-around rows: [2][max_m + 1] tagged slots per problem, tags -1
     const int64_t rows_stride = 2 * ((int64_t)max_m + 1);
     double2 *rows = nullptr;
     BIMINE_CUDA(cudaMallocAsync((void **)&rows, sizeof(double2) * rows_stride * nprob, st));
     BIMINE_CUDA(cudaMemsetAsync(rows, 0xff, sizeof(double2) * rows_stride * nprob, st));
-    BIMINE_CUDA(cudaLaunchKernelEx(&cfg, kern, A, dirs, (const int64_t *)offs, rows, rows_stride, lastv, (const double *)diag,
-                                   (const int64_t *)d_doff));
+    BIMINE_CUDA(cudaLaunchKernelEx(&cfg, kern, A, dirs, stride, rows, rows_stride, lastv, (const double *)diag,
+                                   (const int64_t *)d_doff, diag_stride));
     const cudaError_t e = cudaGetLastError();
     cudaFreeAsync(dirs, st);
-    cudaFreeAsync(offs, st);
     cudaFreeAsync(rows, st);
     cudaFreeAsync(lastv, st);
     cudaFreeAsync(diag, st);

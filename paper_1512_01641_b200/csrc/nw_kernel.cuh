@@ -825,16 +825,16 @@ __global__ void __launch_bounds__(256) nw_diag_kernel(const double *__restrict__
                                                        const int32_t *__restrict__ pair_n,
                                                        const int32_t *__restrict__ pair_m,
                                                        const int64_t *__restrict__ pairs,
-                                                       const int64_t *__restrict__ diag_off, double mismatch,
-                                                       double span, double *__restrict__ diag_all) {
+                                                       const int64_t *__restrict__ diag_off, int64_t diag_stride,
+                                                       double mismatch, double span, double *__restrict__ diag_all) {
   const int64_t ps = blockIdx.z;
   const int g = blockIdx.y;
-  const int64_t pair = pairs[ps];
+  const int64_t pair = pairs ? pairs[ps] : ps;  // null: pairs 0, 1, ... at a uniform stride
   const int N = pair_n[pair], M = pair_m[pair];
   if (32 * g >= N) return;
   const double *__restrict__ sim = sim_all + sim_off[pair];
   const int64_t S = nw_diag_steps(M);
-  double *__restrict__ out = diag_all + diag_off[ps] + (int64_t)g * S * 32;
+  double *__restrict__ out = diag_all + (diag_off ? diag_off[ps] : ps * diag_stride) + (int64_t)g * S * 32;
   for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < S * 32; x += (int64_t)gridDim.x * blockDim.x) {
     const int l = (int)(x & 31);
     const int64_t st = x >> 5;
@@ -904,9 +904,10 @@ struct BotRemote {  // lane 31 writes ring 0 of the next CTA of the cluster
 };
 
 template <int MODE, int W>
-__global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t *g_dirs_all, const int64_t *dir_off,
+__global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t *g_dirs_all, int64_t dir_stride,
                                                         double2 *g_rows, int64_t rows_stride, double *last_val,
-                                                        const double *diag_all, const int64_t *diag_off) {
+                                                        const double *diag_all, const int64_t *diag_off,
+                                                        int64_t diag_stride) {
   extern __shared__ __align__(16) unsigned char big_smem[];
   BigRing *rings = (BigRing *)big_smem;  // [W], ring w feeds warp w
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -920,11 +921,12 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
   const double gap = A.gap_per_problem ? A.gap[q] : A.gap[setting];
   const double ng = -gap, mismatch = A.mismatch, span = fsub(A.bonus, A.mismatch);
   const int G = (N + 31) >> 5, G8 = nw_groups(M);
-  uint16_t *dirs = (uint16_t *)(g_dirs_all + dir_off[slot]);  // [G][G8][32]
+  uint16_t *dirs = (uint16_t *)(g_dirs_all + slot * dir_stride);  // [G][G8][32]
   double2 *wrap = g_rows + slot * rows_stride;                // [2][M+1] tagged, pre-filled with tag -1
   const long long W1 = (long long)M + 1;
   const int per_round = W * K;
-  const double *__restrict__ diag = diag_all + diag_off[slot];  // [G][nw_diag_steps(M)][32]
+  // [G][nw_diag_steps(M)][32], per pair: listed offsets, or a uniform stride per pair index
+  const double *__restrict__ diag = diag_all + (diag_off ? diag_off[slot] : pair * diag_stride);
   const int64_t dstride = nw_diag_steps(M) * 32;
   for (int k = threadIdx.x; k < W * kRing; k += blockDim.x)
     rings[k / kRing].slot[k % kRing] = make_double2(0.0, __longlong_as_double(-1ll));
