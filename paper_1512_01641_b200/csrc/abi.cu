@@ -485,6 +485,10 @@ int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
     if (nprob > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "nw: too many large problems");
     const int gmax = (max_n + 31) / 32;
     int kc = std::max(1, std::min(16, (gmax + kBigW - 1) / kBigW));  // CTAs per cluster (= per problem)
+    static const int skip_tb = [] {
+      const char *v = getenv("BIMINE_NW_SKIP_TRACEBACK");
+      return v && v[0] == '1';
+    }();
     constexpr size_t smem = big_smem_bytes<kBigW>();
     auto kern = nw_big_kernel<MODE, kBigW>;
     BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -591,6 +595,8 @@ int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
     BIMINE_CUDA(cudaMemsetAsync(rows, 0xff, sizeof(double2) * rows_stride * nprob, st));
     BIMINE_CUDA(cudaLaunchKernelEx(&cfg, kern, A, dirs, stride, rows, rows_stride, lastv, (const double *)diag,
                                    (const int64_t *)d_doff, diag_stride));
+    if (MODE != kNwTable && !skip_tb)
+      nw_big_traceback_kernel<MODE><<<(unsigned)nprob, 32, 0, st>>>(A, dirs, stride, lastv);
     const cudaError_t e = cudaGetLastError();
     cudaFreeAsync(dirs, st);
     cudaFreeAsync(rows, st);

@@ -928,12 +928,19 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
   // [G][nw_diag_steps(M)][32], per pair: listed offsets, or a uniform stride per pair index
   const double *__restrict__ diag = diag_all + (diag_off ? diag_off[slot] : pair * diag_stride);
   const int64_t dstride = nw_diag_steps(M) * 32;
+#if defined(BIMINE_NW_PROFILE) || defined(BIMINE_PROF_ENTRY)
+  if (threadIdx.x == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    printf("prof entry cta %d ns %llu\n", crank, gt);
+  }
+#endif
   for (int k = threadIdx.x; k < W * kRing; k += blockDim.x)
     rings[k / kRing].slot[k % kRing] = make_double2(0.0, __longlong_as_double(-1ll));
   if (threadIdx.x < W) rings[threadIdx.x].cons = 0;
   __syncthreads();
   cluster_barrier();  // every ring initialised before any remote write
-#ifdef BIMINE_NW_PROFILE
+#if defined(BIMINE_NW_PROFILE) || defined(BIMINE_PROF_START)
   if (threadIdx.x == 0) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
@@ -980,7 +987,14 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
     }
     if (32 * g + 1 + lane == N) last_val[slot] = fin;
     __syncwarp();
-#ifdef BIMINE_NW_PROFILE
+    // Diagnostic for a launch without the operand layout (never true for
+    // the launcher in abi.cu).  Measured side effect, kept on purpose: with
+    // a call site in this loop ptxas schedules the band pipeline's ring
+    // loops so that the 4096x4096 sweep takes 2.12 ms instead of 3.58 ms
+    // (an unreachable printf reproduces it; a memory clobber or fence does
+    // not) -- see DESIGN.md 4.3.
+    if (diag_all == nullptr) printf("bimine: nw_big_kernel band %d without its operand layout\n", g);
+#if defined(BIMINE_NW_PROFILE) || defined(BIMINE_PROF_BAND)
     if (lane == 0) {
       unsigned long long gt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
@@ -988,11 +1002,29 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
     }
 #endif
   }
-  // all bands of the problem are done (and no remote access is pending)
-  __syncthreads();
-  cluster_barrier();
-  if (crank != 0) return;
-  const double s_last = __ldcg(&last_val[slot]);
+  // The kernel ends with the sweep: the traceback is a separate launch
+  // (nw_big_traceback_kernel) that reads every CTA's directions after the
+  // kernel boundary.  No cluster barrier is needed here either: a CTA's
+  // shared memory is last touched remotely by the previous CTA's final ring
+  // writes, which its warp 0 has consumed before finishing, and the previous
+  // CTA's last remote `cons` poll precedes those writes.
+}
+
+// Traceback + threshold filter of large problems (one warp per problem),
+// over the 2-bit directions the band pipeline wrote.
+template <int MODE>
+__global__ void __launch_bounds__(32) nw_big_traceback_kernel(const NwArgs A, const uint32_t *g_dirs_all,
+                                                                int64_t dir_stride, const double *last_val) {
+  const int64_t slot = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = 0;
+  const int64_t q = A.problem_ids ? A.problem_ids[slot] : slot;
+  const int64_t pair = q / A.n_settings;
+  const int setting = (int)(q % A.n_settings);
+  const int N = A.pair_n[pair], M = A.pair_m[pair];
+  const double *__restrict__ sim = A.sim + A.sim_off[pair];
+  const int G8 = nw_groups(M);
+  const uint16_t *dirs = (const uint16_t *)(g_dirs_all + slot * dir_stride);  // [G][G8][32]
+  const double s_last = last_val[slot];
   if (MODE == kNwTable) return;
   // ---- traceback on warp 0: lane 0 walks, the warp stages 16 direction
   // groups (128 steps) of the current band at a time
@@ -1027,10 +1059,14 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
         __syncwarp();
       }
       if (lane == 0) {
+        // window bounds and base in registers: nothing but the direction
+        // load itself on the walk's dependency chain
+        const int wg = win_g, wk0 = win_k0;
+        const uint16_t *wb = win;
         while (a > 0 && b > 0) {
           const int gg = (a - 1) >> 5, ll = (a - 1) & 31, ss = b + ll - 1, kk = ss >> 3;
-          if (gg != win_g || kk < win_k0 || kk >= win_k0 + 16) break;
-          const uint32_t d = ((uint32_t)win[(kk - win_k0) * 32 + ll] >> (2 * (ss & 7))) & 3u;
+          if (gg != wg || kk < wk0 || kk >= wk0 + 16) break;
+          const uint32_t d = ((uint32_t)wb[(kk - wk0) * 32 + ll] >> (2 * (ss & 7))) & 3u;
           if (MODE == kNwMine) {
             if (d == 0u) {
               outm[cnt].i = N - a;  // score filled below
@@ -1087,7 +1123,7 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
       if (lane == 0) A.counts[q] = (int32_t)kept;
     }
     if (lane == 0 && A.score) A.score[q] = s_last;
-#ifdef BIMINE_NW_PROFILE
+#if defined(BIMINE_NW_PROFILE) || defined(BIMINE_PROF_TB)
     if (lane == 0) {
       unsigned long long gt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));

@@ -2,8 +2,11 @@
 import re
 import sys
 
-start, bands, tb = {}, {}, None
+start, bands, tb, entry = {}, {}, None, {}
 for line in sys.stdin:
+    m = re.match(r"prof entry cta (\d+) ns (\d+)", line)
+    if m:
+        entry[int(m[1])] = int(m[2])
     m = re.match(r"prof start cta (\d+) ns (\d+)", line)
     if m:
         start[int(m[1])] = int(m[2])
@@ -14,6 +17,9 @@ for line in sys.stdin:
     if m:
         tb = int(m[1])
 t0 = min(start.values())
+if entry:
+    e0 = min(entry.values())
+    print("cta entries (us before first start):", round((t0 - e0) / 1e3, 1), " spread", round((max(entry.values()) - e0) / 1e3, 1))
 print("cta starts (us):", sorted(round((v - t0) / 1e3, 1) for v in start.values())[:8], "...", round((max(start.values()) - t0) / 1e3, 1))
 ks = sorted(bands)
 for g in ks[:10] + ks[-3:]:
