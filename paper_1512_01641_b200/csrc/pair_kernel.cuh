@@ -85,6 +85,7 @@ struct PairSmem {
   int32_t *src_len, *src_uniq, *src_chars;  // [64]
   int32_t *tgt_len, *tgt_uniq, *tgt_chars;  // [64]
   int32_t *tgt_occ0;   // [65] chunk-local occurrence offsets
+  uint8_t *src_order;  // [64] source sentences, longest first (phase D claim order)
   int32_t *o_n;        // [warps][32] translations found per occurrence
   int32_t *misc;       // [8]: 0 distinct count, 1 chunk end, 2 D work counter, 3 C work counter
   int16_t *dense;      // [slots]
@@ -134,6 +135,7 @@ __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_
   t.tgt_chars = (int32_t *)take(64 * 4, 4);
   t.tgt_occ0 = (int32_t *)take(65 * 4, 4);
   t.misc = (int32_t *)take(8 * 4, 4);
+  t.src_order = (uint8_t *)take(64, 4);
   t.covt = (uint8_t *)take(64 * 64, 4);
   if (s) *s = t;
   return (o + 15) / 16 * 16;
@@ -266,6 +268,16 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
     const int l = tid < N ? S.src_len[tid] : (tid >= 64 && tid - 64 < M) ? S.tgt_len[tid - 64] : 0;
     if (__syncthreads_or(l > kPairMaxLen)) return;
   }
+  if (tid < N) {  // phase D claims source sentences longest first (shorter tail at its barrier)
+    const int li = S.src_len[tid];
+    int rank = 0;
+    for (int k = 0; k < N; ++k) {
+      const int lk = S.src_len[k];
+      rank += (lk > li) || (lk == li && k < tid);
+    }
+    S.src_order[rank] = (uint8_t)tid;
+  }
+  __syncthreads();
 
   for (int jc0 = 0; jc0 < M;) {
     // ---- chunk [jc0, jc1): at most cap_t target occurrences
@@ -370,7 +382,10 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
       // sentence is claimed one sentence ahead
       auto claim = [&]() -> int {
         int v = 0;
-        if (lane == 0) v = atomicAdd(&S.misc[2], 1);
+        if (lane == 0) {
+          v = atomicAdd(&S.misc[2], 1);
+          v = v < N ? (int)S.src_order[v] : N;
+        }
         return __shfl_sync(kFull, v, 0);
       };
       auto load_tok = [&](int si, int pos) -> int32_t {
