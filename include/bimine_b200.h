@@ -274,6 +274,24 @@ int bimine_tokenize_batch(bimine_vocab *vocab, const char *buf,
                           int64_t cap, int64_t *n_tokens, int32_t *len_out,
                           int32_t *uniq_out, int32_t *chars_out);
 
+/* ---- lexicon EM -----------------------------
+ * Replaces the EM loop of build_lexicon (lexicon.py:60-120): `iterations`
+ * rounds over device arrays, bit-identical to the reference's float64
+ * sums (see csrc/lexicon_em.cuh).  Inputs, all device pointers:
+ *   tgt_off[n_pairs + 1], tgt_tok[..]: target-side token ids per pair;
+ *   row_ptr[n_src + 1], row_tgt[E]: the support of every source id (all
+ *     co-occurring target ids, sorted per row);
+ *   prob[E]: in/out, initially 1 / row length (lexicon.py:92-94);
+ *   alive[E]: in/out, 1 initially; 0 once an entry left its row;
+ *   occ_ptr[n_src + 1], occ_pair[..]: the pair of every occurrence of each
+ *     source id, in corpus order (pairs with an empty side removed).
+ * Returns BIMINE_E_ARG if a round looked up a target its row no longer
+ * holds (the reference raises KeyError there). */
+int bimine_lexicon_em(const int32_t *tgt_off, const int32_t *tgt_tok, int64_t n_pairs, int32_t n_src,
+                      const int64_t *row_ptr, const int32_t *row_tgt, int64_t n_entries, double *prob,
+                      uint8_t *alive, const int64_t *occ_ptr, const int32_t *occ_pair, int32_t iterations,
+                      void *stream);
+
 /* ---- test hook -------------------------------------------------------
  * Device evaluation of the score_from_margin logistic's exp
  * (classifier.py:145-147, glibc __exp_fma restated) over n host doubles;

@@ -11,9 +11,11 @@ from __future__ import annotations
 
 import ctypes
 import glob
+import math
 import importlib.util
 import os
 import subprocess
+import sys
 
 import numpy as np
 
@@ -197,3 +199,75 @@ def reference_nwcore():
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
     return mod
+
+
+# ---------------------------------------------------------------------------
+# f4: lexicon EM, restated in plain Python (lexicon.py:60-120).  Test
+# infrastructure only: the product runs the rounds on the GPU.
+# ---------------------------------------------------------------------------
+
+def py_sum(values):
+    """CPython >= 3.12 built-in sum() over floats (Python/bltinmodule.c):
+    0 + x0, then Neumaier's compensated steps, the compensation added at the
+    end when it is nonzero and finite -- what `sum(row_counts.values())`
+    computes in lexicon.py:112."""
+    it = iter(values)
+    try:
+        f = 0 + next(it)
+    except StopIteration:
+        return 0
+    c = 0.0
+    for x in it:
+        t = f + x
+        if abs(f) >= abs(x):
+            c = c + ((f - t) + x)
+        else:
+            c = c + ((x - t) + f)
+        f = t
+    if c and math.isfinite(c):
+        f = f + c
+    return f
+
+
+def build_lexicon(parallel, iterations, prune_threshold=1e-4, tokenize=None):
+    """dict[s][t] -> p with the reference's float64 operation order: per
+    round, for every pair in order and every source occurrence in order,
+    denom = sequential sum over the target positions; counts[s][t] += p/denom
+    per position; rows renormalised by Python's sum() (compensated, see
+    py_sum) of their counts in first-count order."""
+    if tokenize is None:
+        sys.path.insert(0, os.path.dirname(HERE))
+        from paper_1512_01641_b200.text import tokenize
+    if not parallel:
+        raise ValueError("no training pairs")
+    if iterations < 1:
+        raise ValueError("iterations must be >= 1")
+    data = [(a, b) for a, b in ((tokenize(x), tokenize(y)) for x, y in parallel) if a and b]
+    if not data:
+        raise ValueError("no training pairs")
+    support = {}
+    for src, tgt in data:
+        for s in src:
+            support.setdefault(s, set()).update(tgt)
+    prob = {s: dict.fromkeys(ts, 1.0 / len(ts)) for s, ts in support.items()}
+    for _ in range(iterations):
+        counts = {s: {} for s in prob}
+        for src, tgt in data:
+            for s in src:
+                row = prob[s]
+                denom = 0.0
+                for t in tgt:
+                    denom = denom + row[t]
+                if not denom > 0.0:
+                    continue
+                acc = counts[s]
+                for t in tgt:
+                    acc[t] = acc.get(t, 0.0) + row[t] / denom
+        for s, acc in counts.items():
+            total = py_sum(acc.values())  # first-count (insertion) order
+            if total > 0.0:
+                prob[s] = {t: v / total for t, v in acc.items()}
+    if prune_threshold > 0.0:
+        kept = {s: {t: p for t, p in row.items() if p >= prune_threshold} for s, row in prob.items()}
+        prob = {s: row for s, row in kept.items() if row}
+    return prob

@@ -113,6 +113,9 @@ SIGNATURES = {
                                         ctypes.c_double, ctypes.c_double, _i32p, _vp, ctypes.c_int64, _i64p,
                                         _vp, _vp]),
     "bimine_exp_device": (ctypes.c_int, [_f64p, _f64p, ctypes.c_int64]),
+    # device pointers (torch tensors' data_ptr)
+    "bimine_lexicon_em": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp, ctypes.c_int64, _vp,
+                                         _vp, _vp, _vp, ctypes.c_int32, _vp]),
     "bimine_vocab_create": (ctypes.c_int, [ctypes.POINTER(_vp)]),
     "bimine_vocab_destroy": (ctypes.c_int, [_vp]),
     "bimine_vocab_size": (ctypes.c_int64, [_vp]),

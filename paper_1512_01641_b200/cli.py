@@ -1,10 +1,11 @@
-"""``bimine mine`` / ``bimine tune`` on the GPU path.
+"""``bimine mine`` / ``tune`` / ``dict`` on the GPU path.
 
 Same positional arguments, options, defaults, outputs and exit codes as
 the reference CLI for these two commands (cli.py:36-53, 157-230, 336-425):
 
     python -m paper_1512_01641_b200 mine CORPUS_DIR MODEL LEXICON OUT [--threshold ...]
     python -m paper_1512_01641_b200 tune CORPUS_DIR MODEL LEXICON REFERENCE [--budget ...]
+    python -m paper_1512_01641_b200 dict PARALLEL OUT [--titles LINKS] [--iterations N]
 
 ``mine`` writes the bitext (``%.4f\\tsrc\\ttgt`` per mined pair, input
 order) and ``OUT.manifest.json``, prints ``N sentence pairs mined from K
@@ -26,8 +27,8 @@ import time
 from . import __version__
 from .align import MiningConfig, mine_corpus
 from .classifier import load_model
-from .corpus import load_corpus, write_bitext
-from .lexicon import read_lexicon
+from .corpus import load_corpus, read_links, read_parallel, write_bitext
+from .lexicon import build_lexicon, merge_title_lexicon, read_lexicon, write_lexicon
 from .manifest import RunManifest, file_digest, write_manifest
 
 _ENGINES = {"nw": "nw", "nw-wavefront": "nw_wavefront"}
@@ -124,6 +125,23 @@ def cmd_tune(args: argparse.Namespace) -> int:
     return 0
 
 
+def cmd_dict(args: argparse.Namespace) -> int:
+    """cli.py:95-108: EM lexicon from sentence pairs (GPU rounds), optional
+    title merge, sorted TSV + manifest."""
+    started = time.perf_counter()
+    lexicon = build_lexicon(read_parallel(args.parallel_file), args.iterations)
+    inputs = [args.parallel_file]
+    if args.titles:
+        titles = read_links(args.titles)
+        lexicon, skipped = merge_title_lexicon(lexicon, titles)
+        inputs.append(args.titles)
+        print(f"merged {len(titles) - skipped} title pairs, skipped {skipped}")
+    write_lexicon(lexicon, args.out_file)
+    write_manifest(args.out_file + ".manifest.json", _manifest(args, inputs, started))
+    print(f"{len(lexicon)} lexicon entries written to {args.out_file}")
+    return 0
+
+
 def build_parser() -> argparse.ArgumentParser:
     common = argparse.ArgumentParser(add_help=False)
     common.add_argument("--seed", type=int, default=42)
@@ -132,6 +150,12 @@ def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="bimine", description="Mine translation-equivalent sentence pairs (GPU path).")
     parser.add_argument("--version", action="version", version=f"%(prog)s {__version__}")
     sub = parser.add_subparsers(dest="command", required=True)
+    p = sub.add_parser("dict", parents=[common], help="build the translation lexicon")
+    p.add_argument("parallel_file")
+    p.add_argument("out_file")
+    p.add_argument("--titles")
+    p.add_argument("--iterations", type=int, default=10)
+    p.set_defaults(func=cmd_dict)
     p = sub.add_parser("mine", parents=[common], help="mine parallel sentences")
     for name in ("corpus_dir", "model_file", "lexicon_file", "out_file"):
         p.add_argument(name)
@@ -150,6 +174,8 @@ def build_parser() -> argparse.ArgumentParser:
 def main(argv: list[str] | None = None) -> int:
     parser = build_parser()
     args = parser.parse_args(argv)
+    if args.command == "dict" and args.iterations < 1:
+        parser.error("--iterations must be >= 1")
     if args.command == "tune" and args.budget < 1:
         parser.error("--budget must be >= 1")
     if args.workers < 1:

@@ -137,3 +137,28 @@ def load_corpus(corpus_dir: str | os.PathLike) -> list[DocumentPair]:
         tgt = Document(id=f[4], lang=f[5], title=unescape_field(f[6]), sentences=sentences_of(topic, "tgt"))
         out.append(DocumentPair(topic_id=topic, source=src, target=tgt))
     return out
+
+
+# ---- two-column files: training pairs, title / document links (corpus.py:170-200)
+def _two_fields(path) -> list[tuple[str, str]]:
+    out = []
+    with open(path, encoding="utf-8") as fh:
+        for lineno, raw in enumerate(fh, 1):
+            line = raw.rstrip("\n")
+            if not line:
+                continue
+            fields = line.split("\t")
+            if len(fields) != 2:
+                raise ValueError(f"{path}: line {lineno}: expected 2 tab-separated fields, got {len(fields)}")
+            out.append((fields[0], fields[1]))
+    return out
+
+
+def read_parallel(path: str | os.PathLike) -> list[tuple[str, str]]:
+    """``source<TAB>target`` sentence pairs (lexicon / classifier training)."""
+    return _two_fields(path)
+
+
+def read_links(path: str | os.PathLike) -> list[tuple[str, str]]:
+    """Two tab-separated columns per line (document links, title pairs)."""
+    return _two_fields(path)

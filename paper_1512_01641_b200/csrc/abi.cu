@@ -23,6 +23,7 @@
 
 #include "../../include/bimine_b200.h"
 #include "common.cuh"
+#include "lexicon_em.cuh"
 #include "nw_kernel.cuh"
 #include "pair_kernel.cuh"
 #include "score_kernel.cuh"
@@ -1137,6 +1138,49 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
 __global__ void exp_kernel(const double *x, double *y, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = glibc_exp(x[i], kExpTableDev);
+}
+
+int bimine_lexicon_em(const int32_t *tgt_off, const int32_t *tgt_tok, int64_t n_pairs, int32_t n_src,
+                      const int64_t *row_ptr, const int32_t *row_tgt, int64_t n_entries, double *prob,
+                      uint8_t *alive, const int64_t *occ_ptr, const int32_t *occ_pair, int32_t iterations,
+                      void *stream) {
+  if (iterations < 1) return fail(BIMINE_E_ARG, "iterations must be >= 1");
+  if (n_src <= 0 || n_entries <= 0 || n_pairs <= 0) return BIMINE_OK;
+  if (!tgt_off || !tgt_tok || !row_ptr || !row_tgt || !prob || !alive || !occ_ptr || !occ_pair)
+    return fail(BIMINE_E_ARG, "bimine_lexicon_em: null argument");
+  pool_setup();
+  cudaStream_t st = as_stream(stream);
+  EmArgs A;
+  A.tgt_off = tgt_off;
+  A.tgt_tok = tgt_tok;
+  A.n_src = n_src;
+  A.row_ptr = row_ptr;
+  A.row_tgt = row_tgt;
+  A.prob = prob;
+  A.alive = alive;
+  A.occ_ptr = occ_ptr;
+  A.occ_pair = occ_pair;
+  char *scratch = nullptr;
+  const size_t b_cnt = sizeof(double) * n_entries, b_first = sizeof(int32_t) * n_entries;
+  BIMINE_CUDA(cudaMallocAsync((void **)&scratch, b_cnt + 2 * b_first + 16, st));
+  A.cnt = (double *)scratch;
+  A.first = (int32_t *)(scratch + b_cnt);
+  A.order = (int32_t *)(scratch + b_cnt + b_first);
+  A.status = (int32_t *)(scratch + b_cnt + 2 * b_first);
+  BIMINE_CUDA(cudaMemsetAsync(A.status, 0, sizeof(int32_t), st));
+  const int grid = (int)std::min<int64_t>((n_src + kEmWarps - 1) / kEmWarps, (int64_t)num_sms() * 8);
+  for (int it = 0; it < iterations; ++it) {
+    BIMINE_CUDA(cudaMemsetAsync(A.cnt, 0, b_cnt, st));
+    BIMINE_CUDA(cudaMemsetAsync(A.first, 0xff, b_first, st));
+    lexicon_em_round<<<grid, kEmWarps * 32, 0, st>>>(A);
+    BIMINE_CUDA(cudaGetLastError());
+  }
+  int32_t status = 0;
+  BIMINE_CUDA(cudaMemcpyAsync(&status, A.status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  BIMINE_CUDA(cudaStreamSynchronize(st));
+  cudaFreeAsync(scratch, st);
+  if (status) return fail(BIMINE_E_ARG, "bimine_lexicon_em: a target left its row and was looked up again");
+  return BIMINE_OK;
 }
 
 int bimine_exp_device(const double *x_host, double *y_host, int64_t n) {

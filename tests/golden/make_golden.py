@@ -303,6 +303,38 @@ def tuning_fixture():
     print("tuning fixture:", result)
 
 
+def lexicon_em_fixture():
+    """build_lexicon (lexicon.py:60-120) run by the reference on (a) the
+    parallel corpus its own test fixtures train on (conftest.py) and (b) a
+    synthetic corpus with repeated tokens, mixed case, punctuation, a pair
+    with an empty side and unrelated pairs; several round counts and prune
+    thresholds.  Probabilities are stored as float.hex()."""
+    cases = []
+    toy = ref_conftest.make_parallel_sentences(np.random.default_rng(1234), 60)
+    cases.append(("toy", toy, [(10, 1e-4), (1, 1e-4), (3, 0.0)]))
+    rng = np.random.default_rng(555)
+    d = synth.make_dictionary(rng, 300)
+    corpus = synth.make_corpus(556, 6, 300, dictionary=d)
+    par = []
+    for p in range(6):
+        src, tgt = corpus.pair_sentences(p)
+        for i, j in corpus.reference[p]:
+            par.append((src[i], tgt[j]))
+        par.append((src[0], tgt[-1]))  # an unrelated pair
+    par += [("Domo domo, KATO!", "house House cat"), ("...", "nothing"), ("alpha beta alpha", "gamma gamma delta")]
+    cases.append(("synth", par, [(5, 1e-4), (8, 0.05)]))
+    out = []
+    for name, parallel, runs in cases:
+        for iters, prune in runs:
+            lex = build_lexicon(parallel, iters, prune_threshold=prune)
+            table = {s: {t: float(p).hex() for t, p in row.items()} for s, row in lex._table.items()}
+            out.append({"name": name, "iterations": iters, "prune": prune, "table": table})
+        out_inputs = {name: [list(x) for x in parallel] for name, parallel, _ in cases}
+    with open(os.path.join(HERE, "lexicon_em.json"), "w") as fh:
+        json.dump({"inputs": out_inputs, "runs": out}, fh, indent=0)
+    print("lexicon fixture:", [(r["name"], r["iterations"], len(r["table"])) for r in out])
+
+
 def cli_fixture():
     """The reference CLI's `mine` and `tune` (cli.py:129-230) on a small
     synthetic corpus directory: the bitext bytes, printed lines, exit codes
@@ -365,15 +397,37 @@ def cli_fixture():
                           "--budget", "8", "--seed", "3", "--out", rep])
         with open(rep) as fh:
             expect["tune"] = {"rc": rc, "stdout": so, "stderr": se, "report": json.load(fh)}
+    # `dict`: EM lexicon from a parallel file, merged with single-token titles
+    par = []
+    for p in range(4):
+        src, tgt = corpus.pair_sentences(p)
+        par += [(src[i], tgt[j]) for i, j in corpus.reference[p]]
+    with open(os.path.join(out_dir, "parallel.tsv"), "w", encoding="utf-8") as fh:
+        fh.writelines(f"{a}\t{b}\n" for a, b in par)
+    words = d.words(np.arange(20))  # source words s0..s19
+    twords = d.words(d.n_words + np.arange(20))  # target words t0..t19
+    with open(os.path.join(out_dir, "titles.tsv"), "w", encoding="utf-8") as fh:
+        for k in range(20):
+            fh.write(f"{words[k]}\t{twords[k]}\n")
+        fh.write("two words\tone\n")
+        fh.write("...\tx\n")
+    with tempfile.TemporaryDirectory() as tmp:
+        out = os.path.join(tmp, "lex.tsv")
+        rc, so, se = run(["dict", os.path.join(out_dir, "parallel.tsv"), out,
+                          "--titles", os.path.join(out_dir, "titles.tsv")])
+        shutil.copy(out, os.path.join(out_dir, "dict_lexicon.tsv"))
+        expect["dict"] = {"rc": rc, "stdout": so.replace(out, "<OUT>"), "stderr": se}
     with open(os.path.join(out_dir, "expect.json"), "w") as fh:
         json.dump(expect, fh, indent=1)
     print("cli fixture:", {k: (v["rc"], v["stdout"].strip()[:80]) for k, v in expect.items()})
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["toy", "synth", "nw", "exp", "tune", "cli"]
+    which = sys.argv[1:] or ["toy", "synth", "nw", "exp", "tune", "cli", "lexicon"]
     if "cli" in which:
         cli_fixture()
+    if "lexicon" in which:
+        lexicon_em_fixture()
     if "toy" in which:
         toy_fixture()
     if "synth" in which:

@@ -99,3 +99,21 @@ def test_cli_tune_matches_reference(tmp_path):
                        "--budget", "8", "--seed", "3", "--out", str(rep)])
     assert (rc, so) == (want["rc"], want["stdout"])
     assert json.load(open(rep)) == want["report"]
+
+
+@pytest.mark.gpu
+def test_cli_dict_matches_reference_bytes(tmp_path):
+    """`dict`: EM rounds on the GPU + title merge + sorted TSV, byte-identical
+    to the reference CLI's lexicon file and printed lines."""
+    want = _expect()["dict"]
+    out = tmp_path / "lex.tsv"
+    rc, so, se = _run(["dict", os.path.join(G, "parallel.tsv"), str(out), "--titles", os.path.join(G, "titles.tsv")])
+    assert (rc, so.replace(str(out), "<OUT>"), se) == (want["rc"], want["stdout"], want["stderr"])
+    assert out.read_bytes() == open(os.path.join(G, "dict_lexicon.tsv"), "rb").read()
+
+
+def test_read_parallel_errors(tmp_path):
+    (tmp_path / "p.tsv").write_text("a\tb\n\nc\td\te\n")
+    with pytest.raises(ValueError, match="line 3: expected 2 tab-separated fields, got 3"):
+        C.read_parallel(tmp_path / "p.tsv")
+    assert C.read_links(os.path.join(G, "titles.tsv"))[0][0] == "s0"
