@@ -104,3 +104,19 @@ def model_vector(model) -> np.ndarray:
     if len(model.weights) != 6 or len(model.feature_means) != 6 or len(model.feature_scales) != 6:
         raise ValueError(f"model vectors must have length {FEATURE_COUNT}")
     return vec
+
+
+def similarity(model, source_sentence: str, target_sentence: str, lexicon) -> float:
+    """Calibrated translation-likelihood score of one sentence pair
+    (classifier.py:357-362): the 1x1 score matrix of the GPU path, so the
+    same bits as ``build_score_matrix`` (align.py:102-129)."""
+    from .align import build_score_matrix
+
+    try:
+        return float(build_score_matrix(model, lexicon, [source_sentence], [target_sentence])[0, 0])
+    except ValueError as exc:  # the reference reports profile_sentence's message unprefixed
+        msg = str(exc)
+        for prefix in ("source sentence 0: ", "target sentence 0: "):
+            if msg.startswith(prefix):
+                raise ValueError(msg[len(prefix):]) from None
+        raise

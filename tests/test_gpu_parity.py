@@ -154,6 +154,20 @@ def test_toy_score_matrices_bit_exact():
         np.testing.assert_allclose(got, ref, rtol=SCORE_RTOL, atol=0)
 
 
+def test_similarity_is_the_score_matrix_cell():
+    """classifier.similarity (classifier.py:357-362) = the cell of the
+    reference's score matrix, bit for bit; errors unprefixed."""
+    from paper_1512_01641_b200.classifier import similarity
+
+    model, lex = H.toy_model(), H.toy_lexicon()
+    (src, tgt), ref = H.toy_pairs()[0], H.toy_sims()[0]
+    for i in range(min(3, len(src))):
+        for j in range(min(3, len(tgt))):
+            assert bits_equal(np.array([similarity(model, src[i], tgt[j], lex)]), np.array([ref[i, j]]))
+    with pytest.raises(ValueError, match=r"^untokenizable sentence: '\.\.\.'$"):
+        similarity(model, "domo", "...", lex)
+
+
 def test_score_matrix_errors_match_reference():
     model, lex = H.toy_model(), H.toy_lexicon()
     with pytest.raises(ValueError) as exc:
