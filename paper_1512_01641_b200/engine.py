@@ -9,6 +9,7 @@ all compute is in libbimine_b200.so.
 from __future__ import annotations
 
 import ctypes
+import itertools
 import threading
 import weakref
 from dataclasses import dataclass
@@ -323,8 +324,8 @@ def tune_device(dd: DeviceDictionary, model_vec: np.ndarray, batch: PackedBatch,
         ref_off = np.zeros(P, dtype=np.int64)
         if P > 1:
             np.cumsum(ref_len[:-1].astype(np.int64), out=ref_off[1:])
-        flat = [np.asarray(r, dtype=np.int32).reshape(-1) for r in refs if len(r)]
-        ref_ij = np.concatenate(flat) if flat else np.zeros(0, dtype=np.int32)
+        ref_ij = np.fromiter(itertools.chain.from_iterable(itertools.chain.from_iterable(refs)), dtype=np.int32,
+                             count=2 * int(ref_len.sum()))
         t_rij = torch.from_numpy(ref_ij if ref_ij.size else np.zeros(2, np.int32)).to(dev)
         t_roff = torch.from_numpy(ref_off).to(dev)
         t_rlen = torch.from_numpy(ref_len).to(dev)
