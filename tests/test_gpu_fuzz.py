@@ -83,3 +83,34 @@ def test_random_batches_match_oracle(case):
     assert np.array_equal(counts, want_counts)
     flat = np.concatenate(want_rows) if want_rows else np.zeros(0, dtype=matches.dtype)
     assert np.array_equal(matches.view(np.uint8), flat.view(np.uint8))
+
+
+@st.composite
+def nw_problems(draw):
+    rng = np.random.default_rng(draw(st.integers(0, 2**32 - 1)))
+    n, m = draw(st.integers(1, 300)), draw(st.integers(1, 300))
+    kind = draw(st.sampled_from(["uniform", "binary", "levels"]))
+    if kind == "uniform":
+        sim = rng.random((n, m))
+    elif kind == "binary":
+        sim = (rng.random((n, m)) > 0.7).astype(np.float64)
+    else:  # few distinct values: tie-heavy DP
+        sim = rng.integers(0, 4, size=(n, m)) / 3.0
+    gap = draw(st.sampled_from([0.0, 0.25, 0.5, 1.0, 2.0]))
+    return sim, gap
+
+
+@settings(max_examples=40, deadline=None, derandomize=True, suppress_health_check=list(HealthCheck))
+@given(st.lists(nw_problems(), min_size=1, max_size=3))
+def test_random_nw_problems_match_oracle(problems):
+    """Small (warp per problem) and large (cluster band pipeline) NW paths,
+    one batch: step codes and dp[N][M] bit-identical to the oracle."""
+    from paper_1512_01641_b200 import engine as E
+
+    sims = [s for s, _ in problems]
+    gaps = [g for _, g in problems]
+    out = E.nw_steps_host(sims, gaps, -1.0, 1.0)
+    for (sim, gap), (codes, score) in zip(problems, out):
+        want, _, _, want_score = oracle.nw_align(sim, -1.0, 1.0, gap)
+        assert np.array_equal(codes, want)
+        assert np.array_equal(np.array([score]).view(np.uint64), np.array([want_score]).view(np.uint64))
