@@ -274,6 +274,15 @@ int bimine_tokenize_batch(bimine_vocab *vocab, const char *buf,
                           int64_t cap, int64_t *n_tokens, int32_t *len_out,
                           int32_t *uniq_out, int32_t *chars_out);
 
+/* Like bimine_score_batch, and also writes the six features of every cell
+ * (extract_features / features_from_profiles, classifier.py:62-112) to
+ * features_dev[6 * (pair_sim_off + i * M + j) + k], k = token ratio,
+ * source coverage, target coverage, mean best probability, char ratio,
+ * shared-token overlap.  Pairs whose sentences exceed 255 tokens
+ * (plan->n_long > 0) are refused with BIMINE_E_LIMIT. */
+int bimine_features_batch(const bimine_dict *dict, const double *model, const bimine_batch *batch,
+                          const bimine_plan *plan, double *sim_dev, double *features_dev, void *stream);
+
 /* ---- lexicon EM -----------------------------
  * Replaces the EM loop of build_lexicon (lexicon.py:60-120): `iterations`
  * rounds over device arrays, bit-identical to the reference's float64

@@ -113,6 +113,8 @@ SIGNATURES = {
                                         ctypes.c_double, ctypes.c_double, _i32p, _vp, ctypes.c_int64, _i64p,
                                         _vp, _vp]),
     "bimine_exp_device": (ctypes.c_int, [_f64p, _f64p, ctypes.c_int64]),
+    "bimine_features_batch": (ctypes.c_int, [_vp, _f64p, ctypes.POINTER(CBatch), ctypes.POINTER(CPlan), _vp, _vp,
+                                             _vp]),
     # device pointers (torch tensors' data_ptr)
     "bimine_lexicon_em": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp, ctypes.c_int64, _vp,
                                          _vp, _vp, _vp, ctypes.c_int32, _vp]),

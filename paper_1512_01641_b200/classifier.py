@@ -120,3 +120,29 @@ def similarity(model, source_sentence: str, target_sentence: str, lexicon) -> fl
             if msg.startswith(prefix):
                 raise ValueError(msg[len(prefix):]) from None
         raise
+
+
+# any valid model: the features do not depend on it (the kernel also scores)
+_FEATURE_MODEL = np.array([0.0] * 6 + [0.0, -1.0, 0.0] + [0.0] * 6 + [1.0] * 6, dtype=np.float64)
+
+
+def extract_features(source_sentence: str, target_sentence: str, lexicon) -> list[float]:
+    """Six-feature description of a sentence pair (classifier.py:100-112):
+    token-length ratio (capped at 4), source coverage, target coverage, mean
+    best translation probability, char-length ratio (capped at 4), shared
+    identical tokens -- computed by the score kernel's features mode
+    (bimine_features_batch), the same arithmetic the scores use."""
+    from . import engine as E
+    from .align import _pack_one
+
+    ctx = E.lexicon_context(lexicon)
+    try:
+        batch = _pack_one(ctx.vocab, [source_sentence], [target_sentence])
+    except ValueError as exc:  # profile_sentence's message, unprefixed
+        msg = str(exc)
+        for prefix in ("source sentence 0: ", "target sentence 0: "):
+            if msg.startswith(prefix):
+                raise ValueError(msg[len(prefix):]) from None
+        raise
+    feats = E.features_host(ctx.on(E.current_device()), _FEATURE_MODEL, batch)
+    return [float(v) for v in feats[0]]

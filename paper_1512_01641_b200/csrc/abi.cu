@@ -354,7 +354,7 @@ struct FusedNw {
 };
 
 int launch_scores(const bimine_dict *dict, const double *model, const bimine_batch *b, const bimine_plan *plan,
-                  double *sim_dev, const FusedNw *nw, cudaStream_t st) {
+                  double *sim_dev, const FusedNw *nw, cudaStream_t st, double *features = nullptr) {
   if (!dict || !model || !b || !plan || !sim_dev) return fail(BIMINE_E_ARG, "bimine_score_batch: null argument");
   if (b->n_pairs == 0) return BIMINE_OK;
   if (plan->max_n < 1 || plan->max_m < 1 || plan->max_uniq < 1 || plan->max_len < 1)
@@ -400,6 +400,7 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
     // one launch: the tiles of pairs larger than 64x64, then one CTA per pair
     A.tiles = plan->n_tiles ? plan->work : nullptr;
     A.n_tiles = plan->n_tiles;
+    A.features = features;
     if (tl_gate) {
       A.ready = tl_gate->ready;
       A.need = tl_gate->need;
@@ -1138,6 +1139,15 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
 __global__ void exp_kernel(const double *x, double *y, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = glibc_exp(x[i], kExpTableDev);
+}
+
+int bimine_features_batch(const bimine_dict *dict, const double *model, const bimine_batch *b,
+                          const bimine_plan *plan, double *sim_dev, double *features_dev, void *stream) {
+  if (!features_dev) return fail(BIMINE_E_ARG, "bimine_features_batch: null features buffer");
+  if (plan && plan->n_long > 0)
+    return fail(BIMINE_E_LIMIT, "bimine_features_batch: sentences longer than 255 tokens are not supported");
+  pool_setup();
+  return launch_scores(dict, model, b, plan, sim_dev, nullptr, as_stream(stream), features_dev);
 }
 
 int bimine_lexicon_em(const int32_t *tgt_off, const int32_t *tgt_tok, int64_t n_pairs, int32_t n_src,

@@ -63,6 +63,9 @@ struct PairArgs {
   int32_t *nw_counts;
   double *nw_score;          // optional
   double gap, threshold, mismatch, bonus;
+  // features mode (extract_features, classifier.py:62-112): the six
+  // features of every cell at features[6 * (pair_sim_off + i * M + j) + k]
+  double *features;
   // upload gate (bimine_mine_host): pair p's data are on the device once
   // *ready >= need[p] (the counter grows as pieces land); null: no wait
   const int32_t *ready;
@@ -635,6 +638,17 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
     const double v = cell_score_t(A.md, A.T, S.src_len[i], S.src_uniq[i], S.src_chars[i], S.tgt_len[j],
                                   S.tgt_uniq[j], S.tgt_chars[j], (int)(ax & 0xffu), out[o], S.covt[x],
                                   (int)(ax >> 8), S.exp_tab);
+    if (A.features) {  // features_from_profiles (classifier.py:69-97), IEEE divisions
+      const int cov = (int)(ax & 0xffu), sh = (int)(ax >> 8), covt = S.covt[x];
+      const int Ls = S.src_len[i], Lt = S.tgt_len[j], Us = S.src_uniq[i], Ut = S.tgt_uniq[j];
+      double *f = A.features + 6 * (A.b.pair_sim_off[p] + (int64_t)(i0 + i) * Mfull + (j0 + j));
+      f[0] = clip4(fdiv((double)Ls, (double)Lt));
+      f[1] = fdiv((double)cov, (double)Ls);
+      f[2] = fdiv((double)covt, (double)Lt);
+      f[3] = cov ? fdiv(out[o], (double)cov) : 0.0;
+      f[4] = clip4(fdiv((double)S.src_chars[i], (double)S.tgt_chars[j]));
+      f[5] = fdiv((double)sh, (double)(Us > Ut ? Us : Ut));
+    }
     out[o] = v;
     if (fuse_nw) tile[i * 64 + j] = v;
     i += di;

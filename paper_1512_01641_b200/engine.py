@@ -236,6 +236,22 @@ def score_host(dd: DeviceDictionary, model_vec: np.ndarray, batch: PackedBatch) 
         return sim[: batch.n_cells].cpu().numpy()
 
 
+def features_host(dd: DeviceDictionary, model_vec: np.ndarray, batch: PackedBatch) -> np.ndarray:
+    """The six features of every cell of a host batch (bimine_features_batch),
+    [cells, 6] in pair_sim_off order."""
+    torch = _torch()
+    L = N.load()
+    mv = np.ascontiguousarray(model_vec, dtype=np.float64)
+    with torch.cuda.device(dd.device):
+        db = DeviceBatch(batch, dd.device)
+        dev = f"cuda:{dd.device}"
+        sim = torch.empty(max(batch.n_cells, 1), dtype=torch.float64, device=dev)
+        feats = torch.empty(max(batch.n_cells, 1) * 6, dtype=torch.float64, device=dev)
+        N.check(L.bimine_features_batch(dd.handle, N.ptr(mv, N._f64p), ctypes.byref(db.struct), ctypes.byref(db.plan),
+                                        sim.data_ptr(), feats.data_ptr(), stream_ptr(None)))
+        return feats[: 6 * batch.n_cells].cpu().numpy().reshape(-1, 6)
+
+
 def nw_steps_host(sims: list[np.ndarray], gaps: list[float], mismatch: float, bonus: float, device: int | None = None):
     """Full step lists for a list of matrices: [(codes uint8[k], score)]."""
     torch = _torch()

@@ -303,6 +303,34 @@ def tuning_fixture():
     print("tuning fixture:", result)
 
 
+def features_fixture():
+    """extract_features (classifier.py:100-112) by the reference on every
+    cell of the toy pairs (toy.json's lexicon) and on hand-picked edge
+    pairs: ratio caps at 4, no coverage, identical sentences, repeated and
+    shared tokens."""
+    from bimine.classifier import extract_features
+
+    with open(os.path.join(HERE, "toy.json")) as fh:
+        toy = json.load(fh)
+    table = {}
+    for s, t, p in toy["lexicon"]:
+        table.setdefault(s, {})[t] = float.fromhex(p)
+    lex = Lexicon(table)
+    cells = []
+    for pair in toy["pairs"]:
+        for a in pair["source"]:
+            for b in pair["target"]:
+                cells.append([a, b, [float(v).hex() for v in extract_features(a, b, lex)]])
+    edge = [("domo kato hundo domo kato hundo domo kato hundo", "house"), ("x", "a b c d e f g h i j"),
+            ("zork blip", "quux flub"), ("domo domo domo", "house house"), ("Domo, KATO!", "domo kato"),
+            ("libro floro", "libro book flower"), ("a", "a")]
+    for a, b in edge:
+        cells.append([a, b, [float(v).hex() for v in extract_features(a, b, lex)]])
+    with open(os.path.join(HERE, "features_golden.json"), "w") as fh:
+        json.dump({"cells": cells}, fh, indent=0)
+    print("features fixture:", len(cells), "cells")
+
+
 def lexicon_em_fixture():
     """build_lexicon (lexicon.py:60-120) run by the reference on (a) the
     parallel corpus its own test fixtures train on (conftest.py) and (b) a
@@ -423,11 +451,13 @@ def cli_fixture():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["toy", "synth", "nw", "exp", "tune", "cli", "lexicon"]
+    which = sys.argv[1:] or ["toy", "synth", "nw", "exp", "tune", "cli", "lexicon", "features"]
     if "cli" in which:
         cli_fixture()
     if "lexicon" in which:
         lexicon_em_fixture()
+    if "features" in which:
+        features_fixture()
     if "toy" in which:
         toy_fixture()
     if "synth" in which:

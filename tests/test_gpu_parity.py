@@ -168,6 +168,20 @@ def test_similarity_is_the_score_matrix_cell():
         similarity(model, "domo", "...", lex)
 
 
+def test_extract_features_match_reference():
+    """classifier.extract_features (features mode of the score kernel) =
+    the reference's extract_features bit for bit (tests/golden/
+    features_golden.json: every toy cell + edge pairs)."""
+    from paper_1512_01641_b200.classifier import extract_features
+
+    lex = H.toy_lexicon()
+    for a, b, want in H.load_json("features_golden.json")["cells"]:
+        got = extract_features(a, b, lex)
+        assert [float(v).hex() for v in got] == want, (a, b)
+    with pytest.raises(ValueError, match=r"^untokenizable sentence: '\.\.\.'$"):
+        extract_features("...", "house", lex)
+
+
 def test_score_matrix_errors_match_reference():
     model, lex = H.toy_model(), H.toy_lexicon()
     with pytest.raises(ValueError) as exc:
