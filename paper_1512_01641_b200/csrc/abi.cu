@@ -395,8 +395,9 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
       A.mismatch = nw->mismatch;
       A.bonus = nw->bonus;
     }
-    BIMINE_CUDA(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    BIMINE_CUDA(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    auto kern = features ? pair_kernel<true> : pair_kernel<false>;
+    BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     // one launch: the tiles of pairs larger than 64x64, then one CTA per pair
     A.tiles = plan->n_tiles ? plan->work : nullptr;
     A.n_tiles = plan->n_tiles;
@@ -407,7 +408,7 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
     }
     const int64_t grid = plan->n_tiles + b->n_pairs;
     if (grid > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: too many CTAs");
-    pair_kernel<<<(unsigned)grid, kPairThreads, smem, st>>>(A);
+    kern<<<(unsigned)grid, kPairThreads, smem, st>>>(A);
     const cudaError_t le = cudaGetLastError();
     cudaFreeAsync(A.aux, st);
     if (le != cudaSuccess) return fail(BIMINE_E_CUDA, std::string("pair_kernel: ") + cudaGetErrorString(le));

@@ -206,6 +206,8 @@ __host__ __device__ inline bool pair_is_small(int n, int m, int max_len) {
   return n <= kPairMax && m <= kPairMax && max_len <= kPairMaxLen;
 }
 
+// kFeatures: also write the six features per cell (bimine_features_batch)
+template <bool kFeatures>
 __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // CTAs [0, n_tiles) take the 64x64 tiles of large pairs (first, so the
@@ -638,7 +640,7 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
     const double v = cell_score_t(A.md, A.T, S.src_len[i], S.src_uniq[i], S.src_chars[i], S.tgt_len[j],
                                   S.tgt_uniq[j], S.tgt_chars[j], (int)(ax & 0xffu), out[o], S.covt[x],
                                   (int)(ax >> 8), S.exp_tab);
-    if (A.features) {  // features_from_profiles (classifier.py:69-97), IEEE divisions
+    if (kFeatures) {  // features_from_profiles (classifier.py:69-97), IEEE divisions
       const int cov = (int)(ax & 0xffu), sh = (int)(ax >> 8), covt = S.covt[x];
       const int Ls = S.src_len[i], Lt = S.tgt_len[j], Us = S.src_uniq[i], Ut = S.tgt_uniq[j];
       double *f = A.features + 6 * (A.b.pair_sim_off[p] + (int64_t)(i0 + i) * Mfull + (j0 + j));
