@@ -1063,10 +1063,9 @@ __global__ void __launch_bounds__(32) nw_big_traceback_kernel(const NwArgs A, co
         // load itself on the walk's dependency chain
         const int wg = win_g, wk0 = win_k0;
         const uint16_t *wb = win;
-        while (a > 0 && b > 0) {
-          const int gg = (a - 1) >> 5, ll = (a - 1) & 31, ss = b + ll - 1, kk = ss >> 3;
-          if (gg != wg || kk < wk0 || kk >= wk0 + 16) break;
-          const uint32_t d = ((uint32_t)wb[(kk - wk0) * 32 + ll] >> (2 * (ss & 7))) & 3u;
+        auto step = [&]() {
+          const int ll = (a - 1) & 31, ss = b + ll - 1;
+          const uint32_t d = ((uint32_t)wb[((ss >> 3) - wk0) * 32 + ll] >> (2 * (ss & 7))) & 3u;
           if (MODE == kNwMine) {
             if (d == 0u) {
               outm[cnt].i = N - a;  // score filled below
@@ -1078,6 +1077,25 @@ __global__ void __launch_bounds__(32) nw_big_traceback_kernel(const NwArgs A, co
           }
           a -= (d != 2u);
           b -= (d != 1u);
+        };
+        while (a > 0 && b > 0) {
+          const int gg = (a - 1) >> 5, ll = (a - 1) & 31, ss = b + ll - 1, kk = ss >> 3;
+          if (gg != wg || kk < wk0 || kk >= wk0 + 16) break;
+          // steps that cannot leave the band, the window or the table: each
+          // step lowers a by <= 1 and s = b + l - 1 by <= 2, and b by <= 1
+          const int safe = min(min(ll, b - 1), (ss - 8 * wk0) >> 1);
+          if (safe <= 0) {
+            step();
+            continue;
+          }
+          int t = 0;
+          for (; t + 4 <= safe; t += 4) {
+            step();
+            step();
+            step();
+            step();
+          }
+          for (; t < safe; ++t) step();
         }
       }
       __syncwarp();
