@@ -206,15 +206,26 @@ def nw_device(db: DeviceBatch, sim, gap: float, threshold: float, mismatch: floa
 # ---------------------------------------------------------------------------
 
 def mine_host(dd: DeviceDictionary, model_vec: np.ndarray, batch: PackedBatch, gap: float, threshold: float,
-              mismatch: float, bonus: float, want_sim: bool = False, stream=None):
+              mismatch: float, bonus: float, want_sim: bool = False, stream=None, out=None):
     """bimine_mine_host: H2D, score, NW, filter, compact, D2H.  Returns
-    (counts[P], matches structured array, sim or None)."""
+    (counts[P], matches structured array, sim or None).
+
+    `out`: optional dict reused across calls (a streaming caller's output
+    buffers: counts and matches land in the same host memory every call, so
+    the copy-out does not first-touch fresh pages); the returned arrays are
+    views into it, valid until the next call with the same `out`."""
     L = N.load()
     torch = _torch()
     P = batch.n_pairs
-    counts = np.empty(max(P, 1), dtype=np.int32)  # filled for every pair
     cap = int(batch.match_capacity()[-1])
-    matches = np.empty(max(cap, 1), dtype=N.MATCH_DTYPE)  # the first `total` are filled
+    if out is not None and out.get("counts") is not None and out["counts"].size >= max(P, 1) \
+            and out["matches"].size >= max(cap, 1):
+        counts, matches = out["counts"], out["matches"]
+    else:
+        counts = np.empty(max(P, 1), dtype=np.int32)  # filled for every pair
+        matches = np.empty(max(cap, 1), dtype=N.MATCH_DTYPE)  # the first `total` are filled
+        if out is not None:
+            out["counts"], out["matches"] = counts, matches
     total = np.zeros(1, dtype=np.int64)
     sim = np.empty(max(batch.n_cells, 1), dtype=np.float64) if want_sim else None
     cb = N.batch_struct_host(batch)

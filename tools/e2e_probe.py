@@ -55,3 +55,13 @@ c.record()
 torch.cuda.synchronize()
 ms = a.elapsed_time(c) / 5
 print(f"pinned H2D {tok.numel()*4/1e6:.1f} MB in {ms:.3f} ms = {tok.numel()*4/ms/1e6:.1f} GB/s")
+outbuf = {}
+E.mine_host(dd, mv, pb, 2.0, 0.5, -1.0, 1.0, out=outbuf)
+t = time.perf_counter()
+for _ in range(reps):
+    E.mine_host(dd, mv, pb, 2.0, 0.5, -1.0, 1.0, out=outbuf)
+print(f"mine_host with reused outputs {(time.perf_counter() - t) / reps * 1e3:.2f} ms")
+t = time.perf_counter()
+for _ in range(100):
+    cb2 = N.batch_struct_host(pb)
+print(f"batch_struct_host {(time.perf_counter() - t) / 100 * 1e3:.3f} ms")
