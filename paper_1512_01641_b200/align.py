@@ -9,8 +9,9 @@ GPU through libbimine_b200.so:
   kernel in step mode (both engines are the same GPU wavefront; the
   reference guarantees their outputs are identical, align.py:184-187)
 * ``align_pair_indices`` / ``mine_document_pair`` / ``mine_corpus``
-  (align.py:347-448) -> score + NW + traceback + threshold filter fused
-  per batch, compacted on device in input order.
+  (align.py:347-448) -> one ``bimine_mine_host`` call per batch: score
+  kernel, NW + traceback + threshold filter, compaction in input order
+  (uploads overlapped with the scoring).
 
 ``mine_corpus`` packs all pairs into one batch (pairs whose sentences do
 not tokenise are reported as failures with the reference's message and
@@ -283,9 +284,10 @@ def mine_corpus(model, lexicon, pairs: Sequence, config: MiningConfig, engine: s
             with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
                 results = list(ex.map(run, jobs))
         for lo, counts, matches in results:
+            score, ii, jj = matches["score"].tolist(), matches["i"].tolist(), matches["j"].tolist()
             pos = 0
             for b, c in enumerate(counts.tolist()):
-                per_pair[index_of[lo + b]] = matches[pos : pos + c]
+                per_pair[index_of[lo + b]] = (score[pos : pos + c], ii[pos : pos + c], jj[pos : pos + c])
                 pos += c
     rows: list[tuple[float, str, str]] = []
     failures: list[tuple[str, str]] = []
@@ -294,6 +296,6 @@ def mine_corpus(model, lexicon, pairs: Sequence, config: MiningConfig, engine: s
             failures.append((pair.topic_id, errors[k]))
             continue
         src, tgt = pair.source.sentences, pair.target.sentences
-        for r in per_pair[k]:
-            rows.append((float(r["score"]), src[int(r["i"])], tgt[int(r["j"])]))
+        score, ii, jj = per_pair[k]
+        rows.extend(zip(score, [src[i] for i in ii], [tgt[j] for j in jj]))
     return MiningOutcome(rows=tuple(rows), failures=tuple(failures))

@@ -9,39 +9,244 @@
 // with any non-ASCII byte is reported back (length -1) and tokenised by
 // the Python rules on the host (full Unicode lower()/split()), through the
 // same vocabulary, so both paths produce the same ids.
+//
+// The vocabulary is a flat open-addressing table (32-byte slots: hash,
+// id, length, the first 16 bytes of the word; all word bytes in a block
+// arena, so bimine_vocab_word pointers stay valid).  A large batch is tokenised in three phases: (1) threads
+// split, lowercase, hash and LOOK UP their contiguous sentence range in
+// the read-only table, recording words not found; (2) one thread inserts
+// the missing words in batch order -- thread ranges are in sentence order,
+// so ids are assigned in first-occurrence order exactly as a serial pass
+// would; (3) threads patch the new ids in, count distinct tokens per
+// sentence and copy their tokens to the output.
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
-#include <string>
-#include <string_view>
-#include <unordered_map>
-#include <unordered_set>
+#include <memory>
+#include <thread>
 #include <vector>
 
 #include "../../include/bimine_b200.h"
 
-struct bimine_vocab {
-  std::unordered_map<std::string, int32_t> ids;
-  std::vector<const std::string *> words;  // id -> key stored in `ids`
-
-  int32_t get(std::string_view w) {
-    auto it = ids.find(std::string(w));
-    if (it != ids.end()) return it->second;
-    const int32_t id = (int32_t)words.size();
-    auto ins = ids.emplace(std::string(w), id);
-    words.push_back(&ins.first->first);
-    return id;
-  }
-};
-
 namespace {
+
+inline uint64_t hash_words(const char *p, uint32_t n) {
+  // p is readable and zero-padded up to the next multiple of 8 bytes.
+  uint64_t h = 0x243F6A8885A308D3ull ^ ((uint64_t)n * 0x9E3779B97F4A7C15ull);
+  for (uint32_t i = 0; i < n; i += 8) {
+    uint64_t w;
+    memcpy(&w, p + i, 8);
+    h = (h ^ w) * 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 31;
+  }
+  h ^= h >> 30;
+  h *= 0x94D049BB133111EBull;
+  return h ^ (h >> 29);
+}
+
+// zero-padded copy of a word (the layout find() and hash_words() read)
+inline const char *padded(const char *w, uint32_t n, std::vector<char> &pad) {
+  if (pad.size() < (size_t)n + 16) pad.resize((size_t)n + 16);
+  memcpy(pad.data(), w, n);
+  memset(pad.data() + n, 0, 16);
+  return pad.data();
+}
 
 constexpr bool is_space(unsigned char c) {
   return c == ' ' || (c >= '\t' && c <= '\r') || (c >= 0x1c && c <= 0x1f);
 }
 
-bool is_punct(unsigned char c) {
-  static const char *P = "!\"#$%&'()*+,-./:;<=>?@[\\]^_`{|}~";
-  return c < 128 && c && strchr(P, c) != nullptr;
+struct PunctTable {
+  bool p[256] = {};
+  constexpr PunctTable() {
+    const char *P = "!\"#$%&'()*+,-./:;<=>?@[\\]^_`{|}~";
+    for (int i = 0; P[i]; ++i) p[(unsigned char)P[i]] = true;
+  }
+};
+constexpr PunctTable kPunct;
+
+int host_threads() {
+  static const int n = [] {
+    const char *e = getenv("BIMINE_HOST_THREADS");
+    int v = e ? atoi(e) : (int)std::thread::hardware_concurrency();
+    return std::max(1, std::min(v, 64));
+  }();
+  return n;
+}
+
+}  // namespace
+
+struct bimine_vocab {
+  struct Slot {
+    uint64_t hash;
+    int32_t id;  // -1: empty
+    uint32_t len;
+    uint64_t key[2];  // first 16 bytes of the word, zero-padded
+  };
+  std::vector<Slot> slots = std::vector<Slot>(1u << 16, Slot{0, -1, 0, {0, 0}});
+  size_t mask = (1u << 16) - 1;
+  std::vector<const char *> word_ptr;  // id -> bytes in `blocks`
+  std::vector<uint32_t> word_len;
+  std::vector<std::unique_ptr<char[]>> blocks;
+  size_t block_used = 0, block_cap = 0;
+
+  int32_t size() const { return (int32_t)word_ptr.size(); }
+
+  const Slot *slot_of(uint64_t h) const { return &slots[h & mask]; }
+
+  // w: n bytes, then zeros to at least max(16, n rounded up to 8) bytes
+  int32_t find(uint64_t h, const char *w, uint32_t n) const {
+    uint64_t k0, k1;
+    memcpy(&k0, w, 8);
+    memcpy(&k1, w + 8, 8);
+    for (size_t i = h & mask;; i = (i + 1) & mask) {
+      const Slot &s = slots[i];
+      if (s.id < 0) return -1;
+      if (s.hash == h && s.len == n && s.key[0] == k0 && s.key[1] == k1 &&
+          (n <= 16 || memcmp(word_ptr[s.id] + 16, w + 16, n - 16) == 0))
+        return s.id;
+    }
+  }
+
+  int32_t insert(uint64_t h, const char *w, uint32_t n) {  // w absent
+    if (block_used + n + 1 > block_cap) {
+      block_cap = std::max<size_t>(1u << 20, (size_t)n + 1);
+      blocks.emplace_back(new char[block_cap]);
+      block_used = 0;
+    }
+    char *dst = blocks.back().get() + block_used;
+    memcpy(dst, w, n);
+    dst[n] = 0;
+    block_used += n + 1;
+    const int32_t id = size();
+    word_ptr.push_back(dst);
+    word_len.push_back(n);
+    if ((size_t)(id + 1) * 2 > slots.size()) grow();
+    size_t i = h & mask;
+    while (slots[i].id >= 0) i = (i + 1) & mask;
+    Slot &s = slots[i];
+    s = Slot{h, id, n, {0, 0}};
+    memcpy(s.key, w, std::min<uint32_t>(n, 16));
+    return id;
+  }
+
+  void grow() {
+    std::vector<Slot> old(slots.size() * 2, Slot{0, -1, 0, {0, 0}});
+    old.swap(slots);
+    mask = slots.size() - 1;
+    for (const Slot &s : old)
+      if (s.id >= 0) {
+        size_t i = s.hash & mask;
+        while (slots[i].id >= 0) i = (i + 1) & mask;
+        slots[i] = s;
+      }
+  }
+
+  int32_t get(uint64_t h, const char *w, uint32_t n) {
+    const int32_t id = find(h, w, n);
+    return id >= 0 ? id : insert(h, w, n);
+  }
+};
+
+namespace {
+
+// Phase 1 state of one thread: its sentences [k0, k1).
+struct TokRange {
+  int64_t k0 = 0, k1 = 0;
+  std::vector<int32_t> tok;  // id, or -(index into miss) - 1
+  struct Miss {
+    uint64_t hash;
+    uint32_t off, len;  // in `words`
+  };
+  std::vector<Miss> miss;
+  std::vector<char> words;  // lowercased missing words, zero-padded like tokenize_range's
+  std::vector<int32_t> resolved;
+  int64_t out_off = 0;
+};
+
+// Per sentence, two passes: split + lowercase + hash every token and
+// prefetch its home slot, then resolve them (the table is far larger than
+// the caches; the prefetches overlap the misses).
+void tokenize_range(const bimine_vocab &v, const unsigned char *buf, const int64_t *off, TokRange &r,
+                    int32_t *len_out, int32_t *chars_out) {
+  std::vector<char> low;  // the sentence's words, each zero-padded (16 + round-up to 8)
+  struct Tok {
+    uint64_t hash;
+    uint32_t off, len;
+  };
+  std::vector<Tok> toks;
+  for (int64_t k = r.k0; k < r.k1; ++k) {
+    const unsigned char *p = buf + off[k];
+    const int64_t L = off[k + 1] - off[k];
+    chars_out[k] = (int32_t)L;
+    bool ascii = true;
+    for (int64_t x = 0; x < L; ++x)
+      if (p[x] >= 0x80) {
+        ascii = false;
+        break;
+      }
+    if (!ascii) {
+      len_out[k] = -1;  // the caller applies the Unicode rules
+      continue;
+    }
+    low.resize((size_t)L + 12 * (size_t)(L + 1) + 32);  // <= (L+1)/2 tokens, each its bytes + <= 23
+    toks.clear();
+    uint32_t lo = 0;
+    int64_t x = 0;
+    while (x < L) {
+      while (x < L && is_space(p[x])) ++x;
+      int64_t a = x;
+      while (x < L && !is_space(p[x])) ++x;
+      int64_t b = x;
+      while (a < b && kPunct.p[p[a]]) ++a;
+      while (b > a && kPunct.p[p[b - 1]]) --b;
+      if (b > a) {
+        const uint32_t n = (uint32_t)(b - a);
+        char *w = low.data() + lo;
+        for (uint32_t i = 0; i < n; ++i) {
+          const unsigned char c = p[a + i];
+          w[i] = (char)((unsigned)(c - 'A') < 26u ? c | 0x20 : c);
+        }
+        memset(w + n, 0, 16);
+        const uint64_t h = hash_words(w, n);
+        __builtin_prefetch(v.slot_of(h));
+        toks.push_back({h, lo, n});
+        lo += ((n + 7) & ~7u) + 16;
+      }
+    }
+    for (const Tok &t : toks) {
+      int32_t id = v.find(t.hash, low.data() + t.off, t.len);
+      if (id < 0) {
+        const uint32_t wo = (uint32_t)r.words.size();
+        const char *w = low.data() + t.off;
+        r.words.insert(r.words.end(), w, w + ((t.len + 7) & ~7u) + 16);
+        r.miss.push_back({t.hash, wo, t.len});
+        id = -(int32_t)r.miss.size();
+      }
+      r.tok.push_back(id);
+    }
+    len_out[k] = (int32_t)toks.size();
+  }
+}
+
+void finish_range(TokRange &r, const int32_t *len_out, int32_t *uniq_out, int32_t *tokens) {
+  int32_t *dst = tokens + r.out_off;
+  const int32_t *src = r.tok.data();
+  std::vector<int32_t> scratch;
+  for (int64_t k = r.k0; k < r.k1; ++k) {
+    const int32_t n = len_out[k];
+    if (n < 0) {
+      uniq_out[k] = 0;
+      continue;
+    }
+    for (int32_t i = 0; i < n; ++i) dst[i] = src[i] >= 0 ? src[i] : r.resolved[-src[i] - 1];
+    scratch.assign(dst, dst + n);
+    std::sort(scratch.begin(), scratch.end());
+    uniq_out[k] = (int32_t)(std::unique(scratch.begin(), scratch.end()) - scratch.begin());
+    dst += n;
+    src += n;
+  }
 }
 
 }  // namespace
@@ -59,18 +264,23 @@ int bimine_vocab_destroy(bimine_vocab *v) {
   return BIMINE_OK;
 }
 
-int64_t bimine_vocab_size(const bimine_vocab *v) { return v ? (int64_t)v->words.size() : -1; }
+int64_t bimine_vocab_size(const bimine_vocab *v) { return v ? (int64_t)v->size() : -1; }
 
 int bimine_vocab_add_batch(bimine_vocab *v, const char *buf, const int64_t *off, int64_t n, int32_t *ids) {
   if (!v || (n > 0 && (!buf || !off || !ids))) return BIMINE_E_ARG;
-  for (int64_t k = 0; k < n; ++k) ids[k] = v->get(std::string_view(buf + off[k], (size_t)(off[k + 1] - off[k])));
+  std::vector<char> pad;
+  for (int64_t k = 0; k < n; ++k) {
+    const uint32_t len = (uint32_t)(off[k + 1] - off[k]);
+    const char *w = padded(buf + off[k], len, pad);
+    ids[k] = v->get(hash_words(w, len), w, len);
+  }
   return BIMINE_OK;
 }
 
 int bimine_vocab_word(const bimine_vocab *v, int32_t id, const char **ptr, int64_t *len) {
-  if (!v || !ptr || !len || id < 0 || id >= (int32_t)v->words.size()) return BIMINE_E_ARG;
-  *ptr = v->words[id]->data();
-  *len = (int64_t)v->words[id]->size();
+  if (!v || !ptr || !len || id < 0 || id >= v->size()) return BIMINE_E_ARG;
+  *ptr = v->word_ptr[id];
+  *len = (int64_t)v->word_len[id];
   return BIMINE_OK;
 }
 
@@ -78,48 +288,39 @@ int bimine_tokenize_batch(bimine_vocab *v, const char *buf, const int64_t *off, 
                           int64_t cap, int64_t *n_tokens, int32_t *len_out, int32_t *uniq_out, int32_t *chars_out) {
   if (!v || !n_tokens || (n > 0 && (!buf || !off || !len_out || !uniq_out || !chars_out)))
     return BIMINE_E_ARG;
-  int64_t t = 0;
-  std::string low;
-  std::unordered_set<int32_t> seen;
-  for (int64_t k = 0; k < n; ++k) {
-    const unsigned char *p = (const unsigned char *)buf + off[k];
-    const int64_t L = off[k + 1] - off[k];
-    bool ascii = true;
-    for (int64_t x = 0; x < L; ++x)
-      if (p[x] >= 0x80) {
-        ascii = false;
-        break;
-      }
-    chars_out[k] = (int32_t)L;
-    if (!ascii) {
-      len_out[k] = -1;  // the caller applies the Unicode rules
-      uniq_out[k] = 0;
-      continue;
-    }
-    const int64_t t0 = t;
-    seen.clear();
-    int64_t x = 0;
-    while (x < L) {
-      while (x < L && is_space(p[x])) ++x;
-      int64_t a = x;
-      while (x < L && !is_space(p[x])) ++x;
-      int64_t b = x;
-      while (a < b && is_punct(p[a])) ++a;
-      while (b > a && is_punct(p[b - 1])) --b;
-      if (b > a) {
-        low.assign((const char *)p + a, (size_t)(b - a));
-        for (char &c : low)
-          if (c >= 'A' && c <= 'Z') c = (char)(c - 'A' + 'a');
-        if (t >= cap) return BIMINE_E_LIMIT;
-        const int32_t id = v->get(low);
-        tokens[t++] = id;
-        seen.insert(id);
-      }
-    }
-    len_out[k] = (int32_t)(t - t0);
-    uniq_out[k] = (int32_t)seen.size();
+  *n_tokens = 0;
+  if (n <= 0) return BIMINE_OK;
+  // contiguous sentence ranges of about equal bytes, >= 256 KB each
+  const int64_t bytes = off[n] - off[0];
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(host_threads(), bytes >> 18));
+  std::vector<TokRange> R(nt);
+  for (int t = 0; t < nt; ++t) {
+    R[t].k0 = t == 0 ? 0 : R[t - 1].k1;
+    R[t].k1 = t == nt - 1 ? n
+                          : std::lower_bound(off + R[t].k0, off + n, off[0] + bytes * (t + 1) / nt) - off;
   }
-  *n_tokens = t;
+  auto parallel = [&](auto &&fn) {
+    if (nt == 1) return fn(R[0]);
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back([&, t] { fn(R[t]); });
+    fn(R[0]);
+    for (auto &th : pool) th.join();
+  };
+  const unsigned char *ubuf = (const unsigned char *)buf;
+  parallel([&](TokRange &r) { tokenize_range(*v, ubuf, off, r, len_out, chars_out); });
+  int64_t total = 0;
+  for (TokRange &r : R) {
+    r.out_off = total;
+    total += (int64_t)r.tok.size();
+  }
+  if (total > cap) return BIMINE_E_LIMIT;  // vocabulary unchanged
+  for (TokRange &r : R) {  // serial: first-occurrence id order
+    r.resolved.resize(r.miss.size());
+    for (size_t i = 0; i < r.miss.size(); ++i)
+      r.resolved[i] = v->get(r.miss[i].hash, r.words.data() + r.miss[i].off, r.miss[i].len);
+  }
+  parallel([&](TokRange &r) { finish_range(r, len_out, uniq_out, tokens); });
+  *n_tokens = total;
   return BIMINE_OK;
 }
 

@@ -152,8 +152,9 @@ def score_device(dd: DeviceDictionary, model_vec: np.ndarray, db: DeviceBatch, s
 
 def mine_device(dd: DeviceDictionary, model_vec: np.ndarray, db: DeviceBatch, sim, gap: float, threshold: float,
                 mismatch: float, bonus: float, out: dict | None = None, stream=None, events=None) -> dict:
-    """The fused mining step on a device batch (score kernel with the NW
-    tail for one-CTA pairs, NW launch for the rest) + order-preserving
+    """The mining step on a device batch (bimine_mine_batch: score kernel,
+    then the NW + traceback + filter launch; the NW runs in the score
+    kernel's tail only with BIMINE_FUSE_NW=1) + order-preserving
     compaction; returns device tensors (counts, base, compact, total).
     `events` (3 CUDA events) bracket the mining call and the compaction."""
     torch = _torch()

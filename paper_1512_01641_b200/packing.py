@@ -332,35 +332,36 @@ class BatchBuilder:
         pairs = [(list(src), list(tgt)) for src, tgt in pairs]
         flat = [x for src, tgt in pairs for x in src + tgt]
         tokens, lens, uniq, chars = self.vocab.tokenize(flat)
-        tstart = np.zeros(len(flat) + 1, dtype=np.int64)
-        np.cumsum(lens, out=tstart[1:])
-        out, k = [], 0
-        keep_tok, keep_sent = [], []
-        for src, tgt in pairs:
-            ns, nt = len(src), len(tgt)
-            span = range(k, k + ns + nt)
-            k += ns + nt
-            if not src or not tgt:
-                out.append("both sentence sequences must be non-empty")
+        P = len(pairs)
+        ns = np.fromiter((len(src) for src, _ in pairs), dtype=np.int64, count=P)
+        nt = np.fromiter((len(tgt) for _, tgt in pairs), dtype=np.int64, count=P)
+        start = np.zeros(P + 1, dtype=np.int64)
+        np.cumsum(ns + nt, out=start[1:])
+        zero = np.zeros(len(flat) + 1, dtype=np.int64)
+        np.cumsum(lens == 0, out=zero[1:])
+        ok = (ns > 0) & (nt > 0) & (zero[start[1:]] == zero[start[:-1]])
+        out: list = [None] * P
+        for k in np.flatnonzero(~ok).tolist():  # the reference's messages
+            if not ns[k] or not nt[k]:
+                out[k] = "both sentence sequences must be non-empty"
                 continue
-            bad = next((x for x in span if lens[x] == 0), None)
-            if bad is not None:
-                side, index = ("source", bad - span.start) if bad - span.start < ns else ("target", bad - span.start - ns)
-                out.append(f"{side} sentence {index}: untokenizable sentence: {flat[bad]!r}")
-                continue
-            first = len(self.sent_len)
-            keep_sent.append(span)
-            keep_tok.append((tstart[span.start], tstart[span.stop]))
-            self.sent_len.extend(lens[span.start : span.stop].tolist())
-            self.sent_uniq.extend(uniq[span.start : span.stop].tolist())
-            self.sent_chars.extend(chars[span.start : span.stop].tolist())
-            self.pair_src.append(first)
-            self.pair_n.append(ns)
-            self.pair_tgt.append(first + ns)
-            self.pair_m.append(nt)
-            out.append(len(self.pair_n) - 1)
-        for a, b in keep_tok:
-            self.tok_chunks.append(tokens[a:b])
+            bad = int(start[k]) + int(np.flatnonzero(lens[start[k] : start[k + 1]] == 0)[0])
+            side, index = ("source", bad - start[k]) if bad - start[k] < ns[k] else ("target", bad - start[k] - ns[k])
+            out[k] = f"{side} sentence {index}: untokenizable sentence: {flat[bad]!r}"
+        keep = np.flatnonzero(ok)
+        first = len(self.sent_len) + np.concatenate(([0], np.cumsum((ns + nt)[keep])[:-1])) if keep.size else keep
+        for k, b, f, n_, m_ in zip(keep.tolist(), range(len(self.pair_n), len(self.pair_n) + keep.size),
+                                   first.tolist(), ns[keep].tolist(), nt[keep].tolist()):
+            out[k] = b
+            self.pair_src.append(f)
+            self.pair_n.append(n_)
+            self.pair_tgt.append(f + n_)
+            self.pair_m.append(m_)
+        sent_keep = np.repeat(ok, ns + nt)
+        self.sent_len.extend(lens[sent_keep].tolist())
+        self.sent_uniq.extend(uniq[sent_keep].tolist())
+        self.sent_chars.extend(chars[sent_keep].tolist())
+        self.tok_chunks.append(tokens if sent_keep.all() else tokens[np.repeat(sent_keep, lens)])
         return out
 
     def build(self) -> PackedBatch:

@@ -207,6 +207,44 @@ def test_native_tokenizer_matches_python_rules():
     assert pos == tokens.shape[0]
 
 
+def test_native_tokenizer_threaded_batch():
+    """A batch past the multi-thread split (>= 512 KB): same tokens as the
+    Python rules, long words sharing their first 16 bytes kept apart, and
+    ids assigned in first-occurrence order as by one serial pass."""
+    import random
+
+    from paper_1512_01641_b200.packing import NativeVocabulary
+
+    _native_vocab()
+    rng = random.Random(11)
+    words = [f"w{k}" for k in range(5000)] + [f"internationalisation{k}x" for k in range(300)]
+    words += ["".join(rng.choice("abcdefghijklmnopqrstuvwxyz") for _ in range(rng.randint(1, 30))) for _ in range(3000)]
+
+    def sentence():
+        out = []
+        for _ in range(rng.randint(1, 30)):
+            w = rng.choice(words)
+            w = w.upper() if rng.random() < 0.1 else w
+            out.append(rng.choice(["", "(", '"']) + w + rng.choice(["", ",", ".", "!?"]))
+        return rng.choice([" ", "  ", "\t"]).join(out)
+
+    sents = [sentence() for _ in range(9000)]
+    assert sum(map(len, sents)) > 1 << 20
+    v = NativeVocabulary()
+    tokens, lens, uniq, chars = v.tokenize(sents)
+    first = list(dict.fromkeys(tokens.tolist()))
+    assert first == list(range(len(first))) == list(range(len(v)))
+    sents[100:100] = ["Żółw INTERNATIONALISATION7X w1", "ǅ w2."]  # Python-rule sentences in the same batch
+    tokens, lens, uniq, chars = v.tokenize(sents)
+    pos = 0
+    for s, L, U, C in zip(sents, lens.tolist(), uniq.tolist(), chars.tolist()):
+        want = tokenize(s)
+        assert [v.get(w) for w in want] == tokens[pos : pos + L].tolist(), s
+        assert U == len(set(want)) and C == len(s)
+        pos += L
+    assert pos == tokens.shape[0]
+
+
 def test_native_and_python_builders_agree():
     from paper_1512_01641_b200.packing import BatchBuilder, Vocabulary
 
