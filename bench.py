@@ -572,7 +572,7 @@ def main():
             "h2d_bytes_per_step": int(pb.nbytes()),
             "d2h_bytes_per_step": int(4 * batch.n_pairs + 8 + 16 * int(counts.sum())),
             "steps": e2e_steps,
-            "path": "bimine_mine_host (C ABI): pinned host inputs, results copied into reused host output buffers",
+            "path": "bimine_mine_host (C ABI): pinned host inputs, results copied into reused page-locked host output buffers",
         }
 
     if world > 1:

@@ -69,7 +69,7 @@ def _ptr(a: np.ndarray, t):
 
 def build() -> str:
     """Compile the oracle (and oracle/_ref when /root/reference exists)."""
-    subprocess.run(["make", "-s", "-C", HERE], check=True)
+    subprocess.run(["make", "-s", "-C", HERE], check=True, stdout=sys.stderr)  # keep stdout for JSON lines
     return LIB_PATH
 
 

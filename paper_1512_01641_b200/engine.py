@@ -206,28 +206,40 @@ def nw_device(db: DeviceBatch, sim, gap: float, threshold: float, mismatch: floa
 # host-buffer entry points
 # ---------------------------------------------------------------------------
 
+def _pinned_empty(n: int, dtype) -> np.ndarray:
+    """Page-locked host array (torch's caching host allocator owns it)."""
+    torch = _torch()
+    dt = np.dtype(dtype)
+    return torch.empty(n * dt.itemsize, dtype=torch.uint8, pin_memory=True).numpy().view(dt)
+
+
 def mine_host(dd: DeviceDictionary, model_vec: np.ndarray, batch: PackedBatch, gap: float, threshold: float,
               mismatch: float, bonus: float, want_sim: bool = False, stream=None, out=None):
     """bimine_mine_host: H2D, score, NW, filter, compact, D2H.  Returns
     (counts[P], matches structured array, sim or None).
 
     `out`: optional dict reused across calls (a streaming caller's output
-    buffers: counts and matches land in the same host memory every call, so
-    the copy-out does not first-touch fresh pages); the returned arrays are
-    views into it, valid until the next call with the same `out`."""
+    buffers, in page-locked memory: the copy-out runs at full link speed and
+    does not first-touch fresh pages); the returned arrays are views into it,
+    valid until the next call with the same `out`."""
     L = N.load()
     torch = _torch()
     P = batch.n_pairs
-    cap = int(batch.match_capacity()[-1])
+    cap = int(np.minimum(batch.pair_n, batch.pair_m).sum(dtype=np.int64))
     if out is not None and out.get("counts") is not None and out["counts"].size >= max(P, 1) \
             and out["matches"].size >= max(cap, 1):
-        counts, matches = out["counts"], out["matches"]
+        counts, matches, total = out["counts"], out["matches"], out["total"]
+    elif out is not None:
+        grow = max(P, 1), max(cap, 1)
+        if out.get("counts") is not None:  # amortise regrowth
+            grow = max(grow[0], out["counts"].size * 5 // 4), max(grow[1], out["matches"].size * 5 // 4)
+        out["counts"] = counts = _pinned_empty(grow[0], np.int32)
+        out["matches"] = matches = _pinned_empty(grow[1], N.MATCH_DTYPE)
+        out["total"] = total = _pinned_empty(1, np.int64)
     else:
         counts = np.empty(max(P, 1), dtype=np.int32)  # filled for every pair
         matches = np.empty(max(cap, 1), dtype=N.MATCH_DTYPE)  # the first `total` are filled
-        if out is not None:
-            out["counts"], out["matches"] = counts, matches
-    total = np.zeros(1, dtype=np.int64)
+        total = np.zeros(1, dtype=np.int64)
     sim = np.empty(max(batch.n_cells, 1), dtype=np.float64) if want_sim else None
     cb = N.batch_struct_host(batch)
     mv = np.ascontiguousarray(model_vec, dtype=np.float64)
