@@ -917,7 +917,6 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
   const int64_t pair = q / A.n_settings;
   const int setting = (int)(q % A.n_settings);
   const int N = A.pair_n[pair], M = A.pair_m[pair];
-  const double *__restrict__ sim = A.sim + A.sim_off[pair];
   const double gap = A.gap_per_problem ? A.gap[q] : A.gap[setting];
   const double ng = -gap, mismatch = A.mismatch, span = fsub(A.bonus, A.mismatch);
   const int G = (N + 31) >> 5, G8 = nw_groups(M);
