@@ -90,6 +90,7 @@ struct PairSmem {
   int32_t *tgt_occ0;   // [65] chunk-local occurrence offsets
   uint8_t *src_order;  // [64] source sentences, longest first (phase D claim order)
   int32_t *o_n;        // [warps][32] translations found per occurrence
+  uint32_t *seen;      // [warps][1024 / 32] chunk tokens already met in the warp's source sentence
   int32_t *misc;       // [8]: 0 distinct count, 1 chunk end, 2 D work counter, 3 C work counter
   int16_t *dense;      // [slots]
   int16_t *tgt_d;      // [cap_t]
@@ -125,6 +126,7 @@ __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_
   t.dense = (int16_t *)take(slots * 2, 4);
   t.tgt_d = (int16_t *)take((size_t)cap_t * 2, 4);
   t.o_n = (int32_t *)take(W * 4, 4);
+  t.seen = (uint32_t *)take((size_t)kPairWarps * 32 * 4, 16);
   t.overlay_bytes = o;
   // live until the end
   t.exp_tab = (uint64_t *)take(256 * 8, 16);
@@ -379,6 +381,7 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
       uint64_t *oany = S.o_any + warp * 32;
       int32_t *on = S.o_n + warp * 32;
       uint64_t *cm = S.c_m + warp * kSegItems;
+      uint32_t *seen = S.seen + warp * 32;
       double *cp = S.c_p + warp * kSegItems;
       const int jlo = lane, jhi = lane + 32;
       const unsigned lt_mask = (1u << lane) - 1u;
@@ -408,15 +411,16 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
         rl_w = (int)(row_ptr[s_w + 1] - e0_w);
       }
       while (i < N) {
-        const int64_t off = S.src_off[i];
         const int L = S.src_len[i];
         const unsigned long long ibit = 1ull << i;
         int cov_lo = 0, cov_hi = 0, sh_lo = 0, sh_hi = 0;
         double sum_lo = 0.0, sum_hi = 0.0;
+        seen[lane] = 0u;  // (cap_u = 1024 dense ids: 32 words)
+        __syncwarp();
         for (int seg = 0; seg < L;) {
           const int k = seg + lane;
           const bool valid = k < L;
-          const int32_t s = s_w;  // tokens[off + k] or -1
+          const int32_t s = s_w;  // token k of sentence i, or -1
           const int64_t e0 = e0_w;
           const int rl = rl_w;
           // segment: the longest prefix of occurrences whose rows total
@@ -435,17 +439,15 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           // next window: the rest of this sentence, else the next sentence
           const bool more = seg + cnt < L;
           const int32_t tok_nx = more ? load_tok(i, seg + cnt) : load_tok(i_nxt, 0);
-          // shared tokens: first occurrence of a source token that is a chunk token
+          // shared tokens: first occurrence of a source token that is a chunk
+          // token (one lane of each distinct dense id claims its seen bit)
           const int ds = in_seg ? pk_find_f(S.bloom, S.keys, S.dense, hbits, s) : -1;
-          const unsigned peers = __match_any_sync(kFull, in_seg ? s : -1);
-          bool first = (__ffs(peers) - 1) == lane;
-          if (ds >= 0 && first && seg > 0)
-            for (int kk = 0; kk < seg; ++kk)
-              if (tokens[off + kk] == s) {
-                first = false;
-                break;
-              }
-          const uint64_t shm = (ds >= 0 && first) ? S.colmask[ds] : 0ull;
+          bool first = false;
+          if (ds >= 0) {
+            const uint32_t bit = 1u << (ds & 31);
+            first = !(atomicOr(&seen[ds >> 5], bit) & bit);
+          }
+          const uint64_t shm = first ? S.colmask[ds] : 0ull;
           if (__any_sync(kFull, shm != 0ull)) {
             sh_lo += __popc(transpose32((uint32_t)shm, lane));
             sh_hi += __popc(transpose32((uint32_t)(shm >> 32), lane));
@@ -560,7 +562,6 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           while (rel) {
             const int kk = __ffs(rel) - 1;
             rel &= rel - 1u;
-            const uint64_t a = __shfl_sync(kFull, my_any, kk);
             const int n = __shfl_sync(kFull, my_n, kk);
             const uint64_t m0 = __shfl_sync(kFull, my_m0, kk);
             const double p0 = __shfl_sync(kFull, my_p0, kk);
@@ -575,10 +576,12 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
                 if (((uint32_t)(m >> 32) & lbit) && pr > bh) bh = pr;
               }
             }
+            // every dictionary probability is > 0, so a translation of this
+            // occurrence is in sentence j exactly when its best there is > 0
             sum_lo = fadd(sum_lo, bl);
             sum_hi = fadd(sum_hi, bh);
-            cov_lo += ((uint32_t)a & lbit) ? 1 : 0;
-            cov_hi += ((uint32_t)(a >> 32) & lbit) ? 1 : 0;
+            cov_lo += bl > 0.0 ? 1 : 0;
+            cov_hi += bh > 0.0 ? 1 : 0;
           }
           __syncwarp();
           seg += cnt;
