@@ -3,24 +3,25 @@
 // build_score_matrix (align.py:102-129) for pairs with N, M <= 64 and
 // sentences of <= 255 tokens (all C2/C4/C5 pairs); larger pairs (C1, C3)
 // run the same kernel over 64x64 sentence tiles, (pair, i0, j0) per CTA.
-// 8 warps; all per-pair state lives in shared memory and every count is
-// produced 32 cells at a time by bit-matrix transposes:
+// 8 warps, 4 CTAs per SM; the per-pair tables live in shared memory, the
+// per-cell counters in global scratch (L2-resident while the CTA works).
 //
 //  A  target hash: every target token of the chunk -> dense id d;
 //     colmask[d] = 64-bit set of target sentences containing d.
-//  D  warp per source sentence i, lanes = 32 occurrences at a time, in
-//     order.  Lane k walks its token's dictionary row (p > 0 entries
-//     only, CSR) against the hash (behind a Bloom prefilter): anyhit_k =
-//     OR of colmask over its translations; up to six (colmask, p) are kept
-//     sorted by p; reachcol[d] |= bit i (reachable_targets,
-//     classifier.py:54-59).  A 32x32 bit
-//     transpose turns the anyhit rows into, for lane j, the set of
-//     occurrences with a translation in target sentence j; popc adds
-//     `covered`, and walking the set bits in ascending order adds the
-//     max probability to the running sum -- the exact sequential sum of
-//     classifier.py:75-82.  Shared tokens (classifier.py:94) are counted
-//     the same way from the first occurrences of source tokens that are
-//     themselves target tokens.
+//  D  warp per source sentence i (claimed longest first); lane j owns
+//     target sentences j and j + 32.  The sentence's occurrences are cut
+//     into segments of <= 32 occurrences whose dictionary rows (p > 0
+//     entries, CSR) total <= 64 entries.  The warp walks a segment's
+//     entries flattened, 32 per step, against the hash (behind a Bloom
+//     prefilter); each hit (colmask, p) is appended to the warp's
+//     candidate list in entry order and sets reachcol[d] |= bit i
+//     (reachable_targets, classifier.py:54-59).  Then, occurrence by
+//     occurrence in order, lane j takes the max p over the occurrence's
+//     candidates present in sentence j and adds it to the running sum --
+//     the exact sequential sum of classifier.py:75-82 -- and counts it in
+//     `covered` when > 0 (all p > 0).  Shared tokens (classifier.py:94):
+//     the first occurrence of each distinct chunk token (a per-warp seen
+//     bitmap) adds its colmask bits.
 //  C  warp per target sentence j, lanes = occurrences: transposing the
 //     reachcol rows gives covered_target(i, j) by popc
 //     (classifier.py:88-92), multiplicities included.
@@ -79,7 +80,6 @@ struct PairSmem {
   uint64_t *exp_tab;   // [256]
   uint64_t *colmask;   // [cap_u]
   uint64_t *reachcol;  // [cap_u]
-  uint64_t *o_any;     // [warps][32] per occurrence: OR of its translations' colmasks
   uint64_t *c_m;       // [warps][kSegItems] in-chunk translations: colmask
   double *c_p;         // [warps][kSegItems]                        probability
   int64_t *src_off, *tgt_off;  // [64]
@@ -118,7 +118,6 @@ __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_
   // region reused by the fused NW once the score phases are done
   t.colmask = (uint64_t *)take((size_t)cap_u * 8, 16);
   t.reachcol = (uint64_t *)take((size_t)cap_u * 8, 16);
-  t.o_any = (uint64_t *)take(W * 8, 16);
   t.c_m = (uint64_t *)take((size_t)kPairWarps * kSegItems * 8, 16);
   t.c_p = (double *)take((size_t)kPairWarps * kSegItems * 8, 16);
   t.bloom = (uint32_t *)take(((size_t)1 << kBloomBits) / 8, 16);
@@ -378,7 +377,6 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
     __syncthreads();
     // ---- D: source side, warps take sentences dynamically
     {
-      uint64_t *oany = S.o_any + warp * 32;
       int32_t *on = S.o_n + warp * 32;
       uint64_t *cm = S.c_m + warp * kSegItems;
       uint32_t *seen = S.seen + warp * 32;
@@ -448,9 +446,10 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
             first = !(atomicOr(&seen[ds >> 5], bit) & bit);
           }
           const uint64_t shm = first ? S.colmask[ds] : 0ull;
-          if (__any_sync(kFull, shm != 0ull)) {
-            sh_lo += __popc(transpose32((uint32_t)shm, lane));
-            sh_hi += __popc(transpose32((uint32_t)(shm >> 32), lane));
+          for (unsigned sb = __ballot_sync(kFull, shm != 0ull); sb; sb &= sb - 1u) {
+            const uint64_t mm = __shfl_sync(kFull, shm, __ffs(sb) - 1);
+            sh_lo += (int)(((uint32_t)mm >> lane) & 1u);
+            sh_hi += (int)(((uint32_t)(mm >> 32) >> lane) & 1u);
           }
           const int rl0 = __shfl_sync(kFull, rl, 0);
           if (rl0 > kSegItems) {
@@ -493,7 +492,6 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
             seg += 1;  // cnt == 1 here
             continue;
           }
-          oany[lane] = 0ull;
           on[lane] = 0;
           __syncwarp();
           // all dictionary entries of the segment, 32 at a time, in order
@@ -526,7 +524,6 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
               cm[pos] = m;
               cp[pos] = pr;
               or64(&S.reachcol[d], ibit);
-              or64(&oany[owner], m);
               atomicAdd(&on[owner], 1);
             }
             ncand += __popc(bal);
@@ -544,10 +541,10 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           // translations present in sentence j, added to the running sum
           // (adding +0.0 when absent leaves the non-negative sum unchanged)
           const uint32_t lbit = 1u << lane;  // bit of target jlo in the low word, jhi in the high word
-          // per-occurrence records in registers of lane k: anyhit, first
-          // candidate, candidate range; only occurrences with a translation
-          // in the chunk are visited (in order)
-          const uint64_t my_any = in_seg ? oany[lane] : 0ull;
+          // per-occurrence record in lane k: its candidates [cs, cs + n)
+          // (n > 0 exactly when a translation is in the chunk: every chunk
+          // token's colmask is nonzero); only those occurrences are visited,
+          // in order
           const int my_n = in_seg ? on[lane] : 0;
           int my_cs = my_n;
 #pragma unroll
@@ -555,26 +552,22 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
             const int y = __shfl_up_sync(kFull, my_cs, o);
             if (lane >= o) my_cs += y;
           }
-          my_cs -= my_n;  // exclusive prefix: first candidate of occurrence `lane`
-          const uint64_t my_m0 = my_n ? cm[my_cs] : 0ull;
-          const double my_p0 = my_n ? cp[my_cs] : 0.0;
-          unsigned rel = __ballot_sync(kFull, my_any != 0ull);
+          const int my_rec = (my_cs - my_n) | (my_n << 8);  // exclusive prefix | count (both <= kSegItems)
+          unsigned rel = __ballot_sync(kFull, my_n > 0);
           while (rel) {
             const int kk = __ffs(rel) - 1;
             rel &= rel - 1u;
-            const int n = __shfl_sync(kFull, my_n, kk);
-            const uint64_t m0 = __shfl_sync(kFull, my_m0, kk);
-            const double p0 = __shfl_sync(kFull, my_p0, kk);
+            const int rec = __shfl_sync(kFull, my_rec, kk);
+            const int cs = rec & 0xff, ce = cs + (rec >> 8);
+            const uint64_t m0 = cm[cs];  // same address in every lane: broadcast
+            const double p0 = cp[cs];
             double bl = ((uint32_t)m0 & lbit) ? p0 : 0.0;
             double bh = ((uint32_t)(m0 >> 32) & lbit) ? p0 : 0.0;
-            if (n > 1) {
-              const int cs = __shfl_sync(kFull, my_cs, kk);
-              for (int c = cs + 1; c < cs + n; ++c) {
-                const uint64_t m = cm[c];
-                const double pr = cp[c];
-                if (((uint32_t)m & lbit) && pr > bl) bl = pr;
-                if (((uint32_t)(m >> 32) & lbit) && pr > bh) bh = pr;
-              }
+            for (int c = cs + 1; c < ce; ++c) {
+              const uint64_t m = cm[c];
+              const double pr = cp[c];
+              if (((uint32_t)m & lbit) && pr > bl) bl = pr;
+              if (((uint32_t)(m >> 32) & lbit) && pr > bh) bh = pr;
             }
             // every dictionary probability is > 0, so a translation of this
             // occurrence is in sentence j exactly when its best there is > 0
