@@ -434,6 +434,37 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           const bool in_seg = lane < cnt;
           const int items = min(kSegItems, __shfl_sync(kFull, x, cnt - 1));
           const int ofs = x - rl;  // exclusive prefix: first item of this occurrence
+          // the segment's dictionary entries (<= 2 steps of 32, in order):
+          // owners found and loads issued now, so their L2 latency overlaps
+          // the shared-token work below
+          static_assert(kSegItems == 64, "the walk below is two steps");
+          int w_owner[2];
+          int32_t w_tgt[2];
+          double w_p[2];
+#pragma unroll
+          for (int st = 0; st < 2; ++st) {
+            w_owner[st] = 0;
+            w_tgt[st] = -1;
+            w_p[st] = 0.0;
+            if (st * 32 < items) {  // warp-uniform
+              const int it = st * 32 + lane;
+              int owner = 0;  // last segment lane whose first item <= it
+#pragma unroll
+              for (int step = 16; step >= 1; step >>= 1) {
+                const int cand = owner + step;
+                const int v = __shfl_sync(kFull, ofs, cand & 31);
+                if (cand < cnt && v <= it) owner = cand;
+              }
+              const int64_t oe0 = __shfl_sync(kFull, e0, owner);
+              const int oofs = __shfl_sync(kFull, ofs, owner);
+              w_owner[st] = owner;
+              if (it < items) {
+                const int64_t e = oe0 + (it - oofs);
+                w_tgt[st] = dtgt[e];
+                w_p[st] = dprob[e];
+              }
+            }
+          }
           // next window: the rest of this sentence, else the next sentence
           const bool more = seg + cnt < L;
           const int32_t tok_nx = more ? load_tok(i, seg + cnt) : load_tok(i_nxt, 0);
@@ -496,26 +527,12 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           __syncwarp();
           // all dictionary entries of the segment, 32 at a time, in order
           int ncand = 0;
-          for (int base = 0; base < items; base += 32) {
-            const int it = base + lane;
-            const bool live = it < items;
-            int owner = 0;  // last segment lane whose first item <= it
 #pragma unroll
-            for (int step = 16; step >= 1; step >>= 1) {
-              const int cand = owner + step;
-              const int v = __shfl_sync(kFull, ofs, cand & 31);
-              if (cand < cnt && v <= it) owner = cand;
-            }
-            const int64_t oe0 = __shfl_sync(kFull, e0, owner);
-            const int oofs = __shfl_sync(kFull, ofs, owner);
-            int d = -1;
-            double pr = 0.0;
-            if (live) {
-              const int64_t e = oe0 + (it - oofs);
-              const int32_t t = dtgt[e];
-              pr = dprob[e];  // issued with the id load: no second round trip for hits
-              d = pk_find_f(S.bloom, S.keys, S.dense, hbits, t);
-            }
+          for (int st = 0; st < 2; ++st) {
+            if (st * 32 >= items) break;  // warp-uniform
+            const int owner = w_owner[st];
+            const double pr = w_p[st];  // loaded with the id: no second round trip for hits
+            const int d = w_tgt[st] >= 0 ? pk_find_f(S.bloom, S.keys, S.dense, hbits, w_tgt[st]) : -1;
             const bool pres = d >= 0;
             const unsigned bal = __ballot_sync(kFull, pres);
             if (pres) {
