@@ -89,7 +89,7 @@ struct PairSmem {
   int32_t *tgt_len, *tgt_uniq, *tgt_chars;  // [64]
   int32_t *tgt_occ0;   // [65] chunk-local occurrence offsets
   uint8_t *src_order;  // [64] source sentences, longest first (phase D claim order)
-  int32_t *o_n;        // [warps][32] translations found per occurrence
+  uint8_t *c_o;        // [warps][kSegItems]                        owning occurrence
   uint32_t *seen;      // [warps][1024 / 32] chunk tokens already met in the warp's source sentence
   int32_t *misc;       // [8]: 0 distinct count, 1 chunk end, 2 D work counter, 3 C work counter
   int16_t *dense;      // [slots]
@@ -113,7 +113,6 @@ __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_
     return p;
   };
   const size_t slots = (size_t)1 << hash_bits;
-  const size_t W = kPairWarps * 32;
   PairSmem t;
   // region reused by the fused NW once the score phases are done
   t.colmask = (uint64_t *)take((size_t)cap_u * 8, 16);
@@ -124,7 +123,7 @@ __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_
   t.keys = (int32_t *)take(slots * 4, 16);
   t.dense = (int16_t *)take(slots * 2, 4);
   t.tgt_d = (int16_t *)take((size_t)cap_t * 2, 4);
-  t.o_n = (int32_t *)take(W * 4, 4);
+  t.c_o = (uint8_t *)take((size_t)kPairWarps * kSegItems, 4);
   t.seen = (uint32_t *)take((size_t)kPairWarps * 32 * 4, 16);
   t.overlay_bytes = o;
   // live until the end
@@ -377,7 +376,7 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
     __syncthreads();
     // ---- D: source side, warps take sentences dynamically
     {
-      int32_t *on = S.o_n + warp * 32;
+      uint8_t *co = S.c_o + warp * kSegItems;
       uint64_t *cm = S.c_m + warp * kSegItems;
       uint32_t *seen = S.seen + warp * 32;
       double *cp = S.c_p + warp * kSegItems;
@@ -523,8 +522,6 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
             seg += 1;  // cnt == 1 here
             continue;
           }
-          on[lane] = 0;
-          __syncwarp();
           // all dictionary entries of the segment, 32 at a time, in order
           int ncand = 0;
 #pragma unroll
@@ -541,7 +538,7 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
               cm[pos] = m;
               cp[pos] = pr;
               or64(&S.reachcol[d], ibit);
-              atomicAdd(&on[owner], 1);
+              co[pos] = (uint8_t)owner;
             }
             ncand += __popc(bal);
           }
@@ -558,36 +555,33 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           // translations present in sentence j, added to the running sum
           // (adding +0.0 when absent leaves the non-negative sum unchanged)
           const uint32_t lbit = 1u << lane;  // bit of target jlo in the low word, jhi in the high word
-          // per-occurrence record in lane k: its candidates [cs, cs + n)
-          // (n > 0 exactly when a translation is in the chunk: every chunk
-          // token's colmask is nonzero); only those occurrences are visited,
-          // in order
-          const int my_n = in_seg ? on[lane] : 0;
-          int my_cs = my_n;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(kFull, my_cs, o);
-            if (lane >= o) my_cs += y;
-          }
-          const int my_rec = (my_cs - my_n) | (my_n << 8);  // exclusive prefix | count (both <= kSegItems)
-          unsigned rel = __ballot_sync(kFull, my_n > 0);
-          while (rel) {
-            const int kk = __ffs(rel) - 1;
-            rel &= rel - 1u;
-            const int rec = __shfl_sync(kFull, my_rec, kk);
-            const int cs = rec & 0xff, ce = cs + (rec >> 8);
-            const uint64_t m0 = cm[cs];  // same address in every lane: broadcast
-            const double p0 = cp[cs];
-            double bl = ((uint32_t)m0 & lbit) ? p0 : 0.0;
-            double bh = ((uint32_t)(m0 >> 32) & lbit) ? p0 : 0.0;
-            for (int c = cs + 1; c < ce; ++c) {
-              const uint64_t m = cm[c];
-              const double pr = cp[c];
-              if (((uint32_t)m & lbit) && pr > bl) bl = pr;
-              if (((uint32_t)(m >> 32) & lbit) && pr > bh) bh = pr;
+          // candidate-major: the candidates are in entry order, so each
+          // occurrence's are contiguous and the occurrences come in order;
+          // an occurrence's best is added when its last candidate has been
+          // seen (occurrences without a candidate would add +0.0)
+          int cur = -1;
+          double bl = 0.0, bh = 0.0;
+          for (int c = 0; c < ncand; ++c) {
+            const int o = co[c];  // same address in every lane: broadcast
+            const uint64_t m = cm[c];
+            const double pr = cp[c];
+            if (o != cur) {  // warp-uniform
+              if (cur >= 0) {
+                // every dictionary probability is > 0, so a translation of
+                // the occurrence is in sentence j exactly when its best > 0
+                sum_lo = fadd(sum_lo, bl);
+                sum_hi = fadd(sum_hi, bh);
+                cov_lo += bl > 0.0 ? 1 : 0;
+                cov_hi += bh > 0.0 ? 1 : 0;
+              }
+              cur = o;
+              bl = 0.0;
+              bh = 0.0;
             }
-            // every dictionary probability is > 0, so a translation of this
-            // occurrence is in sentence j exactly when its best there is > 0
+            if (((uint32_t)m & lbit) && pr > bl) bl = pr;
+            if (((uint32_t)(m >> 32) & lbit) && pr > bh) bh = pr;
+          }
+          if (cur >= 0) {
             sum_lo = fadd(sum_lo, bl);
             sum_hi = fadd(sum_hi, bh);
             cov_lo += bl > 0.0 ? 1 : 0;
