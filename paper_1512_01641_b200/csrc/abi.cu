@@ -7,6 +7,9 @@
 // explicit __fma_rn where the host libm fuses).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_scan.cuh>
+#include <thrust/iterator/transform_iterator.h>
+
 #include <algorithm>
 #include <chrono>
 #include <array>
@@ -74,6 +77,17 @@ cudaStream_t copy_stream() {
   cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
   g_copy_streams[dev] = s;
   return s;
+}
+
+// sentence offsets rebuilt on the device: exclusive sum of the lengths,
+// accumulated in int64
+struct LenToI64 {
+  __host__ __device__ int64_t operator()(int32_t x) const { return (int64_t)x; }
+};
+cudaError_t offsets_from_lengths(const int32_t *len, int64_t *off, int64_t n, void *tmp, size_t *tmp_bytes,
+                                 cudaStream_t st) {
+  return cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, thrust::make_transform_iterator(len, LenToI64()), off, n,
+                                       st);
 }
 
 // two doubles into device memory without a host copy (a pageable
@@ -911,15 +925,23 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
                o_slots = carve(sizeof(bimine_match) * cap), o_counts = carve(4 * P), o_base = carve(8 * P),
                o_comp = carve(sizeof(bimine_match) * cap), o_total = carve(8),
                o_work = carve(8 * std::max<int64_t>(work_bound, 1)), o_need = carve(4 * P), o_ready = carve(4);
+  // sent_tok_off is not uploaded: the copy stream rebuilds it from sent_len
+  // (the usual packed layout); the analysis threads check that the caller's
+  // offsets are exactly that, else they are uploaded on `st` before scoring
+  size_t scan_bytes = 0;
+  BIMINE_CUDA(offsets_from_lengths(nullptr, nullptr, S, nullptr, &scan_bytes, st));
+  const size_t o_scan = carve(std::max<size_t>(scan_bytes, 1));
   char *arena = nullptr;
   BIMINE_CUDA(cudaMallocAsync((void **)&arena, off, st));
   cudaStream_t cs = copy_stream();
-  cudaEvent_t ev_start = nullptr, ev_all = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_all = nullptr, ev_scan = nullptr;
   BIMINE_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
   BIMINE_CUDA(cudaEventCreateWithFlags(&ev_all, cudaEventDisableTiming));
+  BIMINE_CUDA(cudaEventCreateWithFlags(&ev_scan, cudaEventDisableTiming));
   auto cleanup = [&]() {
     cudaEventDestroy(ev_start);
     cudaEventDestroy(ev_all);
+    cudaEventDestroy(ev_scan);
   };
 #ifdef BIMINE_E2E_PROFILE
   cudaEventRecord(pe[0], st);
@@ -938,10 +960,13 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     H2D(o_pm, h->pair_m, 4 * P);
     H2D(o_psim, h->pair_sim_off, 8 * P);
     H2D(o_outoff, out_off, 8 * P);
-    H2D(o_soff, h->sent_tok_off, 8 * S);
     H2D(o_slen, h->sent_len, 4 * S);
     H2D(o_suniq, h->sent_uniq, 4 * S);
     H2D(o_schar, h->sent_chars, 4 * S);
+    if (e == cudaSuccess)
+      e = offsets_from_lengths((const int32_t *)(arena + o_slen), (int64_t *)(arena + o_soff), S, arena + o_scan,
+                               &scan_bytes, cs);
+    e = e ? e : cudaEventRecord(ev_scan, cs);
     H2D(o_ready, &ready_vals[0], 4);  // 1: pairs and sentences are in place
     for (int j = 0; j < nt; ++j) {
       H2D(o_tok + 4 * tcut[j], h->tokens + tcut[j], 4 * (tcut[j + 1] - tcut[j]));
@@ -968,10 +993,19 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     std::string err;
     bimine_plan plan;
     std::vector<int64_t> work;
+    bool packed = true;  // sentences [S k / nc, S (k+1) / nc) are at the rebuilt offsets
   };
   std::vector<ChunkInfo> ci(nc);
   auto analyse = [&](int k) {
     ChunkInfo &c = ci[k];
+    {
+      const int64_t s0 = S * k / nc, s1 = S * (k + 1) / nc;
+      const int64_t *so = h->sent_tok_off;
+      const int32_t *sl = h->sent_len;
+      bool ok = s0 > 0 || S == 0 || so[0] == 0;
+      for (int64_t x = s0; ok && x + 1 < s1 + (s1 < S ? 1 : 0); ++x) ok = so[x + 1] == so[x] + sl[x];
+      c.packed = ok;
+    }
     const int64_t p0 = cut[k], p1 = cut[k + 1];
     int64_t wcap = p1 - p0;
     for (int64_t p = p0; p < p1; ++p) {
@@ -1025,6 +1059,12 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   }
   for (int k = 0; k < nc; ++k)
     if (ci[k].rc != BIMINE_OK) return abort_with(ci[k].rc, ci[k].err);
+  bool packed = true;
+  for (int k = 0; k < nc; ++k) packed = packed && ci[k].packed;
+  e = cudaStreamWaitEvent(st, ev_scan, 0);
+  if (!packed && e == cudaSuccess)  // the caller's own layout: overwrite the rebuilt offsets
+    e = cudaMemcpyAsync(arena + o_soff, h->sent_tok_off, 8 * S, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return abort_with(BIMINE_E_CUDA, std::string("bimine_mine_host: ") + cudaGetErrorString(e));
 #ifdef BIMINE_E2E_PROFILE
   h_an = hclock() - h0;
 #endif

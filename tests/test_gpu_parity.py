@@ -443,6 +443,42 @@ def test_fused_nw_tail_matches_standalone(monkeypatch):
     assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-2000:]
 
 
+@pytest.mark.parametrize("layout", ["reversed_with_gaps", "one_gap"])
+def test_mine_host_unpacked_sentence_offsets(layout):
+    """bimine_mine_host rebuilds sent_tok_off from sent_len on the device
+    unless the caller's offsets differ from that packed layout; then it uses
+    the caller's.  Sentences stored out of order, with gaps, mine the same."""
+    from paper_1512_01641_b200.packing import PackedBatch
+
+    corpus = synth.make_config(2, n_pairs=40)
+    d = corpus.dictionary
+    model = model_vector(H.synth_model())
+    dd = E.LexiconContext(vocab=None, coo=(d.src, d.tgt, d.prob), devices={}).on(E.current_device())
+    b = corpus.batch
+    want = E.mine_host(dd, model, b, 2.0, 0.5, -1.0, 1.0, want_sim=True)
+    S = b.n_sentences
+    order = np.arange(S)[::-1] if layout == "reversed_with_gaps" else np.arange(S)
+    gap = 3 if layout == "reversed_with_gaps" else 0
+    pieces, off, pos = [], np.zeros(S, dtype=np.int64), 0
+    for s in order.tolist():
+        if layout == "one_gap" and s == S // 2:
+            pieces.append(np.full(5, 7, dtype=np.int32))
+            pos += 5
+        off[s] = pos
+        pieces.append(b.tokens[b.sent_tok_off[s]: b.sent_tok_off[s] + b.sent_len[s]])
+        pos += int(b.sent_len[s])
+        if gap:
+            pieces.append(np.full(gap, 123456, dtype=np.int32))
+            pos += gap
+    moved = PackedBatch(tokens=np.concatenate(pieces), sent_tok_off=off, sent_len=b.sent_len, sent_uniq=b.sent_uniq,
+                        sent_chars=b.sent_chars, pair_src=b.pair_src, pair_n=b.pair_n, pair_tgt=b.pair_tgt,
+                        pair_m=b.pair_m, pair_sim_off=b.pair_sim_off)
+    got = E.mine_host(dd, model, moved, 2.0, 0.5, -1.0, 1.0, want_sim=True)
+    assert np.array_equal(got[0], want[0])
+    assert np.array_equal(got[1].view(np.uint8), want[1].view(np.uint8))
+    assert bits_equal(got[2], want[2])
+
+
 @pytest.mark.parametrize("chunks", ["3", "7"])
 def test_mine_host_chunked_uploads(chunks):
     """bimine_mine_host with the batch uploaded in chunks (the score kernel
