@@ -244,7 +244,11 @@ int bimine_agreement_batch(const bimine_match *matches_dev,
  *   counts_host[n_pairs]        matches per pair
  *   matches_host[capacity]      compacted matches in pair order
  *   capacity >= sum over pairs of min(N, M)
- *   sim_host (optional, may be NULL): the score matrices. */
+ *   sim_host (optional, may be NULL): the score matrices.
+ * Host buffers are read while the call runs (page-locked ones let the
+ * uploads overlap the scoring).  sent_tok_off is rebuilt on the device as
+ * the exclusive sum of sent_len and uploaded only when the caller's
+ * offsets differ from that packed layout. */
 int bimine_mine_host(const bimine_dict *dict, const double *model,
                      const bimine_batch *batch_host, double gap,
                      double threshold, double mismatch, double bonus,
