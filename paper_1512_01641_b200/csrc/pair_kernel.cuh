@@ -11,7 +11,7 @@
 //  D  warp per source sentence i (claimed longest first); lane j owns
 //     target sentences j and j + 32.  The sentence's occurrences are cut
 //     into segments of <= 32 occurrences whose dictionary rows (p > 0
-//     entries, CSR) total <= 64 entries.  The warp walks a segment's
+//     entries, CSR) total <= 96 entries.  The warp walks a segment's
 //     entries flattened, 32 per step, against the hash (behind a Bloom
 //     prefilter); each hit (colmask, p) is appended to the warp's
 //     candidate list in entry order and sets reachcol[d] |= bit i
@@ -73,11 +73,10 @@ struct PairArgs {
   const int32_t *need;
 };
 
-constexpr int kSegItems = 64;   // dictionary entries examined per warp segment
+constexpr int kSegItems = 96;   // dictionary entries examined per warp segment
 constexpr int kBloomBits = 14;  // 16384-bit prefilter in front of the hash
 
 struct PairSmem {
-  uint64_t *exp_tab;   // [256]
   uint64_t *colmask;   // [cap_u]
   uint64_t *reachcol;  // [cap_u]
   uint64_t *c_m;       // [warps][kSegItems] in-chunk translations: colmask
@@ -127,7 +126,6 @@ __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_
   t.seen = (uint32_t *)take((size_t)kPairWarps * 32 * 4, 16);
   t.overlay_bytes = o;
   // live until the end
-  t.exp_tab = (uint64_t *)take(256 * 8, 16);
   t.src_off = (int64_t *)take(64 * 8, 16);
   t.tgt_off = (int64_t *)take(64 * 8, 16);
   t.src_len = (int32_t *)take(64 * 4, 4);
@@ -255,7 +253,6 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
   uint16_t *__restrict__ aux = A.aux + A.b.pair_sim_off[p] + (int64_t)i0 * Mfull + j0;
 
   // ---- 0: tables and sentence metadata
-  for (int k = tid; k < 256; k += kPairThreads) S.exp_tab[k] = kExpTableDev[k];
   if (tid < N) {
     S.src_off[tid] = A.b.sent_tok_off[s_first + tid];
     S.src_len[tid] = A.b.sent_len[s_first + tid];
@@ -433,10 +430,10 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           const bool in_seg = lane < cnt;
           const int items = min(kSegItems, __shfl_sync(kFull, x, cnt - 1));
           const int ofs = x - rl;  // exclusive prefix: first item of this occurrence
-          // the segment's dictionary entries (<= 2 steps of 32, in order):
-          // owners found and loads issued now, so their L2 latency overlaps
-          // the shared-token work below
-          static_assert(kSegItems == 64, "the walk below is two steps");
+          // the segment's dictionary entries (<= 3 steps of 32, in order):
+          // the first two steps' owners found and loads issued now, so their
+          // L2 latency overlaps the shared-token work below
+          static_assert(kSegItems == 96, "the walk below is three steps");
           int w_owner[2];
           int32_t w_tgt[2];
           double w_p[2];
@@ -525,11 +522,35 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           // all dictionary entries of the segment, 32 at a time, in order
           int ncand = 0;
 #pragma unroll
-          for (int st = 0; st < 2; ++st) {
+          for (int st = 0; st < 3; ++st) {
             if (st * 32 >= items) break;  // warp-uniform
-            const int owner = w_owner[st];
-            const double pr = w_p[st];  // loaded with the id: no second round trip for hits
-            const int d = w_tgt[st] >= 0 ? pk_find_f(S.bloom, S.keys, S.dense, hbits, w_tgt[st]) : -1;
+            int owner;
+            double pr;
+            int32_t tg;
+            if (st < 2) {
+              owner = w_owner[st];
+              pr = w_p[st];  // loaded with the id: no second round trip for hits
+              tg = w_tgt[st];
+            } else {
+              const int it = 64 + lane;
+              owner = 0;
+#pragma unroll
+              for (int step = 16; step >= 1; step >>= 1) {
+                const int cand = owner + step;
+                const int v = __shfl_sync(kFull, ofs, cand & 31);
+                if (cand < cnt && v <= it) owner = cand;
+              }
+              const int64_t oe0 = __shfl_sync(kFull, e0, owner);
+              const int oofs = __shfl_sync(kFull, ofs, owner);
+              tg = -1;
+              pr = 0.0;
+              if (it < items) {
+                const int64_t e = oe0 + (it - oofs);
+                tg = dtgt[e];
+                pr = dprob[e];
+              }
+            }
+            const int d = tg >= 0 ? pk_find_f(S.bloom, S.keys, S.dense, hbits, tg) : -1;
             const bool pres = d >= 0;
             const unsigned bal = __ballot_sync(kFull, pres);
             if (pres) {
@@ -646,7 +667,7 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
     const uint32_t ax = aux[o];
     const double v = cell_score_t(A.md, A.T, S.src_len[i], S.src_uniq[i], S.src_chars[i], S.tgt_len[j],
                                   S.tgt_uniq[j], S.tgt_chars[j], (int)(ax & 0xffu), out[o], S.covt[x],
-                                  (int)(ax >> 8), S.exp_tab);
+                                  (int)(ax >> 8), kExpTableDev);
     if (kFeatures) {  // features_from_profiles (classifier.py:69-97), IEEE divisions
       const int cov = (int)(ax & 0xffu), sh = (int)(ax >> 8), covt = S.covt[x];
       const int Ls = S.src_len[i], Lt = S.tgt_len[j], Us = S.src_uniq[i], Ut = S.tgt_uniq[j];
