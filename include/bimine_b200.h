@@ -262,9 +262,12 @@ int bimine_mine_host(const bimine_dict *dict, const double *model,
  * id equality is string equality.  bimine_tokenize_batch tokenises n
  * sentences (buf[off[k] : off[k+1]]) with the reference's rules and
  * appends their ids to tokens[] (capacity cap); per sentence it writes
- * len(tokens), len(set(tokens)) and the byte length.  Sentences containing
- * non-ASCII bytes get len_out = -1 and are left to the caller (Unicode
- * lower()/split()); everything else is exact. */
+ * len(tokens), len(set(tokens)) and len(text) in code points.  ASCII text
+ * and text of code points below U+0180 (Latin-1, Latin Extended-A) are
+ * tokenised exactly; any other sentence gets len_out = -1 and is left to
+ * the caller (Unicode lower()/split()).  Large batches are split over
+ * BIMINE_HOST_THREADS threads; ids are assigned in first-occurrence order
+ * whatever the thread count. */
 typedef struct bimine_vocab bimine_vocab;
 int bimine_vocab_create(bimine_vocab **out);
 int bimine_vocab_destroy(bimine_vocab *vocab);

@@ -5,10 +5,14 @@
 // text.lower().split() if ...]`.  For ASCII text that is exactly:
 // lowercase A-Z, split on runs of the ASCII characters str.isspace()
 // accepts (\t \n \v \f \r \x1c-\x1f and space), strip the 32 ASCII
-// punctuation characters from both ends, drop empty tokens.  A sentence
-// with any non-ASCII byte is reported back (length -1) and tokenised by
-// the Python rules on the host (full Unicode lower()/split()), through the
-// same vocabulary, so both paths produce the same ids.
+// punctuation characters from both ends, drop empty tokens.  Text whose
+// code points are all below U+0180 (Latin-1 Supplement, Latin Extended-A:
+// Polish, German, French, ...) is handled natively too: there str.lower()
+// is the one-to-one map of lower_latin() (except U+0130, which lowers to
+// two code points) and str.isspace() adds U+0085 and U+00A0.  Any other
+// sentence is reported back (length -1) and tokenised by the Python rules
+// on the host, through the same vocabulary, so every path gives the same
+// ids.
 //
 // The vocabulary is a flat open-addressing table (32-byte slots: hash,
 // id, length, the first 16 bytes of the word; all word bytes in a block
@@ -51,6 +55,53 @@ inline const char *padded(const char *w, uint32_t n, std::vector<char> &pad) {
   memcpy(pad.data(), w, n);
   memset(pad.data() + n, 0, 16);
   return pad.data();
+}
+
+// str.lower() of a code point below U+0180 other than U+0130 (checked
+// exhaustively against CPython in tests/test_host.py)
+constexpr uint32_t lower_latin(uint32_t c) {
+  if (c < 0x80) return (c - 'A' < 26u) ? c + 32 : c;
+  if (c >= 0xC0 && c <= 0xDE && c != 0xD7) return c + 32;
+  if (c >= 0x100 && c <= 0x137) return (c & 1) ? c : c + 1;
+  if (c >= 0x139 && c <= 0x148) return (c & 1) ? c + 1 : c;
+  if (c >= 0x14A && c <= 0x177) return (c & 1) ? c : c + 1;
+  if (c == 0x178) return 0xFF;
+  if (c >= 0x179 && c <= 0x17E) return (c & 1) ? c + 1 : c;
+  return c;
+}
+
+// A non-ASCII sentence of code points < U+0180 (not U+0130): lowered, as
+// UTF-8, into `out`, whitespace code points as ' '; returns its code-point
+// count, or -1 when the sentence needs the Python rules.
+int64_t lower_latin_sentence(const unsigned char *p, int64_t L, std::vector<unsigned char> &out) {
+  out.clear();
+  int64_t cps = 0;
+  for (int64_t x = 0; x < L; ++cps) {
+    const unsigned char b = p[x];
+    uint32_t c;
+    if (b < 0x80) {
+      c = b;
+      x += 1;
+    } else if ((b & 0xE0) == 0xC0 && x + 1 < L && (p[x + 1] & 0xC0) == 0x80) {
+      c = ((uint32_t)(b & 0x1F) << 6) | (p[x + 1] & 0x3F);
+      if (c < 0x80 || c >= 0x180 || c == 0x130) return -1;  // overlong, or outside the table
+      x += 2;
+    } else {
+      return -1;
+    }
+    if (c == 0x85 || c == 0xA0) {
+      out.push_back(' ');
+      continue;
+    }
+    c = lower_latin(c);
+    if (c < 0x80) {
+      out.push_back((unsigned char)c);
+    } else {
+      out.push_back((unsigned char)(0xC0 | (c >> 6)));
+      out.push_back((unsigned char)(0x80 | (c & 0x3F)));
+    }
+  }
+  return cps;
 }
 
 constexpr bool is_space(unsigned char c) {
@@ -176,9 +227,10 @@ void tokenize_range(const bimine_vocab &v, const unsigned char *buf, const int64
     uint32_t off, len;
   };
   std::vector<Tok> toks;
+  std::vector<unsigned char> lat;  // a Latin sentence, lowered
   for (int64_t k = r.k0; k < r.k1; ++k) {
     const unsigned char *p = buf + off[k];
-    const int64_t L = off[k + 1] - off[k];
+    int64_t L = off[k + 1] - off[k];
     chars_out[k] = (int32_t)L;
     bool ascii = true;
     for (int64_t x = 0; x < L; ++x)
@@ -187,8 +239,14 @@ void tokenize_range(const bimine_vocab &v, const unsigned char *buf, const int64
         break;
       }
     if (!ascii) {
-      len_out[k] = -1;  // the caller applies the Unicode rules
-      continue;
+      const int64_t cps = lower_latin_sentence(p, L, lat);
+      if (cps < 0) {
+        len_out[k] = -1;  // the caller applies the Unicode rules
+        continue;
+      }
+      chars_out[k] = (int32_t)cps;  // len(text): code points
+      p = lat.data();
+      L = (int64_t)lat.size();
     }
     low.resize((size_t)L + 12 * (size_t)(L + 1) + 32);  // <= (L+1)/2 tokens, each its bytes + <= 23
     toks.clear();

@@ -46,20 +46,20 @@ class Vocabulary:
 
 
 def _utf8_offsets(strings: list[str]) -> tuple[bytes, np.ndarray]:
-    joined = "".join(strings)
-    data = joined.encode("utf-8", "surrogatepass")
+    """The strings' UTF-8 bytes back to back, and their byte offsets."""
     off = np.zeros(len(strings) + 1, dtype=np.int64)
-    if len(data) == len(joined):  # all ASCII: byte offsets = character offsets
+    if all(map(str.isascii, strings)):  # (O(1) per string) byte offsets = character offsets
         np.cumsum(np.fromiter(map(len, strings), dtype=np.int64, count=len(strings)), out=off[1:])
-    else:
-        np.cumsum(np.fromiter((len(x.encode("utf-8", "surrogatepass")) for x in strings), dtype=np.int64,
-                              count=len(strings)), out=off[1:])
-    return data, off
+        return "".join(strings).encode("ascii"), off
+    enc = [x.encode("utf-8", "surrogatepass") for x in strings]
+    np.cumsum(np.fromiter(map(len, enc), dtype=np.int64, count=len(enc)), out=off[1:])
+    return b"".join(enc), off
 
 
 class NativeVocabulary:
     """The same mapping kept in libbimine_b200.so (bimine_vocab_*), with the
-    native tokenizer (bimine_tokenize_batch) for ASCII sentences."""
+    native tokenizer (bimine_tokenize_batch) for ASCII and Latin-1 /
+    Latin Extended-A sentences (the Python rules for the rest)."""
 
     native = True
 
@@ -113,7 +113,7 @@ class NativeVocabulary:
                                               N.ptr(chars, N._i32p)))
         tokens, lens, uniq, chars = tokens[: int(nt[0])], lens[:n], uniq[:n], chars[:n]
         slow = np.flatnonzero(lens < 0)
-        if slow.size:  # non-ASCII sentences: Python's Unicode rules, same vocabulary
+        if slow.size:  # code points >= U+0180 (or U+0130): Python's Unicode rules, same vocabulary
             starts = np.zeros(n + 1, dtype=np.int64)
             np.cumsum(np.maximum(lens, 0), out=starts[1:])
             pieces = []

@@ -207,6 +207,54 @@ def test_native_tokenizer_matches_python_rules():
     assert pos == tokens.shape[0]
 
 
+def test_native_tokenizer_latin_range_exhaustive(monkeypatch):
+    """Every code point below U+0180, inside words, alone and at token
+    edges: the native Latin path equals CPython's lower()/split()/strip()
+    (text.py:97-104) and len(text); only U+0130 (lowers to two code points)
+    is left to the Python rules."""
+    from paper_1512_01641_b200 import packing
+
+    v = _native_vocab()
+    sents = [f"A{chr(c)}b {chr(c)} .{chr(c)}, Ż{chr(c)}Ó" for c in range(1, 0x180)]
+    fallback = []
+    real = packing.tokenize
+
+    def spy(s):
+        fallback.append(s)
+        return real(s)
+
+    monkeypatch.setattr(packing, "tokenize", spy)
+    tokens, lens, uniq, chars = v.tokenize(sents)
+    pos = 0
+    for s, L, U, C in zip(sents, lens.tolist(), uniq.tolist(), chars.tolist()):
+        want = tokenize(s)
+        assert [v.get(w) for w in want] == tokens[pos: pos + L].tolist(), repr(s)
+        assert U == len(set(want)) and C == len(s), repr(s)
+        pos += L
+    assert fallback == [f"A{chr(0x130)}b {chr(0x130)} .{chr(0x130)}, Ż{chr(0x130)}Ó"]
+
+
+def test_native_tokenizer_polish_text_stays_native(monkeypatch):
+    import random
+
+    from paper_1512_01641_b200 import packing
+
+    v = _native_vocab()
+    rng = random.Random(7)
+    words = ["Zażółć", "gęślą", "jaźń", "ŁÓDŹ", "świeże", "Kraków", "ĄĘ", "über", "Straße", "Ÿ", "naïve", "x"]
+    sents = [" ".join(rng.choice(words) + rng.choice(["", ",", ".", "!"]) for _ in range(rng.randint(1, 12)))
+             + rng.choice(["", "\xa0", "\x85 tail"]) for _ in range(500)]
+    seen = []
+    monkeypatch.setattr(packing, "tokenize", lambda s: seen.append(s) or tokenize(s))
+    tokens, lens, uniq, chars = v.tokenize(sents)
+    assert seen == []
+    pos = 0
+    for s, L, C in zip(sents, lens.tolist(), chars.tolist()):
+        assert [v.get(w) for w in tokenize(s)] == tokens[pos: pos + L].tolist(), repr(s)
+        assert C == len(s)
+        pos += L
+
+
 def test_native_tokenizer_threaded_batch():
     """A batch past the multi-thread split (>= 512 KB): same tokens as the
     Python rules, long words sharing their first 16 bytes kept apart, and
