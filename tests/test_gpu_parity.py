@@ -350,6 +350,9 @@ def test_sentences_longer_than_255_tokens_use_fallback_kernel():
     assert plan.n_long == 1 and plan.n_tiles == 0
     got = E.score_host(ctx.on(E.current_device()), model, batch)
     assert bits_equal(got, want)
+    # through bimine_mine_host too (it uploads sent_uniq only for such pairs)
+    _, _, sim = E.mine_host(ctx.on(E.current_device()), model, batch, 2.0, 0.5, -1.0, 1.0, want_sim=True)
+    assert bits_equal(sim, want)
 
 
 def test_plan_tiles_for_large_pairs():
