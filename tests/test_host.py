@@ -207,6 +207,21 @@ def test_native_tokenizer_matches_python_rules():
     assert pos == tokens.shape[0]
 
 
+def test_utf8_offsets_edge_cases():
+    """The UTF-8 packing behind bimine_tokenize_batch: bytes back to back and
+    byte offsets, for ASCII, non-ASCII, empty strings, NULs and lone
+    surrogates (surrogatepass, as NativeVocabulary.add_many encodes)."""
+    from paper_1512_01641_b200.packing import _utf8_offsets
+
+    cases = [[], [""], ["", ""], ["abc", "", "d"], ["żółw", "", "x\x00y", "ó"], ["\udc80", "a\ud800b"],
+             ["ascii"] * 3 + ["ĄĘ"], [chr(c) for c in range(1, 0x800, 7)]]
+    for strs in cases:
+        data, off = _utf8_offsets(strs)
+        enc = [x.encode("utf-8", "surrogatepass") for x in strs]
+        assert data == b"".join(enc), strs
+        assert off.tolist() == [0] + np.cumsum([len(e) for e in enc]).tolist(), strs
+
+
 def test_native_tokenizer_latin_range_exhaustive(monkeypatch):
     """Every code point below U+0180, inside words, alone and at token
     edges: the native Latin path equals CPython's lower()/split()/strip()
