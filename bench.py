@@ -227,7 +227,7 @@ def run_reference(args):
         "metric": METRIC,
         "value": value,
         "unit": UNIT,
-        "n_gpus": 0,
+        "n_gpus": args.gpus,  # the launch's N; the work runs on rank 0's host cores
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3,
@@ -236,7 +236,8 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (SURVEY.md 8(d) generator, seeded)",
-        "config": {"workload": f"C{args.config}: {corpus.batch.n_pairs} pairs", "sample_pairs_per_step": per_step},
+        "config": {"workload": f"C{args.config}: {corpus.batch.n_pairs} pairs", "sample_pairs_per_step": per_step,
+                   "devices": "host CPU only (rank 0)"},
         "nw_gcups": sample.n_cells * args.steps / dt / 1e9,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{per_step} pairs per step ({sample.n_cells} cells), oracle/bimine_oracle.c, "
