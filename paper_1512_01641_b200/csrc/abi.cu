@@ -127,17 +127,35 @@ struct UploadGate {
 thread_local const UploadGate *tl_gate = nullptr;
 cudaError_t gate_wait_all(cudaStream_t st) { return tl_gate ? cudaStreamWaitEvent(st, tl_gate->all, 0) : cudaSuccess; }
 
+// a device word the long-sentence kernel reports overflows in (one per
+// device: one process may drive several GPUs, one host thread each)
+int *device_status_word() {
+  static std::mutex mu;
+  static std::map<int, int *> words;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  int *&w = words[dev];
+  if (!w && cudaMalloc(&w, sizeof(int)) != cudaSuccess) w = nullptr;
+  return w;
+}
+
+// the current device's default pool keeps freed blocks cached (once per
+// device: one process may drive several GPUs, one host thread each)
 void pool_setup() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t threshold = UINT64_MAX;  // keep freed blocks cached in the pool
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
-    }
-  });
+  static std::mutex mu;
+  static uint64_t done = 0;  // bit per device id < 64
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done >> dev & 1) return;
+  done |= 1ull << dev;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t threshold = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+  }
 }
 
 int next_pow2(int x) {
@@ -438,8 +456,8 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
     A.cap_u = std::min(kMaxCapU, std::max(1024, next_pow2(plan->max_uniq)));
     A.cap_t = std::min(kMaxCapT, std::max(4096, next_pow2(plan->max_len)));
     A.hash_bits = ilog2(2 * A.cap_u);
-    static int *status = nullptr;
-    if (!status) BIMINE_CUDA(cudaMalloc(&status, sizeof(int)));
+    int *status = device_status_word();
+    if (!status) return fail(BIMINE_E_CUDA, "score_kernel: status word allocation failed");
     A.status = status;
     const size_t smem = score_smem_layout(nullptr, A.cap_u, A.cap_t, nullptr);
     BIMINE_CUDA(cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
