@@ -1039,23 +1039,48 @@ __global__ void __launch_bounds__(32) nw_big_traceback_kernel(const NwArgs A, co
       win_k0 = 0;
     }
     __syncwarp();
+    // the next band's window, loaded into registers while lane 0 walks the
+    // current one: the path enters band g-1 at a column no greater than
+    // where it entered band g, so the window ending at that column covers
+    // any path that moves < ~120 columns left within the band
+    uint16_t pre[16];
+    int pre_g = -1, pre_k0 = 0;
     while (true) {
       a = __shfl_sync(kFull, a, 0);
       b = __shfl_sync(kFull, b, 0);
       if (!(a > 0 && b > 0)) break;
       const int g = (a - 1) >> 5, l = (a - 1) & 31, k = (b + l - 1) >> 3;
       if (!(g == win_g && k >= win_k0 && k < win_k0 + 16)) {
-        const int k0 = max(0, k - 15);
-        for (int x = lane; x < 16 * 32; x += 32) {
-          const int kk = k0 + (x >> 5);
-          win[x] = kk < G8 ? __ldcg(dirs + ((int64_t)g * G8 + kk) * 32 + (x & 31)) : (uint16_t)0;
+        if (g == pre_g && k >= pre_k0 && k < pre_k0 + 16) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) win[t * 32 + lane] = pre[t];
+          __syncwarp();
+          if (lane == 0) {
+            win_g = g;
+            win_k0 = pre_k0;
+          }
+        } else {
+          const int k0 = max(0, k - 15);
+          for (int x = lane; x < 16 * 32; x += 32) {
+            const int kk = k0 + (x >> 5);
+            win[x] = kk < G8 ? __ldcg(dirs + ((int64_t)g * G8 + kk) * 32 + (x & 31)) : (uint16_t)0;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            win_g = g;
+            win_k0 = k0;
+          }
         }
         __syncwarp();
-        if (lane == 0) {
-          win_g = g;
-          win_k0 = k0;
+        pre_g = g - 1;  // issue band g-1's loads now; they land during the walk
+        if (pre_g >= 0) {
+          pre_k0 = max(0, ((b + 30) >> 3) - 15);
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int kk = pre_k0 + t;
+            pre[t] = kk < G8 ? __ldcg(dirs + ((int64_t)pre_g * G8 + kk) * 32 + lane) : (uint16_t)0;
+          }
         }
-        __syncwarp();
       }
       if (lane == 0) {
         // window bounds and base in registers: nothing but the direction
