@@ -246,22 +246,35 @@ __device__ __forceinline__ double band_sweep(const double *__restrict__ sim, int
   double cur = left0;
   double diag = __shfl_up_sync(kFull, left0, 1);  // dp[a-1][0] for lanes > 0
   const double *srow = sim + (int64_t)(N - (active ? a : N)) * ld + (M - 1);
-  auto ldr = [&](int b) -> double {
-    if (!(active && b >= 1 && b <= M)) return 0.0;
-    const double *q = srow - (b - 1);
-    return kGlobal ? __ldg(q) : *q;
-  };
   const int nsteps = M + 31;
-  double nxt[8];
+  // the 8 values of the group starting at step t0: element u is column
+  // b = t0 + u - lane + 1, at srow - (b - 1); one base pointer and one
+  // validity mask per group, then predicated loads
+  auto load_group = [&](int t0, double *dst) {
+    const int bb = t0 - lane + 1;
+    const uint32_t lim = active ? (uint32_t)M : 0u;  // column b valid iff (b - 1) < lim
+    const double *q = srow - (bb - 1);
 #pragma unroll
-  for (int u = 0; u < 8; ++u) nxt[u] = kDiag ? __ldg(sim + u * 32 + lane) : ldr(u - lane + 1);
+    for (int u = 0; u < 8; ++u)
+      dst[u] = ((uint32_t)(bb + u - 1) < lim) ? (kGlobal ? __ldg(q - u) : *(q - u)) : 0.0;
+  };
+  double nxt[8];
+  if (kDiag) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) nxt[u] = __ldg(sim + u * 32 + lane);
+  } else {
+    load_group(0, nxt);
+  }
   for (int s0 = 0, grp = 0; s0 < nsteps; s0 += 8, ++grp) {
     double c[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) c[u] = kDiag ? nxt[u] : fadd(mismatch, fmul(nxt[u], span));
+    if (kDiag) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      nxt[u] = kDiag ? __ldg(sim + (int64_t)(s0 + 8 + u) * 32 + lane) : ldr(s0 + 8 + u - lane + 1);
+      for (int u = 0; u < 8; ++u) nxt[u] = __ldg(sim + (int64_t)(s0 + 8 + u) * 32 + lane);
+    } else {
+      load_group(s0 + 8, nxt);
+    }
     // steps s0+u with 1 <= b <= M for this lane
     const int lo = max(lane - s0, 0), hi = min(lane + M - 1 - s0, 7);
     const uint32_t vmask = (active && lo <= hi) ? (((2u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
