@@ -467,7 +467,7 @@ __device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *r
 // row buffer, in dynamic shared memory (g_dirs == null) or in a global
 // scratch slot.
 template <int MODE>
-__global__ void __launch_bounds__(128) nw_kernel(const NwArgs A) {
+__global__ void __launch_bounds__(128, 5) nw_kernel(const NwArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const int warps_per_block = blockDim.x >> 5;
