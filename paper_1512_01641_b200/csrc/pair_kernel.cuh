@@ -80,7 +80,7 @@ struct PairSmem {
   uint64_t *colmask;   // [cap_u]
   uint64_t *reachcol;  // [cap_u]
   uint64_t *c_m;       // [warps][kSegItems] in-chunk translations: colmask
-  double *c_p;         // [warps][kSegItems]                        probability
+  double *c_p;         // [warps][kSegItems]                        probability (negated: first of its occurrence)
   int64_t *src_off, *tgt_off;  // [64]
   uint32_t *bloom;     // [2^kBloomBits / 32]
   int32_t *keys;       // [slots]
@@ -88,7 +88,6 @@ struct PairSmem {
   int32_t *tgt_len, *tgt_uniq, *tgt_chars;  // [64]
   int32_t *tgt_occ0;   // [65] chunk-local occurrence offsets
   uint8_t *src_order;  // [64] source sentences, longest first (phase D claim order)
-  uint8_t *c_o;        // [warps][kSegItems]                        owning occurrence
   uint32_t *seen;      // [warps][1024 / 32] chunk tokens already met in the warp's source sentence
   int32_t *misc;       // [8]: 0 distinct count, 1 chunk end, 2 D work counter, 3 C work counter
   int16_t *dense;      // [slots]
@@ -122,7 +121,6 @@ __host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_
   t.keys = (int32_t *)take(slots * 4, 16);
   t.dense = (int16_t *)take(slots * 2, 4);
   t.tgt_d = (int16_t *)take((size_t)cap_t * 2, 4);
-  t.c_o = (uint8_t *)take((size_t)kPairWarps * kSegItems, 4);
   t.seen = (uint32_t *)take((size_t)kPairWarps * 32 * 4, 16);
   t.overlay_bytes = o;
   // live until the end
@@ -373,7 +371,6 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
     __syncthreads();
     // ---- D: source side, warps take sentences dynamically
     {
-      uint8_t *co = S.c_o + warp * kSegItems;
       uint64_t *cm = S.c_m + warp * kSegItems;
       uint32_t *seen = S.seen + warp * 32;
       double *cp = S.c_p + warp * kSegItems;
@@ -519,8 +516,13 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
             seg += 1;  // cnt == 1 here
             continue;
           }
-          // all dictionary entries of the segment, 32 at a time, in order
+          // all dictionary entries of the segment, 32 at a time, in order.
+          // A candidate whose owner differs from the previous candidate's
+          // (the first of its occurrence) is stored with p negated: every
+          // dictionary p is > 0, so the sign bit is free and the pass below
+          // needs no owner array
           int ncand = 0;
+          int last_owner = -1;  // owner of the segment's latest candidate
 #pragma unroll
           for (int st = 0; st < 3; ++st) {
             if (st * 32 >= items) break;  // warp-uniform
@@ -553,14 +555,17 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
             const int d = tg >= 0 ? pk_find_f(S.bloom, S.keys, S.dense, hbits, tg) : -1;
             const bool pres = d >= 0;
             const unsigned bal = __ballot_sync(kFull, pres);
+            const unsigned below = bal & lt_mask;
+            const int prev_sh = __shfl_sync(kFull, owner, below ? 31 - __clz(below) : 0);
             if (pres) {
               const uint64_t m = S.colmask[d];
-              const int pos = ncand + __popc(bal & lt_mask);
+              const int pos = ncand + __popc(below);
+              const int prev = below ? prev_sh : last_owner;
               cm[pos] = m;
-              cp[pos] = pr;
+              cp[pos] = owner != prev ? -pr : pr;
               or64(&S.reachcol[d], ibit);
-              co[pos] = (uint8_t)owner;
             }
+            if (bal) last_owner = __shfl_sync(kFull, owner, 31 - __clz(bal));
             ncand += __popc(bal);
           }
           // the next window's dictionary rows (its tokens arrived during the walk)
@@ -578,31 +583,29 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           const uint32_t lbit = 1u << lane;  // bit of target jlo in the low word, jhi in the high word
           // candidate-major: the candidates are in entry order, so each
           // occurrence's are contiguous and the occurrences come in order;
-          // an occurrence's best is added when its last candidate has been
-          // seen (occurrences without a candidate would add +0.0)
-          int cur = -1;
+          // an occurrence's best is added when the next one starts (a
+          // negated p) or the list ends.  The flush before the first
+          // candidate adds +0.0 to a non-negative sum: bit-identical
+          // (occurrences without a candidate would add +0.0 too)
           double bl = 0.0, bh = 0.0;
           for (int c = 0; c < ncand; ++c) {
-            const int o = co[c];  // same address in every lane: broadcast
-            const uint64_t m = cm[c];
-            const double pr = cp[c];
-            if (o != cur) {  // warp-uniform
-              if (cur >= 0) {
-                // every dictionary probability is > 0, so a translation of
-                // the occurrence is in sentence j exactly when its best > 0
-                sum_lo = fadd(sum_lo, bl);
-                sum_hi = fadd(sum_hi, bh);
-                cov_lo += bl > 0.0 ? 1 : 0;
-                cov_hi += bh > 0.0 ? 1 : 0;
-              }
-              cur = o;
+            const uint64_t m = cm[c];  // same address in every lane: broadcast
+            double pr = cp[c];
+            if (pr < 0.0) {  // warp-uniform
+              // every dictionary probability is > 0, so a translation of
+              // the occurrence is in sentence j exactly when its best > 0
+              sum_lo = fadd(sum_lo, bl);
+              sum_hi = fadd(sum_hi, bh);
+              cov_lo += bl > 0.0 ? 1 : 0;
+              cov_hi += bh > 0.0 ? 1 : 0;
               bl = 0.0;
               bh = 0.0;
+              pr = -pr;
             }
             if (((uint32_t)m & lbit) && pr > bl) bl = pr;
             if (((uint32_t)(m >> 32) & lbit) && pr > bh) bh = pr;
           }
-          if (cur >= 0) {
+          if (ncand > 0) {
             sum_lo = fadd(sum_lo, bl);
             sum_hi = fadd(sum_hi, bh);
             cov_lo += bl > 0.0 ? 1 : 0;
