@@ -371,9 +371,13 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
     __syncthreads();
     // ---- D: source side, warps take sentences dynamically
     {
-      uint64_t *cm = S.c_m + warp * kSegItems;
+      // the warp's candidate-list offset, opaque to ptxas so that it stays
+      // in a register rather than being re-derived from %tid in the loops
+      int cbase;
+      asm volatile("mov.u32 %0, %1;" : "=r"(cbase) : "r"(warp * kSegItems));
+      uint64_t *cm = S.c_m + cbase;
       uint32_t *seen = S.seen + warp * 32;
-      double *cp = S.c_p + warp * kSegItems;
+      double *cp = S.c_p + cbase;
       const int jlo = lane, jhi = lane + 32;
       const unsigned lt_mask = (1u << lane) - 1u;
       // software pipeline: the next segment's window (token, dictionary row)
@@ -580,7 +584,11 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           // occurrence-major, in order: max p over the occurrence's
           // translations present in sentence j, added to the running sum
           // (adding +0.0 when absent leaves the non-negative sum unchanged)
-          const uint32_t lbit = 1u << lane;  // bit of target jlo in the low word, jhi in the high word
+          // bit of target jlo in the low word, jhi in the high word; read once
+          // per segment through volatile asm so that ptxas keeps it in a
+          // register instead of re-deriving it from %tid in the loop
+          uint32_t lbit;
+          asm volatile("mov.u32 %0, %%lanemask_eq;" : "=r"(lbit));
           // candidate-major: the candidates are in entry order, so each
           // occurrence's are contiguous and the occurrences come in order;
           // an occurrence's best is added when the next one starts (a
