@@ -371,6 +371,11 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
     __syncthreads();
     // ---- D: source side, warps take sentences dynamically
     {
+      // phase D's lane id, read once (%laneid) and opaque to ptxas like
+      // cbase below, so that it is not re-derived from %tid per segment
+      int lane_r;
+      asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane_r));
+      const int lane = lane_r;
       // the warp's candidate-list offset, opaque to ptxas so that it stays
       // in a register rather than being re-derived from %tid in the loops
       int cbase;
