@@ -189,6 +189,20 @@ __device__ __forceinline__ void pk_insert(int32_t *keys, int bits, int32_t key) 
   }
 }
 
+// (bit != 0 && p > best) ? p : best, as one predicate: the bit test feeds
+// the compare's predicate input (LOP3 + DSETP.AND + two selects; written
+// in C++ the compiler selects twice, four FSELs per half)
+__device__ __forceinline__ double max_if_bit(double best, double p, uint32_t bit) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\t"
+      "setp.ne.u32 q, %3, 0;\n\t"
+      "setp.gt.and.f64 q, %2, %1, q;\n\t"
+      "selp.f64 %0, %2, %1, q;\n\t}"
+      : "=d"(r)
+      : "d"(best), "d"(p), "r"(bit));
+  return r;
+}
+
 // 64-bit OR into shared memory as native 32-bit ORs of the nonzero halves
 // (a 64-bit shared atomicOr compiles to a compare-and-swap loop)
 __device__ __forceinline__ void or64(uint64_t *w, uint64_t m) {
@@ -615,8 +629,8 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
               bh = 0.0;
               pr = -pr;
             }
-            if (((uint32_t)m & lbit) && pr > bl) bl = pr;
-            if (((uint32_t)(m >> 32) & lbit) && pr > bh) bh = pr;
+            bl = max_if_bit(bl, pr, (uint32_t)m & lbit);
+            bh = max_if_bit(bh, pr, (uint32_t)(m >> 32) & lbit);
           }
           if (ncand > 0) {
             sum_lo = fadd(sum_lo, bl);
