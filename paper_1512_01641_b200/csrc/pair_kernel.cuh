@@ -147,7 +147,12 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
     const uint32_t m = (s == 16) ? 0x0000FFFFu : (s == 8) ? 0x00FF00FFu : (s == 4) ? 0x0F0F0F0Fu
                        : (s == 2) ? 0x33333333u : 0x55555555u;
     const uint32_t o = __shfl_xor_sync(kFull, x, s);
-    x = (lane & s) ? ((x & ~m) | ((o & ~m) >> s)) : ((x & m) | ((o & m) << s));
+    // lower lane: keep x & m, take (o & m) << s; upper lane: keep x & ~m,
+    // take (o & ~m) >> s -- one bit-select with the lane's keep mask
+    const bool up = (lane & s) != 0;
+    const uint32_t keep = up ? ~m : m;
+    const uint32_t v = up ? (o >> s) : (o << s);
+    x = (x & keep) | (v & ~keep);
   }
   return x;
 }
