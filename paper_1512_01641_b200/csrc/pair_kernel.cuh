@@ -474,7 +474,9 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
               for (int step = 16; step >= 1; step >>= 1) {
                 const int cand = owner + step;
                 const int v = __shfl_sync(kFull, ofs, cand & 31);
-                if (cand < cnt && v <= it) owner = cand;
+                // (no cand < cnt test: ofs is the exclusive prefix, so every
+                // lane from cnt on has ofs >= x[cnt - 1] >= items > it)
+                if (v <= it) owner = cand;
               }
               const int64_t oe0 = __shfl_sync(kFull, e0, owner);
               const int oofs = __shfl_sync(kFull, ofs, owner);
@@ -568,7 +570,7 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
               for (int step = 16; step >= 1; step >>= 1) {
                 const int cand = owner + step;
                 const int v = __shfl_sync(kFull, ofs, cand & 31);
-                if (cand < cnt && v <= it) owner = cand;
+                if (v <= it) owner = cand;
               }
               const int64_t oe0 = __shfl_sync(kFull, e0, owner);
               const int oofs = __shfl_sync(kFull, ofs, owner);
