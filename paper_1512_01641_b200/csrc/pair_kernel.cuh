@@ -455,6 +455,7 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           const bool in_seg = lane < cnt;
           const int items = min(kSegItems, __shfl_sync(kFull, x, cnt - 1));
           const int ofs = x - rl;  // exclusive prefix: first item of this occurrence
+          const int64_t eb = e0 - ofs;  // entry of item `it` of this occurrence: eb + it (one 64-bit shuffle)
           // the segment's dictionary entries (<= 3 steps of 32, in order):
           // the first two steps' owners found and loads issued now, so their
           // L2 latency overlaps the shared-token work below
@@ -478,11 +479,10 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
                 // lane from cnt on has ofs >= x[cnt - 1] >= items > it)
                 if (v <= it) owner = cand;
               }
-              const int64_t oe0 = __shfl_sync(kFull, e0, owner);
-              const int oofs = __shfl_sync(kFull, ofs, owner);
+              const int64_t oeb = __shfl_sync(kFull, eb, owner);
               w_owner[st] = owner;
               if (it < items) {
-                const int64_t e = oe0 + (it - oofs);
+                const int64_t e = oeb + it;
                 w_tgt[st] = dtgt[e];
                 w_p[st] = dprob[e];
               }
@@ -572,12 +572,11 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
                 const int v = __shfl_sync(kFull, ofs, cand & 31);
                 if (v <= it) owner = cand;
               }
-              const int64_t oe0 = __shfl_sync(kFull, e0, owner);
-              const int oofs = __shfl_sync(kFull, ofs, owner);
+              const int64_t oeb = __shfl_sync(kFull, eb, owner);
               tg = -1;
               pr = 0.0;
               if (it < items) {
-                const int64_t e = oe0 + (it - oofs);
+                const int64_t e = oeb + it;
                 tg = dtgt[e];
                 pr = dprob[e];
               }
