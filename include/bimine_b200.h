@@ -131,8 +131,8 @@ int64_t bimine_dict_entries(const bimine_dict *dict);
  *   tiles     pairs with N > 64 or M > 64: (pair, i0, j0) per 64x64 tile
  *   long ids  pairs with a sentence of more than 255 tokens (tiled
  *             fallback kernel)
- *   large ids every pair of the two groups above, ascending (their NW runs
- *             as a separate launch; one-CTA pairs fuse it)
+ *   large ids pairs with N > 64 or M > 64, ascending (their NW runs on
+ *             the cluster kernel; every other pair's on one warp)
  * work_host (capacity work_cap int64) receives 3 * n_tiles tile triples,
  * then n_long pair ids, then n_large pair ids; plan->work_len is the length
  * needed
@@ -166,9 +166,9 @@ int bimine_score_batch(const bimine_dict *dict, const double *model,
 /* ---- the fused mining step ---------------------------------------------
  * build_score_matrix + nw_align + filter_by_threshold for every pair of a
  * device batch under one setting: sim_dev receives the score matrices
- * (written once); pairs of at most 64x64 sentences run the NW wavefront,
- * traceback and filter inside the score kernel on the on-chip tile, the
- * plan's large pairs in a separate NW launch.  Outputs as in
+ * (written once); then one NW + traceback + filter launch for the pairs of
+ * at most 64x64 sentences (a warp each) and, if the plan lists large
+ * pairs, one cluster launch for those.  Outputs as in
  * bimine_nw_mine_batch with n_settings = 1 (out_off_dev: capacity
  * min(N, M) slots per pair; score_dev optional). */
 int bimine_mine_batch(const bimine_dict *dict, const double *model,

@@ -90,13 +90,6 @@ cudaError_t offsets_from_lengths(const int32_t *len, int64_t *off, int64_t n, vo
                                        st);
 }
 
-// two doubles into device memory without a host copy (a pageable
-// host-to-device copy would synchronise the stream)
-__global__ void set_pair_kernel(double *dst, double a, double b) {
-  dst[0] = a;
-  dst[1] = b;
-}
-
 // pinned host scratch per thread, grown on demand (upload staging)
 struct PinnedScratch {
   void *p = nullptr;
@@ -184,6 +177,8 @@ struct bimine_dict {
   int64_t *row_ptr = nullptr;
   int32_t *tgt = nullptr;
   double *prob = nullptr;
+  uint64_t *rowdesc = nullptr;  // score kernel's copy: start << 24 | length per row
+  DictEntry *ent = nullptr;     //                      {p, t} per entry
 };
 
 extern "C" {
@@ -230,20 +225,43 @@ int bimine_dict_create(const int32_t *src, const int32_t *tgt, const double *pro
   std::vector<int64_t> row_ptr(d->n_rows + 1, 0);
   for (int32_t s : ks) row_ptr[s + 1]++;
   for (int64_t r = 0; r < d->n_rows; ++r) row_ptr[r + 1] += row_ptr[r];
+  if (d->n_entries >= ((int64_t)1 << 40)) {
+    delete d;
+    return fail(BIMINE_E_LIMIT, "bimine_dict_create: more than 2^40 entries");
+  }
+  // the score kernel's layout: one 8-byte descriptor per row, one 16-byte
+  // {p, t} record per entry
+  std::vector<uint64_t> rowdesc(std::max<int64_t>(1, d->n_rows));
+  for (int64_t r = 0; r < d->n_rows; ++r) {
+    const int64_t len = row_ptr[r + 1] - row_ptr[r];
+    if (len >= (1 << 24)) {
+      delete d;
+      return fail(BIMINE_E_LIMIT, "bimine_dict_create: a source word has 2^24 or more translations");
+    }
+    rowdesc[r] = ((uint64_t)row_ptr[r] << 24) | (uint64_t)len;
+  }
+  std::vector<DictEntry> ent(std::max<int64_t>(1, d->n_entries));
+  for (int64_t k = 0; k < d->n_entries; ++k) ent[k] = DictEntry{kp[k], kt[k], 0};
   auto cleanup = [&](const char *what) {
     cudaFree(d->row_ptr);
     cudaFree(d->tgt);
     cudaFree(d->prob);
+    cudaFree(d->rowdesc);
+    cudaFree(d->ent);
     delete d;
     return fail(BIMINE_E_CUDA, std::string("bimine_dict_create: ") + what);
   };
   if (cudaMalloc(&d->row_ptr, sizeof(int64_t) * (d->n_rows + 1)) != cudaSuccess) return cleanup("cudaMalloc");
   if (cudaMalloc(&d->tgt, sizeof(int32_t) * std::max<int64_t>(1, d->n_entries)) != cudaSuccess) return cleanup("cudaMalloc");
   if (cudaMalloc(&d->prob, sizeof(double) * std::max<int64_t>(1, d->n_entries)) != cudaSuccess) return cleanup("cudaMalloc");
+  if (cudaMalloc(&d->rowdesc, sizeof(uint64_t) * rowdesc.size()) != cudaSuccess) return cleanup("cudaMalloc");
+  if (cudaMalloc(&d->ent, sizeof(DictEntry) * ent.size()) != cudaSuccess) return cleanup("cudaMalloc");
   if (cudaMemcpy(d->row_ptr, row_ptr.data(), sizeof(int64_t) * (d->n_rows + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
       (d->n_entries &&
        (cudaMemcpy(d->tgt, kt.data(), sizeof(int32_t) * d->n_entries, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(d->prob, kp.data(), sizeof(double) * d->n_entries, cudaMemcpyHostToDevice) != cudaSuccess)))
+        cudaMemcpy(d->prob, kp.data(), sizeof(double) * d->n_entries, cudaMemcpyHostToDevice) != cudaSuccess)) ||
+      cudaMemcpy(d->rowdesc, rowdesc.data(), sizeof(uint64_t) * rowdesc.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(d->ent, ent.data(), sizeof(DictEntry) * ent.size(), cudaMemcpyHostToDevice) != cudaSuccess)
     return cleanup("cudaMemcpy");
   *out = d;
   return BIMINE_OK;
@@ -254,6 +272,8 @@ int bimine_dict_destroy(bimine_dict *d) {
   cudaFree(d->row_ptr);
   cudaFree(d->tgt);
   cudaFree(d->prob);
+  cudaFree(d->rowdesc);
+  cudaFree(d->ent);
   delete d;
   return BIMINE_OK;
 }
@@ -300,7 +320,7 @@ int bimine_plan_batch(const bimine_batch *b, int64_t *work, int64_t work_cap, bi
     }
     P.max_len = std::max(P.max_len, ml);
     P.max_uniq = std::max(P.max_uniq, mu);
-    if (ml > kPairMaxLen || n > kPairMax || m > kPairMax) larges.push_back(p);
+    if (n > kPairMax || m > kPairMax) larges.push_back(p);  // NW: cluster kernel
     if (ml > kPairMaxLen) {
       longs.push_back(p);
       P.long_max_n = std::max(P.long_max_n, n);
@@ -377,16 +397,8 @@ extern "C" {
 
 namespace {
 
-struct FusedNw {
-  double gap, threshold, mismatch, bonus;
-  const int64_t *out_off;
-  bimine_match *matches;
-  int32_t *counts;
-  double *score;
-};
-
 int launch_scores(const bimine_dict *dict, const double *model, const bimine_batch *b, const bimine_plan *plan,
-                  double *sim_dev, const FusedNw *nw, cudaStream_t st, double *features = nullptr) {
+                  double *sim_dev, cudaStream_t st, double *features = nullptr) {
   if (!dict || !model || !b || !plan || !sim_dev) return fail(BIMINE_E_ARG, "bimine_score_batch: null argument");
   if (b->n_pairs == 0) return BIMINE_OK;
   if (plan->max_n < 1 || plan->max_m < 1 || plan->max_uniq < 1 || plan->max_len < 1)
@@ -396,7 +408,7 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
   if (b->n_pairs > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: more than 2^31-1 pairs per call");
   if (plan->work_len > 0 && !plan->work) return fail(BIMINE_E_ARG, "bimine_score_batch: plan.work not set");
   const BatchDev bd = to_dev(*b);
-  const DictDev dd = DictDev{dict->n_rows, dict->row_ptr, dict->tgt, dict->prob};
+  const DictDev dd = DictDev{dict->n_rows, dict->row_ptr, dict->tgt, dict->prob, dict->rowdesc, dict->ent};
   const Model md = to_model(model);
   {
     PairArgs A;
@@ -410,23 +422,7 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
     // per-cell counters scratch (L2 resident while a CTA works on it)
     const int64_t cells = plan->n_cells;
     BIMINE_CUDA(cudaMallocAsync((void **)&A.aux, sizeof(uint16_t) * std::max<int64_t>(cells, 1), st));
-    A.cap_u = 1024;
-    A.hash_bits = 11;
-    A.cap_t = 2048;
-    PairSmem lay;
-    const size_t smem = pair_smem_layout(nullptr, A.cap_u, A.hash_bits, A.cap_t, &lay);
-    if (lay.overlay_bytes < kNwTileBytes + kNwRowBytes + kNwDirBytes)
-      return fail(BIMINE_E_LIMIT, "pair_kernel: overlay too small for the fused NW");
-    if (nw) {
-      A.nw_matches = nw->matches;
-      A.nw_out_off = nw->out_off;
-      A.nw_counts = nw->counts;
-      A.nw_score = nw->score;
-      A.gap = nw->gap;
-      A.threshold = nw->threshold;
-      A.mismatch = nw->mismatch;
-      A.bonus = nw->bonus;
-    }
+    const size_t smem = kPairSmemBytes;
     auto kern = features ? pair_kernel<true> : pair_kernel<false>;
     BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -476,7 +472,7 @@ extern "C" {
 
 int bimine_score_batch(const bimine_dict *dict, const double *model, const bimine_batch *b, const bimine_plan *plan,
                        double *sim_dev, void *stream) {
-  return launch_scores(dict, model, b, plan, sim_dev, nullptr, as_stream(stream));
+  return launch_scores(dict, model, b, plan, sim_dev, as_stream(stream));
 }
 
 }  // extern "C"
@@ -711,45 +707,31 @@ int bimine_mine_batch(const bimine_dict *dict, const double *model, const bimine
   if (!b || b->n_pairs == 0) return BIMINE_OK;
   cudaStream_t st = as_stream(stream);
   pool_setup();
-  // The NW tail fused into the score kernel holds each CTA's shared memory
-  // for the single-warp wavefront; until that tail is faster than the
-  // standalone NW launch it is opt-in (BIMINE_FUSE_NW=1).
-  static const bool fuse = [] {
-    const char *v = getenv("BIMINE_FUSE_NW");
-    return v && v[0] == '1';
-  }();
-  FusedNw nw{gap, threshold, mismatch, bonus, out_off_dev, matches_dev, counts_dev, score_dev};
-  int rc = launch_scores(dict, model, b, plan, sim_dev, fuse ? &nw : nullptr, st);
+  int rc = launch_scores(dict, model, b, plan, sim_dev, st);
   if (rc != BIMINE_OK) return rc;
   BIMINE_CUDA(gate_wait_all(st));
-  if (!fuse) {
-    double *par = nullptr;
-    BIMINE_CUDA(cudaMallocAsync((void **)&par, 2 * sizeof(double), st));
-    set_pair_kernel<<<1, 1, 0, st>>>(par, gap, threshold);
-    NwArgs A = nw_args_base(sim_dev, b->pair_sim_off, b->pair_n, b->pair_m, b->n_pairs, 1, par, mismatch, bonus);
-    A.threshold = par + 1;
-    A.out_off = out_off_dev;
-    A.matches = matches_dev;
-    A.counts = counts_dev;
-    A.score = score_dev;
-    rc = launch_nw<kNwMine>(A, plan->max_n, plan->max_m, st);
-    cudaFreeAsync(par, st);
-    return rc;
-  }
-  if (plan->n_large == 0) return rc;
-  // pairs larger than one CTA: their NW as a separate launch
-  double *par = nullptr;
-  BIMINE_CUDA(cudaMallocAsync((void **)&par, 2 * sizeof(double), st));
-  set_pair_kernel<<<1, 1, 0, st>>>(par, gap, threshold);
-  NwArgs A = nw_args_base(sim_dev, b->pair_sim_off, b->pair_n, b->pair_m, plan->n_large, 1, par, mismatch, bonus);
-  A.problem_ids = plan->work + 3 * plan->n_tiles + plan->n_long;
-  A.threshold = par + 1;
+  // NW + traceback + filter: pairs of at most 64 x 64 sentences one warp
+  // each; the plan's larger pairs on the cluster kernel (one setting,
+  // gap and threshold by value)
+  NwArgs A = nw_args_base(sim_dev, b->pair_sim_off, b->pair_n, b->pair_m, b->n_pairs, 1, nullptr, mismatch, bonus);
+  A.gap1 = gap;
+  A.threshold1 = threshold;
   A.out_off = out_off_dev;
   A.matches = matches_dev;
   A.counts = counts_dev;
   A.score = score_dev;
-  rc = launch_nw<kNwMine>(A, plan->max_n, plan->max_m, st);
-  cudaFreeAsync(par, st);
+  if (plan->n_large < b->n_pairs) {
+    NwArgs As = A;
+    As.small_only = plan->n_large > 0;
+    rc = launch_nw<kNwMine>(As, std::min(plan->max_n, kPairMax), std::min(plan->max_m, kPairMax), st);
+    if (rc != BIMINE_OK) return rc;
+  }
+  if (plan->n_large > 0) {
+    NwArgs Al = A;
+    Al.problem_ids = plan->work + 3 * plan->n_tiles + plan->n_long;
+    Al.n_problems = plan->n_large;
+    rc = launch_nw<kNwMine>(Al, plan->max_n, plan->max_m, st);
+  }
   return rc;
 }
 
@@ -1206,7 +1188,7 @@ int bimine_features_batch(const bimine_dict *dict, const double *model, const bi
   if (plan && plan->n_long > 0)
     return fail(BIMINE_E_LIMIT, "bimine_features_batch: sentences longer than 255 tokens are not supported");
   pool_setup();
-  return launch_scores(dict, model, b, plan, sim_dev, nullptr, as_stream(stream), features_dev);
+  return launch_scores(dict, model, b, plan, sim_dev, as_stream(stream), features_dev);
 }
 
 int bimine_lexicon_em(const int32_t *tgt_off, const int32_t *tgt_tok, int64_t n_pairs, int32_t n_src,

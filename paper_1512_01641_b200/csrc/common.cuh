@@ -26,11 +26,23 @@ struct BatchDev {
   int64_t n_pairs;
 };
 
+// One dictionary entry as the score kernel reads it: p and the target id
+// in one 16-byte record (one load per walked entry).
+struct __align__(16) DictEntry {
+  double p;
+  int32_t t;
+  int32_t pad;
+};
+
 struct DictDev {
   int64_t n_rows;
   const int64_t *row_ptr;
   const int32_t *tgt;
   const double *prob;
+  // the same CSR for the score kernel: row s = entries [rowdesc[s] >> 24,
+  // (rowdesc[s] >> 24) + (rowdesc[s] & 0xFFFFFF)) of `ent`
+  const uint64_t *rowdesc;
+  const DictEntry *ent;
 };
 
 struct Model {

@@ -42,9 +42,11 @@ struct NwArgs {
   const int64_t *problem_ids;  // [n_problems] or null (identity)
   int64_t n_problems;
   int32_t n_settings;          // problem q -> pair q / n_settings, setting q % n_settings
-  const double *gap;           // [n_settings], or [n_problems] if gap_per_problem
+  const double *gap;           // [n_settings], or [n_problems] if gap_per_problem; null: gap1
   int gap_per_problem;
-  const double *threshold;     // [n_settings] (mine mode)
+  const double *threshold;     // [n_settings] (mine mode); null: threshold1
+  double gap1, threshold1;     // one setting passed by value
+  int small_only;              // nw_kernel: skip pairs larger than 64 x 64 (a cluster launch takes them)
   double mismatch, bonus;
   // mine mode
   const int64_t *out_off;      // [problems] slot offsets
@@ -63,6 +65,13 @@ struct NwArgs {
   uint32_t *g_dirs;            // global scratch (null -> shared memory)
   double *g_rows;
 };
+
+__device__ __forceinline__ double nw_gap(const NwArgs &A, int64_t q, int setting) {
+  return A.gap ? (A.gap_per_problem ? A.gap[q] : A.gap[setting]) : A.gap1;
+}
+__device__ __forceinline__ double nw_threshold(const NwArgs &A, int setting) {
+  return A.threshold ? A.threshold[setting] : A.threshold1;
+}
 
 // One problem on one warp.  `sim` is the problem's row-major matrix with
 // row stride `ld` (global memory, or a shared-memory tile in the fused
@@ -449,8 +458,9 @@ __device__ void nw_problem(const NwArgs &A, int64_t q, uint32_t *dirs, double *r
   const int64_t pair = q / A.n_settings;
   const int setting = (int)(q % A.n_settings);
   const int N = A.pair_n[pair], M = A.pair_m[pair];
-  const double gap = A.gap_per_problem ? A.gap[q] : A.gap[setting];
-  const double thr = (MODE == kNwMine) ? A.threshold[setting] : 0.0;
+  if (A.small_only && (N > 64 || M > 64)) return;  // the cluster launch's
+  const double gap = nw_gap(A, q, setting);
+  const double thr = (MODE == kNwMine) ? nw_threshold(A, setting) : 0.0;
   bimine_match *out = (MODE == kNwMine) ? A.matches + A.out_off[q] : nullptr;
   uint8_t *st = (MODE == kNwSteps) ? A.steps + A.step_off[q] : nullptr;
   int32_t *cnt = (MODE == kNwMine) ? A.counts + q : (MODE == kNwSteps) ? A.n_steps + q : nullptr;
@@ -930,7 +940,7 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
   const int64_t pair = q / A.n_settings;
   const int setting = (int)(q % A.n_settings);
   const int N = A.pair_n[pair], M = A.pair_m[pair];
-  const double gap = A.gap_per_problem ? A.gap[q] : A.gap[setting];
+  const double gap = nw_gap(A, q, setting);
   const double ng = -gap, mismatch = A.mismatch, span = fsub(A.bonus, A.mismatch);
   const int G = (N + 31) >> 5, G8 = nw_groups(M);
   uint16_t *dirs = (uint16_t *)(g_dirs_all + slot * dir_stride);  // [G][G8][32]
@@ -1152,7 +1162,7 @@ __global__ void __launch_bounds__(32) nw_big_traceback_kernel(const NwArgs A, co
       }
     } else {
       // gather the scores in parallel, keep those at or above the threshold
-      const double thr = A.threshold[setting];
+      const double thr = nw_threshold(A, setting);
       int64_t kept = 0;
       for (int64_t base = 0; base < cnt; base += 32) {
         const int64_t c = base + lane;

@@ -3,39 +3,46 @@
 // build_score_matrix (align.py:102-129) for pairs with N, M <= 64 and
 // sentences of <= 255 tokens (all C2/C4/C5 pairs); larger pairs (C1, C3)
 // run the same kernel over 64x64 sentence tiles, (pair, i0, j0) per CTA.
-// 8 warps, 4 CTAs per SM; the per-pair tables live in shared memory, the
-// per-cell counters in global scratch (L2-resident while the CTA works).
+// 8 warps, 4 CTAs per SM.
 //
-//  A  target hash: every target token of the chunk -> dense id d;
-//     colmask[d] = 64-bit set of target sentences containing d.
+//  A  target side, warp per target sentence, lanes over its tokens: each
+//     token goes into a shared open-addressing hash whose 64-bit slots
+//     hold (token, dense id); the id is drawn from a counter by the thread
+//     that claims the empty slot, so there is no separate numbering pass.
+//     colmask[d] = 64-bit set of the chunk's target sentences holding
+//     token d; a Bloom filter in front of the hash rejects most of the
+//     dictionary translations that are absent.
 //  D  warp per source sentence i (claimed longest first); lane j owns
 //     target sentences j and j + 32.  The sentence's occurrences are cut
 //     into segments of <= 32 occurrences whose dictionary rows (p > 0
-//     entries, CSR) total <= 96 entries.  The warp walks a segment's
-//     entries flattened, 32 per step, against the hash (behind a Bloom
-//     prefilter); each hit (colmask, p) is appended to the warp's
-//     candidate list in entry order and sets reachcol[d] |= bit i
-//     (reachable_targets, classifier.py:54-59).  Then, occurrence by
-//     occurrence in order, lane j takes the max p over the occurrence's
-//     candidates present in sentence j and adds it to the running sum --
-//     the exact sequential sum of classifier.py:75-82 -- and counts it in
-//     `covered` when > 0 (all p > 0).  Shared tokens (classifier.py:94):
-//     the first occurrence of each distinct chunk token (a per-warp seen
-//     bitmap) adds its colmask bits.
-//  C  warp per target sentence j, lanes = occurrences: transposing the
-//     reachcol rows gives covered_target(i, j) by popc
+//     entries, one 16-byte {p, t} record each) total <= 96 entries.  The
+//     warp walks a segment's entries flattened, 32 per step, each lane
+//     finding its occurrence by a 5-step shuffle search, so lanes stay busy
+//     whatever the row lengths.  Each hit (entry target in the chunk) is
+//     appended, in entry order, to the warp's candidate list as (colmask,
+//     p), p negated on the first candidate of each occurrence, and sets
+//     reachcol[d] |= bit i (reachable_targets, classifier.py:54-59).  A
+//     candidate-major pass then keeps, per lane j, the best p of the
+//     current occurrence; at each negated p the previous best is added to
+//     the running sum and counted in `covered` when > 0 -- the exact
+//     sequential sum of classifier.py:75-82 (an occurrence whose best is 0
+//     would add +0.0 to a non-negative sum: skipping it is bit-identical).
+//     Shared tokens (classifier.py:94): the first occurrence of each
+//     distinct chunk token of the sentence (a per-warp seen bitmap over
+//     dense ids) adds its colmask bits.
+//  C  warp per target sentence j, lanes = occurrences (dense ids looked up
+//     again): transposing the reachcol rows gives covered_target(i, j) by popc
 //     (classifier.py:88-92), multiplicities included.
-//  F  all threads, one cell each (flattened, full lanes): six features ->
-//     margin -> logistic (terms.cuh), one coalesced store per cell.  The
-//     running sums of D are parked in the cell's own output slot (L2) and
-//     overwritten here.
+//  F  all threads, one cell each: six features -> margin -> logistic
+//     (terms.cuh), one coalesced store per cell.  The running sums of D are
+//     parked in the cell's own output slot (L2) and overwritten here.
 //
-// If the chunk's distinct target tokens exceed the hash capacity the
-// target side is processed in halves (same results, more passes).
+// If the chunk's target side exceeds the hash capacity (1024 distinct
+// tokens; chunks start at <= 2048 occurrences) it is processed in parts
+// (same results, more passes).
 #pragma once
 
 #include "common.cuh"
-#include "nw_kernel.cuh"
 #include "terms.cuh"
 
 namespace bimine {
@@ -45,6 +52,12 @@ constexpr int kPairWarps = kPairThreads / 32;
 constexpr int kPairMax = 64;         // sentences per side
 constexpr int kPairMaxLen = 255;     // tokens per sentence (u8 counts)
 constexpr int kCellStride = 64;      // per-cell arrays are [64][64]
+constexpr int kPkHashBits = 11;      // 2048 hash slots
+constexpr int kPkSlots = 1 << kPkHashBits;
+constexpr int kPkCapU = 1024;        // distinct target tokens per chunk
+constexpr int kPkCapT = 2048;        // target occurrences per chunk
+constexpr int kBloomBits = 14;       // 16384-bit prefilter in front of the hash
+constexpr unsigned long long kPkEmpty = ~0ull;
 
 struct PairArgs {
   BatchDev b;
@@ -55,15 +68,6 @@ struct PairArgs {
   uint16_t *aux;            // per-cell scratch, same layout as sim: covered | shared << 8
   const int64_t *tiles;     // (pair, i0, j0) per tile of the pairs larger than 64x64
   int64_t n_tiles;          // CTAs [0, n_tiles) are tiles, the rest one pair each
-  int cap_u;                // distinct target tokens per chunk (dense arrays)
-  int hash_bits;            // log2(hash slots) >= log2(2 cap_u)
-  int cap_t;                // target occurrences per chunk
-  // fused NW + traceback + filter for one-CTA pairs (null: score only)
-  bimine_match *nw_matches;  // slots at nw_out_off[pair]
-  const int64_t *nw_out_off;
-  int32_t *nw_counts;
-  double *nw_score;          // optional
-  double gap, threshold, mismatch, bonus;
   // features mode (extract_features, classifier.py:62-112): the six
   // features of every cell at features[6 * (pair_sim_off + i * M + j) + k]
   double *features;
@@ -74,71 +78,24 @@ struct PairArgs {
 };
 
 constexpr int kSegItems = 96;   // dictionary entries examined per warp segment
-constexpr int kBloomBits = 14;  // 16384-bit prefilter in front of the hash
 
 struct PairSmem {
-  uint64_t *colmask;   // [cap_u]
-  uint64_t *reachcol;  // [cap_u]
-  uint64_t *c_m;       // [warps][kSegItems] in-chunk translations: colmask
-  double *c_p;         // [warps][kSegItems]                        probability (negated: first of its occurrence)
-  int64_t *src_off, *tgt_off;  // [64]
-  uint32_t *bloom;     // [2^kBloomBits / 32]
-  int32_t *keys;       // [slots]
-  int32_t *src_len, *src_uniq, *src_chars;  // [64]
-  int32_t *tgt_len, *tgt_uniq, *tgt_chars;  // [64]
-  int32_t *tgt_occ0;   // [65] chunk-local occurrence offsets
-  uint8_t *src_order;  // [64] source sentences, longest first (phase D claim order)
-  uint32_t *seen;      // [warps][1024 / 32] chunk tokens already met in the warp's source sentence
-  int32_t *misc;       // [8]: 0 distinct count, 1 chunk end, 2 D work counter, 3 C work counter
-  int16_t *dense;      // [slots]
-  int16_t *tgt_d;      // [cap_t]
-  uint8_t *covt;       // [64][64]
-  size_t overlay_bytes;  // bytes of the reusable region at the start
+  unsigned long long hkey[kPkSlots];  // token << 32 | dense id; kPkEmpty
+  uint64_t colmask[kPkCapU];
+  uint64_t reachcol[kPkCapU];
+  uint32_t bloom[(1 << kBloomBits) / 32];
+  uint64_t c_m[kPairWarps][kSegItems];  // per warp: a segment's in-chunk translations: colmask
+  double c_p[kPairWarps][kSegItems];    //   probability (negated: first of its occurrence)
+  uint32_t seen[kPairWarps][kPkCapU / 32];  // dense ids met in the warp's source sentence
+  int64_t src_off[64], tgt_off[64];
+  int32_t src_len[64], src_uniq[64], src_chars[64];
+  int32_t tgt_len[64], tgt_uniq[64], tgt_chars[64];
+  int32_t misc[8];                    // 0 dense-id counter, 1 chunk end, 2 D claims, 3 C claims
+  uint8_t src_order[64];              // source sentences, longest first (phase D claim order)
+  uint8_t covt[64 * 64];
 };
 
-// fused-NW scratch inside the overlay: sim tile [64][64] f64, row buffer, directions
-constexpr size_t kNwTileBytes = 64 * 64 * 8;
-constexpr size_t kNwRowBytes = 66 * 8;
-constexpr size_t kNwDirBytes = 65 * 5 * 4;
-
-__host__ __device__ inline size_t pair_smem_layout(unsigned char *base, int cap_u, int hash_bits, int cap_t,
-                                                   PairSmem *s) {
-  size_t o = 0;
-  auto take = [&](size_t bytes, size_t al) -> unsigned char * {
-    o = (o + al - 1) / al * al;
-    unsigned char *p = base ? base + o : nullptr;
-    o += bytes;
-    return p;
-  };
-  const size_t slots = (size_t)1 << hash_bits;
-  PairSmem t;
-  // region reused by the fused NW once the score phases are done
-  t.colmask = (uint64_t *)take((size_t)cap_u * 8, 16);
-  t.reachcol = (uint64_t *)take((size_t)cap_u * 8, 16);
-  t.c_m = (uint64_t *)take((size_t)kPairWarps * kSegItems * 8, 16);
-  t.c_p = (double *)take((size_t)kPairWarps * kSegItems * 8, 16);
-  t.bloom = (uint32_t *)take(((size_t)1 << kBloomBits) / 8, 16);
-  t.keys = (int32_t *)take(slots * 4, 16);
-  t.dense = (int16_t *)take(slots * 2, 4);
-  t.tgt_d = (int16_t *)take((size_t)cap_t * 2, 4);
-  t.seen = (uint32_t *)take((size_t)kPairWarps * 32 * 4, 16);
-  t.overlay_bytes = o;
-  // live until the end
-  t.src_off = (int64_t *)take(64 * 8, 16);
-  t.tgt_off = (int64_t *)take(64 * 8, 16);
-  t.src_len = (int32_t *)take(64 * 4, 4);
-  t.src_uniq = (int32_t *)take(64 * 4, 4);
-  t.src_chars = (int32_t *)take(64 * 4, 4);
-  t.tgt_len = (int32_t *)take(64 * 4, 4);
-  t.tgt_uniq = (int32_t *)take(64 * 4, 4);
-  t.tgt_chars = (int32_t *)take(64 * 4, 4);
-  t.tgt_occ0 = (int32_t *)take(65 * 4, 4);
-  t.misc = (int32_t *)take(8 * 4, 4);
-  t.src_order = (uint8_t *)take(64, 4);
-  t.covt = (uint8_t *)take(64 * 64, 4);
-  if (s) *s = t;
-  return (o + 15) / 16 * 16;
-}
+constexpr size_t kPairSmemBytes = sizeof(PairSmem);
 
 // lane j of the result holds bit k = bit j of lane k's x (32x32 bit transpose)
 __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
@@ -161,42 +118,67 @@ __device__ __forceinline__ uint32_t bloom_bit(int32_t key) {
   return ((uint32_t)key * 0x85EBCA6Bu) >> (32 - kBloomBits);
 }
 
-__device__ __forceinline__ int pk_find(const int32_t *keys, const int16_t *dense, int bits, int32_t key) {
-  const uint32_t mask = (1u << bits) - 1u;
-  uint32_t slot = hash_slot(key, 32 - bits);
+__device__ __forceinline__ bool bloom_has(const uint32_t *bloom, int32_t key) {
+  const uint32_t b = bloom_bit(key);
+  return (bloom[b >> 5] >> (b & 31)) & 1u;
+}
+
+// The chunk's target hash: 512 buckets of four 64-bit slots (token << 32 |
+// dense id; empty = all ones).  A slot is only ever claimed as the first
+// empty slot of its bucket, so the filled slots of a bucket are a prefix:
+// a lookup reads its bucket with two 16-byte loads and takes the first
+// slot whose token matches -- either the key's slot, or (key -1 only) the
+// first empty slot, whose id field reads -1 = absent.  A full bucket
+// without the key continues in the next one (rare at <= 1024 keys).
+constexpr int kPkBucketBits = kPkHashBits - 2;
+
+__device__ __forceinline__ int pk_find(const unsigned long long *hkey, int32_t key) {
+  uint32_t b = hash_slot(key, 32 - kPkBucketBits);
   while (true) {
-    const int32_t k = keys[slot];
-    if (k == key) return dense[slot];
-    if (k == -1) return -1;
-    slot = (slot + 1u) & mask;
+    const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(hkey + 4 * b);
+    const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(hkey + 4 * b + 2);
+    int d = -2;
+    if ((int32_t)(y.y >> 32) == key) d = (int)(uint32_t)y.y;
+    if ((int32_t)(y.x >> 32) == key) d = (int)(uint32_t)y.x;
+    if ((int32_t)(x.y >> 32) == key) d = (int)(uint32_t)x.y;
+    if ((int32_t)(x.x >> 32) == key) d = (int)(uint32_t)x.x;
+    if (d != -2) return d;
+    if (y.y == kPkEmpty) return -1;
+    b = (b + 1u) & ((1u << kPkBucketBits) - 1u);
   }
 }
 
 // lookup behind the Bloom prefilter (most dictionary translations are absent)
-__device__ __forceinline__ int pk_find_f(const uint32_t *bloom, const int32_t *keys, const int16_t *dense, int bits,
-                                         int32_t key) {
-  const uint32_t b = bloom_bit(key);
-  if (!((bloom[b >> 5] >> (b & 31)) & 1u)) return -1;
-  return pk_find(keys, dense, bits, key);
+__device__ __forceinline__ int pk_find_f(const uint32_t *bloom, const unsigned long long *hkey, int32_t key) {
+  return bloom_has(bloom, key) ? pk_find(hkey, key) : -1;
 }
 
-__device__ __forceinline__ void pk_insert(int32_t *keys, int bits, int32_t key) {
-  const uint32_t mask = (1u << bits) - 1u;
-  uint32_t slot = hash_slot(key, 32 - bits);
+// insert `key` (if absent) and return its dense id.  The thread that finds
+// the bucket's first empty slot draws the id and publishes key and id in
+// one 64-bit CAS, so a reader never sees a key without its id; an id drawn
+// by a thread that loses the CAS to the same key is never used (a hole).
+__device__ __forceinline__ int pk_insert(unsigned long long *hkey, int *counter, int32_t key) {
+  uint32_t b = hash_slot(key, 32 - kPkBucketBits);
+  int d = -1;  // drawn once, kept across attempts
   while (true) {
-    const int32_t k = keys[slot];
-    if (k == key) return;
-    if (k == -1) {
-      const int32_t prev = atomicCAS(&keys[slot], -1, key);
-      if (prev == -1 || prev == key) return;
+    unsigned long long *bk = hkey + 4 * b;
+    int k = 0;
+    for (; k < 4; ++k) {
+      unsigned long long cur = bk[k];
+      if (cur == kPkEmpty) {
+        if (d < 0) d = atomicAdd(counter, 1);
+        const unsigned long long want = ((unsigned long long)(uint32_t)key << 32) | (uint32_t)d;
+        cur = atomicCAS(&bk[k], kPkEmpty, want);
+        if (cur == kPkEmpty) return d;
+      }
+      if ((int32_t)(cur >> 32) == key) return (int)(uint32_t)cur;
     }
-    slot = (slot + 1u) & mask;
+    b = (b + 1u) & ((1u << kPkBucketBits) - 1u);
   }
 }
 
 // (bit != 0 && p > best) ? p : best, as one predicate: the bit test feeds
-// the compare's predicate input (LOP3 + DSETP.AND + two selects; written
-// in C++ the compiler selects twice, four FSELs per half)
+// the compare's predicate input
 __device__ __forceinline__ double max_if_bit(double best, double p, uint32_t bit) {
   double r;
   asm("{\n\t.reg .pred q;\n\t"
@@ -225,6 +207,7 @@ __host__ __device__ inline bool pair_is_small(int n, int m, int max_len) {
 template <bool kFeatures>
 __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  PairSmem &S = *reinterpret_cast<PairSmem *>(smem_raw);
   // CTAs [0, n_tiles) take the 64x64 tiles of large pairs (first, so the
   // long pairs start early), the rest one pair each (pairs larger than
   // 64x64 are skipped there: their tiles cover them)
@@ -254,22 +237,17 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
   if (!is_tile && (Nfull > kPairMax || Mfull > kPairMax)) return;
   // this CTA's block: source sentences [i0, i0 + N), target sentences [j0, j0 + M)
   const int N = min(kPairMax, Nfull - i0), M = min(kPairMax, Mfull - j0);
-  PairSmem S;
-  const int hbits = A.hash_bits;
-  pair_smem_layout(smem_raw, A.cap_u, hbits, A.cap_t, &S);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t s_first = A.b.pair_src[p] + i0, t_first = A.b.pair_tgt[p] + j0;
   const int32_t *__restrict__ tokens = A.b.tokens;
-  const int64_t *__restrict__ row_ptr = A.d.row_ptr;
-  const int32_t *__restrict__ dtgt = A.d.tgt;
-  const double *__restrict__ dprob = A.d.prob;
+  const uint64_t *__restrict__ rowdesc = A.d.rowdesc;
+  const DictEntry *__restrict__ dent = A.d.ent;
   const int64_t n_rows = A.d.n_rows;
-  const int hslots = 1 << hbits;
   // the block's cell (i, j) lives at out[i * Mfull + j]; also the running-sum scratch
   double *__restrict__ out = A.sim + A.b.pair_sim_off[p] + (int64_t)i0 * Mfull + j0;
   uint16_t *__restrict__ aux = A.aux + A.b.pair_sim_off[p] + (int64_t)i0 * Mfull + j0;
 
-  // ---- 0: tables and sentence metadata
+  // ---- 0: sentence metadata
   if (tid < N) {
     S.src_off[tid] = A.b.sent_tok_off[s_first + tid];
     S.src_len[tid] = A.b.sent_len[s_first + tid];
@@ -299,7 +277,7 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
   __syncthreads();
 
   for (int jc0 = 0; jc0 < M;) {
-    // ---- chunk [jc0, jc1): at most cap_t target occurrences
+    // ---- chunk [jc0, jc1): at most kPkCapT target occurrences
     if (warp == 0) {
       int run = 0, end = jc0;
       for (int base = jc0; base < M; base += 32) {
@@ -311,7 +289,7 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           const int y = __shfl_up_sync(kFull, x, o);
           if (lane >= o) x += y;
         }
-        const unsigned ok = __ballot_sync(kFull, j < M && run + x <= A.cap_t);
+        const unsigned ok = __ballot_sync(kFull, j < M && run + x <= kPkCapT);
         const int cnt = __popc(ok);  // lengths >= 0: the fitting lanes are a prefix
         end = base + cnt;
         if (cnt < 32) break;
@@ -323,71 +301,44 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
     int jc1 = S.misc[1];
     while (true) {
       const int nj = jc1 - jc0;
-      if (warp == 0) {  // chunk-local occurrence offsets
-        int run = 0;
-        for (int base = 0; base < nj; base += 32) {
-          const int jj = base + lane;
-          const int v = jj < nj ? S.tgt_len[jc0 + jj] : 0;
-          int x = v;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(kFull, x, o);
-            if (lane >= o) x += y;
-          }
-          if (jj < nj) S.tgt_occ0[jj] = run + x - v;
-          run += __shfl_sync(kFull, x, 31);
-        }
-        if (lane == 0) {
-          S.tgt_occ0[nj] = run;
-          S.misc[0] = 0;
-          S.misc[2] = 0;
-          S.misc[3] = 0;
-        }
+      if (tid == 0) {
+        S.misc[0] = 0;
+        S.misc[2] = 0;
+        S.misc[3] = 0;
       }
-      for (int k = tid; k < hslots; k += kPairThreads) S.keys[k] = -1;
-      for (int k = tid; k < (1 << kBloomBits) / 32; k += kPairThreads) S.bloom[k] = 0u;
+      {  // clear the hash, the masks and the prefilter (16-byte stores)
+        uint4 z = make_uint4(0u, 0u, 0u, 0u);
+        uint4 e = make_uint4(~0u, ~0u, ~0u, ~0u);
+        uint4 *hk = reinterpret_cast<uint4 *>(S.hkey);
+        for (int k = tid; k < kPkSlots / 2; k += kPairThreads) hk[k] = e;
+        uint4 *cm = reinterpret_cast<uint4 *>(S.colmask);
+        for (int k = tid; k < kPkCapU / 2; k += kPairThreads) cm[k] = z;
+        uint4 *rc = reinterpret_cast<uint4 *>(S.reachcol);
+        for (int k = tid; k < kPkCapU / 2; k += kPairThreads) rc[k] = z;
+        uint4 *bl = reinterpret_cast<uint4 *>(S.bloom);
+        for (int k = tid; k < (1 << kBloomBits) / 128; k += kPairThreads) bl[k] = z;
+      }
       __syncthreads();
-      // ---- A1: insert the chunk's target tokens (+ prefilter bits)
+      // ---- A: insert the chunk's target tokens: dense id, colmask bit, prefilter bit
       for (int jj = warp; jj < nj; jj += kPairWarps) {
         const int64_t off = S.tgt_off[jc0 + jj];
         const int L = S.tgt_len[jc0 + jj];
+        uint32_t *cw = reinterpret_cast<uint32_t *>(S.colmask) + (jj >> 5);
+        const uint32_t jbit = 1u << (jj & 31);
         for (int k = lane; k < L; k += 32) {
           const int32_t t = tokens[off + k];
-          pk_insert(S.keys, hbits, t);
+          const int d = pk_insert(S.hkey, &S.misc[0], t);
+          if (d < kPkCapU) atomicOr(cw + 2 * d, jbit);
           const uint32_t b = bloom_bit(t);
           atomicOr(&S.bloom[b >> 5], 1u << (b & 31));
         }
       }
       __syncthreads();
-      // ---- A2: dense ids
-      for (int k = tid; k < hslots; k += kPairThreads) {
-        if (S.keys[k] != -1) {
-          const int d = atomicAdd(&S.misc[0], 1);
-          if (d < A.cap_u) {
-            S.dense[k] = (int16_t)d;
-            S.colmask[d] = 0ull;
-            S.reachcol[d] = 0ull;
-          }
-        }
-      }
-      __syncthreads();
-      if (S.misc[0] <= A.cap_u || nj == 1) break;
+      if (S.misc[0] <= kPkCapU || nj == 1) break;
       jc1 = jc0 + nj / 2;  // too many distinct tokens: halve the chunk
       __syncthreads();
     }
     const int nj = jc1 - jc0;
-    // ---- A3: occurrences -> dense id, sentence sets
-    for (int jj = warp; jj < nj; jj += kPairWarps) {
-      const int64_t off = S.tgt_off[jc0 + jj];
-      const int L = S.tgt_len[jc0 + jj];
-      const int q0 = S.tgt_occ0[jj];
-      for (int k = lane; k < L; k += 32) {
-        const int d = pk_find(S.keys, S.dense, hbits, tokens[off + k]);
-        S.tgt_d[q0 + k] = (int16_t)d;
-        or64(&S.colmask[d], 1ull << jj);
-      }
-    }
-    __syncthreads();
     // ---- D: source side, warps take sentences dynamically
     {
       // phase D's lane id, read once (%laneid) and opaque to ptxas like
@@ -399,9 +350,9 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
       // in a register rather than being re-derived from %tid in the loops
       int cbase;
       asm volatile("mov.u32 %0, %1;" : "=r"(cbase) : "r"(warp * kSegItems));
-      uint64_t *cm = S.c_m + cbase;
-      uint32_t *seen = S.seen + warp * 32;
-      double *cp = S.c_p + cbase;
+      uint64_t *cm = &S.c_m[0][0] + cbase;
+      uint32_t *seen = S.seen[warp];
+      double *cp = &S.c_p[0][0] + cbase;
       const int jlo = lane, jhi = lane + 32;
       const unsigned lt_mask = (1u << lane) - 1u;
       // software pipeline: the next segment's window (token, dictionary row)
@@ -426,15 +377,16 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
       int64_t e0_w = 0;
       int rl_w = 0;
       if (s_w >= 0 && s_w < n_rows) {
-        e0_w = row_ptr[s_w];
-        rl_w = (int)(row_ptr[s_w + 1] - e0_w);
+        const uint64_t rd = rowdesc[s_w];
+        e0_w = (int64_t)(rd >> 24);
+        rl_w = (int)(rd & 0xFFFFFFull);
       }
       while (i < N) {
         const int L = S.src_len[i];
         const unsigned long long ibit = 1ull << i;
         int cov_lo = 0, cov_hi = 0, sh_lo = 0, sh_hi = 0;
         double sum_lo = 0.0, sum_hi = 0.0;
-        seen[lane] = 0u;  // (cap_u = 1024 dense ids: 32 words)
+        seen[lane] = 0u;  // (kPkCapU = 1024 dense ids: 32 words)
         __syncwarp();
         for (int seg = 0; seg < L;) {
           const int k = seg + lane;
@@ -482,9 +434,9 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
               const int64_t oeb = __shfl_sync(kFull, eb, owner);
               w_owner[st] = owner;
               if (it < items) {
-                const int64_t e = oeb + it;
-                w_tgt[st] = dtgt[e];
-                w_p[st] = dprob[e];
+                const DictEntry en = dent[oeb + it];
+                w_tgt[st] = en.t;
+                w_p[st] = en.p;
               }
             }
           }
@@ -493,7 +445,7 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           const int32_t tok_nx = more ? load_tok(i, seg + cnt) : load_tok(i_nxt, 0);
           // shared tokens: first occurrence of a source token that is a chunk
           // token (one lane of each distinct dense id claims its seen bit)
-          const int ds = in_seg ? pk_find_f(S.bloom, S.keys, S.dense, hbits, s) : -1;
+          const int ds = in_seg ? pk_find_f(S.bloom, S.hkey, s) : -1;
           bool first = false;
           if (ds >= 0) {
             const uint32_t bit = 1u << (ds & 31);
@@ -515,9 +467,13 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
             for (int base = 0; base < rl0; base += 32) {
               const int it = base + lane;
               int d = -1;
-              if (it < rl0) d = pk_find_f(S.bloom, S.keys, S.dense, hbits, dtgt[r0 + it]);
+              double pr = 0.0;
+              if (it < rl0) {
+                const DictEntry en = dent[r0 + it];
+                d = pk_find_f(S.bloom, S.hkey, en.t);
+                pr = en.p;
+              }
               const uint64_t m = d >= 0 ? S.colmask[d] : 0ull;
-              const double pr = d >= 0 ? dprob[r0 + it] : 0.0;
               if (d >= 0) or64(&S.reachcol[d], ibit);
               unsigned bal = __ballot_sync(kFull, d >= 0);
               while (bal) {
@@ -540,8 +496,9 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
             e0_w = 0;
             rl_w = 0;
             if (s_w >= 0 && s_w < n_rows) {
-              e0_w = row_ptr[s_w];
-              rl_w = (int)(row_ptr[s_w + 1] - e0_w);
+              const uint64_t rd = rowdesc[s_w];
+              e0_w = (int64_t)(rd >> 24);
+              rl_w = (int)(rd & 0xFFFFFFull);
             }
             seg += 1;  // cnt == 1 here
             continue;
@@ -576,12 +533,12 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
               tg = -1;
               pr = 0.0;
               if (it < items) {
-                const int64_t e = oeb + it;
-                tg = dtgt[e];
-                pr = dprob[e];
+                const DictEntry en = dent[oeb + it];
+                tg = en.t;
+                pr = en.p;
               }
             }
-            const int d = tg >= 0 ? pk_find_f(S.bloom, S.keys, S.dense, hbits, tg) : -1;
+            const int d = tg >= 0 ? pk_find_f(S.bloom, S.hkey, tg) : -1;
             const bool pres = d >= 0;
             const unsigned bal = __ballot_sync(kFull, pres);
             const unsigned below = bal & lt_mask;
@@ -602,8 +559,9 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           e0_w = 0;
           rl_w = 0;
           if (s_w >= 0 && s_w < n_rows) {
-            e0_w = row_ptr[s_w];
-            rl_w = (int)(row_ptr[s_w + 1] - e0_w);
+            const uint64_t rd = rowdesc[s_w];
+            e0_w = (int64_t)(rd >> 24);
+            rl_w = (int)(rd & 0xFFFFFFull);
           }
           __syncwarp();
           // occurrence-major, in order: max p over the occurrence's
@@ -660,8 +618,9 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
           e0_w = 0;
           rl_w = 0;
           if (s_w >= 0 && s_w < n_rows) {
-            e0_w = row_ptr[s_w];
-            rl_w = (int)(row_ptr[s_w + 1] - e0_w);
+            const uint64_t rd = rowdesc[s_w];
+            e0_w = (int64_t)(rd >> 24);
+            rl_w = (int)(rd & 0xFFFFFFull);
           }
         }
         i = i_nxt;  // its first window is already loaded
@@ -675,11 +634,12 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
       if (lane == 0) jj = atomicAdd(&S.misc[3], 1);
       jj = __shfl_sync(kFull, jj, 0);
       if (jj >= nj) break;
-      const int q0 = S.tgt_occ0[jj];
+      const int64_t off = S.tgt_off[jc0 + jj];
       const int L = S.tgt_len[jc0 + jj];
       int c_lo = 0, c_hi = 0;
       for (int seg = 0; seg < L; seg += 32) {
-        const uint64_t r = (seg + lane < L) ? S.reachcol[S.tgt_d[q0 + seg + lane]] : 0ull;
+        // the occurrence's dense id again (every chunk token is in the hash)
+        const uint64_t r = (seg + lane < L) ? S.reachcol[pk_find(S.hkey, tokens[off + seg + lane])] : 0ull;
         c_lo += __popc(transpose32((uint32_t)r, lane));
         c_hi += __popc(transpose32((uint32_t)(r >> 32), lane));
       }
@@ -691,9 +651,17 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
   }
 
   // ---- F: finalize, one cell per thread, coalesced loads/stores
-  const bool fuse_nw = A.nw_matches != nullptr && !is_tile;
-  double *tile = (double *)smem_raw;  // overlay: dead after phase C
   const int cells = N * M;
+  // every integer-ratio term of the block in the tables? (the usual case:
+  // no per-cell range tests)
+  bool in_tables;
+  {
+    bool ok = true;
+    if (tid < N) ok = S.src_len[tid] < kTermDim && S.src_uniq[tid] < kTermDim && S.src_chars[tid] < kCharDim;
+    else if (tid >= 64 && tid - 64 < M)
+      ok = S.tgt_len[tid - 64] < kTermDim && S.tgt_uniq[tid - 64] < kTermDim && S.tgt_chars[tid - 64] < kCharDim;
+    in_tables = __syncthreads_and(ok);
+  }
   // cell c = i * M + j, stepped without integer division
   const int di = kPairThreads / M, dj = kPairThreads - di * M;
   int i = tid / M, j = tid - (tid / M) * M;
@@ -701,9 +669,13 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
     const int x = i * kCellStride + j;
     const int64_t o = (int64_t)i * Mfull + j;
     const uint32_t ax = aux[o];
-    const double v = cell_score_t(A.md, A.T, S.src_len[i], S.src_uniq[i], S.src_chars[i], S.tgt_len[j],
-                                  S.tgt_uniq[j], S.tgt_chars[j], (int)(ax & 0xffu), out[o], S.covt[x],
-                                  (int)(ax >> 8), kExpTableDev);
+    const double v =
+        in_tables ? cell_score_t<true>(A.md, A.T, S.src_len[i], S.src_uniq[i], S.src_chars[i], S.tgt_len[j],
+                                       S.tgt_uniq[j], S.tgt_chars[j], (int)(ax & 0xffu), out[o], S.covt[x],
+                                       (int)(ax >> 8), kExpTableDev)
+                  : cell_score_t<false>(A.md, A.T, S.src_len[i], S.src_uniq[i], S.src_chars[i], S.tgt_len[j],
+                                        S.tgt_uniq[j], S.tgt_chars[j], (int)(ax & 0xffu), out[o], S.covt[x],
+                                        (int)(ax >> 8), kExpTableDev);
     if (kFeatures) {  // features_from_profiles (classifier.py:69-97), IEEE divisions
       const int cov = (int)(ax & 0xffu), sh = (int)(ax >> 8), covt = S.covt[x];
       const int Ls = S.src_len[i], Lt = S.tgt_len[j], Us = S.src_uniq[i], Ut = S.tgt_uniq[j];
@@ -716,24 +688,12 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
       f[5] = fdiv((double)sh, (double)(Us > Ut ? Us : Ut));
     }
     out[o] = v;
-    if (fuse_nw) tile[i * 64 + j] = v;
     i += di;
     j += dj;
     if (j >= M) {
       j -= M;
       ++i;
     }
-  }
-  if (!fuse_nw) return;
-  __syncthreads();
-  // ---- NW fill + traceback + threshold filter on the tile (align.py:170-181,
-  //      132-163, 323-332), one warp; the other warps are done
-  if (warp == 0) {
-    double *rowbuf = (double *)(smem_raw + kNwTileBytes);
-    uint32_t *dirs = (uint32_t *)(smem_raw + kNwTileBytes + kNwRowBytes);
-    nw_solve<kNwMine, false>(tile, 64, N, M, A.gap, A.mismatch, A.bonus, A.threshold, nullptr, dirs, rowbuf,
-                             A.nw_matches + A.nw_out_off[p], nullptr, A.nw_counts + p,
-                             A.nw_score ? A.nw_score + p : nullptr);
   }
 }
 

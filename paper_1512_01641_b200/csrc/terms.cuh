@@ -76,24 +76,31 @@ __global__ void build_term_tables(const Model md, double *t0, double *t1, double
 // One cell: features -> margin -> logistic, bit-identical to
 // score_from_margin(margin(features_from_profiles(...))).
 // rct = RN(1/Ct) (used only outside the char table).
+// kInTables: the caller guarantees Ls, Lt, max(Us, Ut) < kTermDim and
+// Cs, Ct < kCharDim (checked once per block), so every integer-ratio term
+// is a table load
+template <bool kInTables = false>
 __device__ __forceinline__ double cell_score_t(const Model &md, const TermTables &T, int Ls, int Us, int Cs, int Lt,
                                                int Ut, int Ct, int cov, double sum, int covt, int sh,
                                                const uint64_t *tab) {
-  const double t0 = (Ls < kTermDim && Lt < kTermDim) ? T.t0[Ls * kTermDim + Lt]
+  const double t0 = (kInTables || (Ls < kTermDim && Lt < kTermDim)) ? T.t0[Ls * kTermDim + Lt]
                                                      : term(md, 0, clip4(fdiv((double)Ls, (double)Lt)));
-  const double t1 = (Ls < kTermDim) ? T.t1[Ls * kTermDim + cov] : term(md, 1, fdiv((double)cov, (double)Ls));
-  const double t2 = (Lt < kTermDim) ? T.t2[Lt * kTermDim + covt] : term(md, 2, fdiv((double)covt, (double)Lt));
+  const double t1 = (kInTables || Ls < kTermDim) ? T.t1[Ls * kTermDim + cov]
+                                                 : term(md, 1, fdiv((double)cov, (double)Ls));
+  const double t2 = (kInTables || Lt < kTermDim) ? T.t2[Lt * kTermDim + covt]
+                                                 : term(md, 2, fdiv((double)covt, (double)Lt));
   double t3;
   if (cov) {
-    const double f3 = (cov < kRecipDim) ? div_cr(sum, (double)cov, T.rc[cov]) : fdiv(sum, (double)cov);
+    const double f3 = (kInTables || cov < kRecipDim) ? div_cr(sum, (double)cov, T.rc[cov]) : fdiv(sum, (double)cov);
     t3 = div_cr(fmul(md.w[3], fsub(f3, md.mean[3])), md.scale[3], T.misc[1]);
   } else {
     t3 = T.misc[0];
   }
-  const double t4 = (Cs < kCharDim && Ct < kCharDim) ? T.t4[Cs * kCharDim + Ct]
+  const double t4 = (kInTables || (Cs < kCharDim && Ct < kCharDim)) ? T.t4[Cs * kCharDim + Ct]
                                                      : term(md, 4, clip4(fdiv((double)Cs, (double)Ct)));
   const int u = Us > Ut ? Us : Ut;
-  const double t5 = (u < kTermDim) ? T.t5[u * kTermDim + sh] : term(md, 5, fdiv((double)sh, (double)u));
+  const double t5 = (kInTables || u < kTermDim) ? T.t5[u * kTermDim + sh]
+                                                : term(md, 5, fdiv((double)sh, (double)u));
   double d = md.bias;
   d = fadd(d, t0);
   d = fadd(d, t1);
