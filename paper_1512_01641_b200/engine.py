@@ -331,47 +331,155 @@ def exp_device(x: np.ndarray) -> np.ndarray:
     return y
 
 
-def tune_device(dd: DeviceDictionary, model_vec: np.ndarray, batch: PackedBatch, thresholds, gaps,
-                mismatch: float, bonus: float, refs: list, stream=None):
-    """Score every pair once, align it under every (threshold, gap) trial in
-    one batched launch (problem = pair * S + trial) and compute each trial's
-    agreement NW on device.  Returns (counts[P*S], matched[P*S]) on host."""
-    torch = _torch()
-    L = N.load()
-    dev = f"cuda:{dd.device}"
-    P, S = batch.n_pairs, len(gaps)
-    sp = stream_ptr(stream)
-    with torch.cuda.device(dd.device):
-        db = DeviceBatch(batch, dd.device)
-        sim = torch.empty(max(batch.n_cells, 1), dtype=torch.float64, device=dev)
-        score_device(dd, model_vec, db, sim, stream)
-        cap = np.minimum(batch.pair_n, batch.pair_m).astype(np.int64)
-        per_problem = np.repeat(cap, S)
-        out_off = np.zeros(P * S, dtype=np.int64)
-        if P * S > 1:
-            np.cumsum(per_problem[:-1], out=out_off[1:])
-        total_cap = int(per_problem.sum())
-        t_off = torch.from_numpy(out_off).to(dev)
-        t_gap = torch.tensor(np.asarray(gaps, dtype=np.float64)).to(dev)
-        t_thr = torch.tensor(np.asarray(thresholds, dtype=np.float64)).to(dev)
-        slots = torch.empty(max(total_cap, 1) * 16, dtype=torch.uint8, device=dev)
-        counts = torch.empty(max(P * S, 1), dtype=torch.int32, device=dev)
-        N.check(L.bimine_nw_mine_batch(sim.data_ptr(), db.t["pair_sim_off"].data_ptr(), db.t["pair_n"].data_ptr(),
-                                       db.t["pair_m"].data_ptr(), P, db.max_n, db.max_m, S, t_gap.data_ptr(),
-                                       t_thr.data_ptr(), mismatch, bonus, t_off.data_ptr(), slots.data_ptr(),
-                                       counts.data_ptr(), None, sp))
+class DeviceTuner:
+    """The tuning sweep's device state, kept across calls: the device batch
+    and its plan, the score buffer, the per-(pair, trial) match slots, the
+    trial parameters, the reference lists and page-locked staging for the
+    inputs and the two result arrays.  A call uploads the batch from the
+    staging (non-blocking copies on the tuner's stream), scores every pair
+    once, aligns it under every trial in one launch (problem = pair * S +
+    trial), runs the agreement NW on device and reads the results back with
+    one synchronisation."""
+
+    def __init__(self, dd: DeviceDictionary, model_vec: np.ndarray, batch: PackedBatch, thresholds, gaps,
+                 mismatch: float, bonus: float, refs: list, stream=None):
+        torch = _torch()
+        self.torch = torch
+        self.dd = dd
+        self.device = dd.device
+        self.batch = batch
+        self.model = np.ascontiguousarray(model_vec, dtype=np.float64)
+        self.mismatch, self.bonus = float(mismatch), float(bonus)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        dev = f"cuda:{self.device}"
+        P, S = batch.n_pairs, len(gaps)
+        self.P, self.S = P, S
+        with torch.cuda.device(self.device):
+            # page-locked staging of every input array; the device copies
+            self.host = {f: torch.empty(max(getattr(batch, f).shape[0], 1), dtype=_torch_dtype(getattr(batch, f)),
+                                        pin_memory=True) for f in _FIELDS}
+            self.db = DeviceBatch(batch, self.device)
+            self.sim = torch.empty(max(batch.n_cells, 1), dtype=torch.float64, device=dev)
+            cap = np.minimum(batch.pair_n, batch.pair_m).astype(np.int64)
+            self.cap_max = int(cap.max(initial=1))
+            per_problem = np.repeat(cap, S)
+            out_off = np.zeros(P * S, dtype=np.int64)
+            if P * S > 1:
+                np.cumsum(per_problem[:-1], out=out_off[1:])
+            self.t_off = torch.from_numpy(out_off).to(dev)
+            self.trials = (np.asarray(thresholds, dtype=np.float64).copy(), np.asarray(gaps, dtype=np.float64).copy())
+            self.t_gap = torch.from_numpy(self.trials[1]).to(dev)
+            self.t_thr = torch.from_numpy(self.trials[0]).to(dev)
+            self.slots = torch.empty(max(int(per_problem.sum()), 1) * 16, dtype=torch.uint8, device=dev)
+            self.counts = torch.empty(max(P * S, 1), dtype=torch.int32, device=dev)
+            self.matched = torch.empty(max(P * S, 1), dtype=torch.int32, device=dev)
+            self.h_counts = torch.empty(max(P * S, 1), dtype=torch.int32, pin_memory=True)
+            self.h_matched = torch.empty(max(P * S, 1), dtype=torch.int32, pin_memory=True)
+            self._refs = None
+            self.set_refs(refs)
+
+    def fits(self, batch: PackedBatch, n_settings: int) -> bool:
+        """Same shapes as the tuner's batch (its plan and slot offsets hold)."""
+        b = self.batch
+        return (batch is b) or (
+            n_settings == self.S and batch.n_pairs == b.n_pairs and batch.n_sentences == b.n_sentences
+            and batch.n_tokens == b.n_tokens and np.array_equal(batch.pair_n, b.pair_n)
+            and np.array_equal(batch.pair_m, b.pair_m) and np.array_equal(batch.sent_len, b.sent_len)
+            and np.array_equal(batch.pair_sim_off, b.pair_sim_off))
+
+    def set_refs(self, refs: list) -> None:
+        if refs is self._refs:
+            return
+        self._refs = refs
+        torch = self.torch
+        dev = f"cuda:{self.device}"
+        P = self.P
         ref_len = np.array([len(r) for r in refs], dtype=np.int32)
         ref_off = np.zeros(P, dtype=np.int64)
         if P > 1:
             np.cumsum(ref_len[:-1].astype(np.int64), out=ref_off[1:])
         ref_ij = np.fromiter(itertools.chain.from_iterable(itertools.chain.from_iterable(refs)), dtype=np.int32,
                              count=2 * int(ref_len.sum()))
-        t_rij = torch.from_numpy(ref_ij if ref_ij.size else np.zeros(2, np.int32)).to(dev)
-        t_roff = torch.from_numpy(ref_off).to(dev)
-        t_rlen = torch.from_numpy(ref_len).to(dev)
-        matched = torch.empty(max(P * S, 1), dtype=torch.int32, device=dev)
-        N.check(L.bimine_agreement_batch(slots.data_ptr(), t_off.data_ptr(), counts.data_ptr(), P, S,
-                                         t_rij.data_ptr(), t_roff.data_ptr(), t_rlen.data_ptr(),
-                                         int(cap.max(initial=1)), int(ref_len.max(initial=1)), matched.data_ptr(),
-                                         sp))
-        return counts[: P * S].cpu().numpy(), matched[: P * S].cpu().numpy()
+        self.ref_max = int(ref_len.max(initial=1))
+        self.t_rij = torch.from_numpy(ref_ij if ref_ij.size else np.zeros(2, np.int32)).to(dev)
+        self.t_roff = torch.from_numpy(ref_off).to(dev)
+        self.t_rlen = torch.from_numpy(ref_len).to(dev)
+
+    def set_trials(self, thresholds, gaps) -> None:
+        thr = np.asarray(thresholds, dtype=np.float64)
+        gp = np.asarray(gaps, dtype=np.float64)
+        if np.array_equal(thr, self.trials[0]) and np.array_equal(gp, self.trials[1]):
+            return
+        self.trials = (thr.copy(), gp.copy())
+        with self.torch.cuda.stream(self.stream):
+            self.t_thr.copy_(self.torch.from_numpy(self.trials[0]))
+            self.t_gap.copy_(self.torch.from_numpy(self.trials[1]))
+
+    def upload(self, batch: PackedBatch) -> None:
+        """The batch's arrays into the staging, then non-blocking H2D copies
+        on the tuner's stream (same shapes as the tuner's batch)."""
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            for f in _FIELDS:
+                a = getattr(batch, f)
+                h = self.host[f]
+                if a.shape[0]:
+                    h[: a.shape[0]].numpy()[:] = a
+                    self.db.t[f][: a.shape[0]].copy_(h[: a.shape[0]], non_blocking=True)
+
+    def run_device(self, events=None) -> None:
+        """Enqueue score -> NW (all trials) -> agreement on the stream."""
+        L = N.load()
+        sp = stream_ptr(self.stream)
+        db = self.db
+        if events:
+            events[0].record(self.stream)
+        score_device(self.dd, self.model, db, self.sim, self.stream)
+        if events:
+            events[1].record(self.stream)
+        N.check(L.bimine_nw_mine_batch(self.sim.data_ptr(), db.t["pair_sim_off"].data_ptr(),
+                                       db.t["pair_n"].data_ptr(), db.t["pair_m"].data_ptr(), self.P, db.max_n,
+                                       db.max_m, self.S, self.t_gap.data_ptr(), self.t_thr.data_ptr(), self.mismatch,
+                                       self.bonus, self.t_off.data_ptr(), self.slots.data_ptr(),
+                                       self.counts.data_ptr(), None, sp))
+        if events:
+            events[2].record(self.stream)
+        N.check(L.bimine_agreement_batch(self.slots.data_ptr(), self.t_off.data_ptr(), self.counts.data_ptr(),
+                                         self.P, self.S, self.t_rij.data_ptr(), self.t_roff.data_ptr(),
+                                         self.t_rlen.data_ptr(), self.cap_max, self.ref_max,
+                                         self.matched.data_ptr(), sp))
+        if events:
+            events[3].record(self.stream)
+
+    def results(self):
+        """D2H of counts and agreements (one synchronisation)."""
+        n = self.P * self.S
+        with self.torch.cuda.stream(self.stream):
+            self.h_counts[:n].copy_(self.counts[:n], non_blocking=True)
+            self.h_matched[:n].copy_(self.matched[:n], non_blocking=True)
+        self.stream.synchronize()
+        return self.h_counts[:n].numpy().copy(), self.h_matched[:n].numpy().copy()
+
+
+def _torch_dtype(a: np.ndarray):
+    torch = _torch()
+    return {np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64}[a.dtype]
+
+
+def tune_device(dd: DeviceDictionary, model_vec: np.ndarray, batch: PackedBatch, thresholds, gaps,
+                mismatch: float, bonus: float, refs: list, stream=None, tuner: DeviceTuner | None = None):
+    """Score every pair once, align it under every (threshold, gap) trial in
+    one batched launch (problem = pair * S + trial) and compute each trial's
+    agreement NW on device.  Returns (counts[P*S], matched[P*S]) on host.
+
+    `tuner`: a DeviceTuner built for this batch's shapes (a caller sweeping
+    repeatedly keeps one); its device buffers and plan are reused and the
+    inputs are uploaded again from its page-locked staging."""
+    if tuner is None or tuner.dd is not dd or not tuner.fits(batch, len(gaps)):
+        tuner = DeviceTuner(dd, model_vec, batch, thresholds, gaps, mismatch, bonus, refs, stream=stream)
+    else:
+        tuner.upload(batch)
+        tuner.set_refs(refs)
+        tuner.set_trials(thresholds, gaps)
+    tuner.run_device()
+    return tuner.results()

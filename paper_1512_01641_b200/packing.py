@@ -224,17 +224,13 @@ class PackedBatch:
     def select(self, pairs: Sequence[int] | np.ndarray) -> "PackedBatch":
         """Sub-batch of the given pairs (order kept), re-packed contiguously."""
         pairs = np.asarray(pairs, dtype=np.int64)
-        sent_idx = []
-        for p in pairs.tolist():
-            sent_idx.append(np.arange(self.pair_src[p], self.pair_src[p] + self.pair_n[p]))
-            sent_idx.append(np.arange(self.pair_tgt[p], self.pair_tgt[p] + self.pair_m[p]))
-        sent_idx = np.concatenate(sent_idx) if sent_idx else np.zeros(0, np.int64)
-        lens = self.sent_len[sent_idx]
-        tok_idx = np.concatenate(
-            [np.arange(self.sent_tok_off[s], self.sent_tok_off[s] + self.sent_len[s]) for s in sent_idx.tolist()]
-        ) if sent_idx.size else np.zeros(0, np.int64)
         pn = self.pair_n[pairs].astype(np.int64)
         pm = self.pair_m[pairs].astype(np.int64)
+        # per pair: its source sentences, then its target sentences
+        sent_idx = _ranges(np.stack([self.pair_src[pairs], self.pair_tgt[pairs]], axis=1).ravel(),
+                           np.stack([pn, pm], axis=1).ravel())
+        lens = self.sent_len[sent_idx]
+        tok_idx = _ranges(self.sent_tok_off[sent_idx], lens)
         starts = np.zeros(pairs.shape[0], dtype=np.int64)
         if pairs.shape[0] > 1:
             np.cumsum((pn + pm)[:-1], out=starts[1:])
@@ -242,6 +238,17 @@ class PackedBatch:
             self.tokens[tok_idx], lens, self.sent_chars[sent_idx],
             starts, pn, starts + pn, pm, sent_uniq=self.sent_uniq[sent_idx],
         )
+
+
+def _ranges(starts, lens) -> np.ndarray:
+    """concatenate(arange(s, s + l) for s, l in zip(starts, lens)), vectorised."""
+    lens = np.asarray(lens, dtype=np.int64)
+    total = int(lens.sum())
+    if total == 0:
+        return np.zeros(0, dtype=np.int64)
+    first = np.zeros(lens.shape[0], dtype=np.int64)
+    np.cumsum(lens[:-1], out=first[1:])
+    return np.repeat(np.asarray(starts, dtype=np.int64) - first, lens) + np.arange(total, dtype=np.int64)
 
 
 def unique_counts(tokens: np.ndarray, sent_len: np.ndarray) -> np.ndarray:

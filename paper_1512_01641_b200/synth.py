@@ -33,7 +33,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .packing import PackedBatch
+from .packing import PackedBatch, _ranges
 
 # BASELINE.json configs (index = config number - 1)
 CONFIGS = {
@@ -133,7 +133,19 @@ def make_dictionary(rng: np.random.Generator, n_words: int) -> SynthDictionary:
 class SynthCorpus:
     dictionary: SynthDictionary
     batch: PackedBatch
-    reference: list  # per pair: list of (i, j) true-translation indices
+    # true-translation index pairs: pair p's (i, j) are ref_i/ref_j[ref_off[p]:ref_off[p + 1]]
+    ref_off: np.ndarray
+    ref_i: np.ndarray
+    ref_j: np.ndarray
+    _reference: list | None = field(default=None, repr=False)
+
+    @property
+    def reference(self) -> list:
+        """per pair: list of (i, j) true-translation indices"""
+        if self._reference is None:
+            ii, jj, off = self.ref_i.tolist(), self.ref_j.tolist(), self.ref_off.tolist()
+            self._reference = [list(zip(ii[off[p]: off[p + 1]], jj[off[p]: off[p + 1]])) for p in range(len(off) - 1)]
+        return self._reference
 
     def sentence_text(self, sent: int) -> str:
         b = self.batch
@@ -202,7 +214,7 @@ def make_corpus(
     # ---- translations of the flagged sentences (token level) ----
     tr_idx = np.flatnonzero(flag)
     tr_len = src_len[tr_idx]
-    gather = np.concatenate([np.arange(src_off[i], src_off[i + 1]) for i in tr_idx]) if tr_idx.size else np.zeros(0, np.int64)
+    gather = _ranges(src_off[tr_idx], tr_len)
     w = src_tok[gather]
     is_src_word = w < S
     r = rng.random(w.shape[0])
@@ -236,49 +248,45 @@ def make_corpus(
     un_tok = _with_shared(rng, S + d.tau[_zipf_words(rng, int(un_len.sum()), S)], d)
     un_off = np.concatenate([[0], np.cumsum(un_len)])
 
-    # ---- assemble: per pair, N source sentences then M target sentences
+    # ---- assemble: per pair, N source sentences then M target sentences;
+    # the pair's translated sentences take the target slots with the k
+    # smallest keys (k = its translated count), in slot order
     slot_keys = rng.random(int(m.sum()))
-    tok_parts, len_parts = [], []
-    reference = []
-    pair_src = np.zeros(n_pairs, dtype=np.int64)
-    pair_tgt = np.zeros(n_pairs, dtype=np.int64)
-    sent_cursor = 0
-    tr_cursor = 0
-    un_cursor = 0
-    key_cursor = 0
-    for p in range(n_pairs):
-        np_, mp = int(n[p]), int(m[p])
-        s0 = int(first_src[p])
-        pair_src[p] = sent_cursor
-        tok_parts.append(src_tok[src_off[s0] : src_off[s0 + np_]])
-        len_parts.append(src_len[s0 : s0 + np_])
-        sent_cursor += np_
-        pair_tgt[p] = sent_cursor
-        k = int(n_tr[p])
-        keys = slot_keys[key_cursor : key_cursor + mp]
-        key_cursor += mp
-        slots = np.sort(np.argsort(keys, kind="stable")[:k])
-        is_tr = np.zeros(mp, dtype=bool)
-        is_tr[slots] = True
-        src_local = np.flatnonzero(flag[s0 : s0 + np_])
-        reference.append(list(zip(src_local.tolist(), slots.tolist())))
-        lens = np.empty(mp, dtype=np.int64)
-        for jj in range(mp):
-            if is_tr[jj]:
-                a, b_ = tr_out_off[tr_cursor], tr_out_off[tr_cursor + 1]
-                tok_parts.append(out_tok[a:b_])
-                lens[jj] = b_ - a
-                tr_cursor += 1
-            else:
-                a, b_ = un_off[un_cursor], un_off[un_cursor + 1]
-                tok_parts.append(un_tok[a:b_])
-                lens[jj] = b_ - a
-                un_cursor += 1
-        len_parts.append(lens)
-        sent_cursor += mp
+    pair_of_slot = np.repeat(np.arange(n_pairs), m)
+    slot_first = np.concatenate([[0], np.cumsum(m)[:-1]])
+    order = np.lexsort((slot_keys, pair_of_slot))  # by pair, then key
+    rank = np.empty(order.shape[0], dtype=np.int64)
+    rank[order] = np.arange(order.shape[0]) - slot_first[pair_of_slot[order]]
+    is_tr = rank < n_tr[pair_of_slot]
+    # the t-th translated slot of a pair gets the pair's t-th translation,
+    # the u-th unrelated slot its u-th unrelated sentence
+    tr_before = np.cumsum(is_tr) - is_tr
+    un_before = np.cumsum(~is_tr) - (~is_tr)
+    # source sentences of the flagged kind, in order, per pair = tr_idx order
+    tgt_start = np.where(is_tr, tr_out_off[np.minimum(tr_before, tr_idx.size)],
+                         (int(tr_out_off[-1]) + un_off[np.minimum(un_before, n_unrel)]))
+    tgt_len = np.where(is_tr, tr_out_len[np.minimum(tr_before, max(tr_idx.size - 1, 0))] if tr_idx.size else 0,
+                       un_len[np.minimum(un_before, max(n_unrel - 1, 0))] if n_unrel else 0)
+    # sentence order: pair p's N source sentences, then its M target slots
+    sent_pair = np.concatenate([np.repeat(np.arange(n_pairs), n), pair_of_slot])
+    sent_kind = np.concatenate([np.zeros(ns, dtype=np.int64), np.ones(int(m.sum()), dtype=np.int64)])
+    sent_start = np.concatenate([src_off[:-1], int(src_off[-1]) + tgt_start])
+    sent_len_all = np.concatenate([src_len, tgt_len])
+    sent_order = np.lexsort((sent_kind, sent_pair))  # stable within (pair, kind): source order, slot order
+    sent_len = sent_len_all[sent_order]
+    pool = np.concatenate([src_tok, out_tok, un_tok])
+    tokens = pool[_ranges(sent_start[sent_order], sent_len)]
+    pair_src = np.concatenate([[0], np.cumsum(n + m)[:-1]]).astype(np.int64)
+    pair_tgt = pair_src + n
+    # reference: (local source index of each flagged sentence, its slot)
+    ref_cnt = n_tr
+    ref_off = np.concatenate([[0], np.cumsum(ref_cnt)]).astype(np.int64)
+    ref_i = (tr_idx - first_src[pair_of_src[tr_idx]]).astype(np.int64)
+    tr_slots = np.flatnonzero(is_tr)
+    ref_j = (tr_slots - slot_first[pair_of_slot[tr_slots]]).astype(np.int64)
 
-    tokens = np.concatenate(tok_parts).astype(np.int32)
-    sent_len = np.concatenate(len_parts).astype(np.int32)
+    tokens = tokens.astype(np.int32)
+    sent_len = sent_len.astype(np.int32)
     batch = PackedBatch.from_token_lengths(
         tokens,
         sent_len,
@@ -288,7 +296,7 @@ def make_corpus(
         pair_tgt=pair_tgt,
         pair_m=m.astype(np.int32),
     )
-    return SynthCorpus(dictionary=d, batch=batch, reference=reference)
+    return SynthCorpus(dictionary=d, batch=batch, ref_off=ref_off, ref_i=ref_i, ref_j=ref_j)
 
 
 def _chars(tokens: np.ndarray, sent_len: np.ndarray, d: SynthDictionary) -> np.ndarray:
