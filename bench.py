@@ -482,6 +482,72 @@ def time_e2e(R, dd, model, batch, steps, warmup, stream, gap, thr, mism, bonus):
     return e2e_s, n_steps, h2d, d2h
 
 
+def time_e2e_pageable(R, dd, model, batch, n_steps, stream, gap, thr, mism, bonus):
+    """bimine_mine_host on the generator's own (pageable) numpy arrays: the
+    library stages them through page-locked memory itself."""
+    from paper_1512_01641_b200 import engine as E
+
+    outbuf = {}
+    E.mine_host(dd, model, batch, gap, thr, mism, bonus, stream=stream, out=outbuf)
+    R.torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n_steps):
+        E.mine_host(dd, model, batch, gap, thr, mism, bonus, stream=stream, out=outbuf)
+    return time.perf_counter() - t0
+
+
+def api_e2e(corpus, reps: int = 2):
+    """The north-star interface end to end: align.mine_corpus from
+    DocumentPairs (sentence text) to (score, src, tgt) rows, host
+    tokenisation included, with a per-stage breakdown."""
+    from paper_1512_01641_b200 import align as A
+    from paper_1512_01641_b200 import engine as E
+    from paper_1512_01641_b200.classifier import load_model
+    from paper_1512_01641_b200.corpus import Document, DocumentPair
+    from paper_1512_01641_b200.lexicon import Lexicon
+    from paper_1512_01641_b200.packing import BatchBuilder
+
+    b = corpus.batch
+    sents = corpus.all_sentences()
+    pairs = []
+    for p in range(b.n_pairs):
+        s0, n, t0, m = int(b.pair_src[p]), int(b.pair_n[p]), int(b.pair_tgt[p]), int(b.pair_m[p])
+        pairs.append(DocumentPair(f"t{p}", Document(f"s{p}", "pl", str(p), tuple(sents[s0:s0 + n])),
+                                  Document(f"d{p}", "en", str(p), tuple(sents[t0:t0 + m]))))
+    lex = Lexicon(corpus.dictionary.table())
+    model = load_model(os.path.join(REPO, "tests", "golden", "synth_model.json"))
+    cfg = A.MiningConfig()
+    A.mine_corpus(model, lex, pairs[:64], cfg)  # lexicon upload, vocabulary, CUDA context: once per lexicon
+    walls = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = A.mine_corpus(model, lex, pairs, cfg)
+        walls.append(time.perf_counter() - t0)
+    wall = min(walls)
+    # stages, timed separately on the same input
+    ctx = E.lexicon_context(lex)
+    t0 = time.perf_counter()
+    builder = BatchBuilder(ctx.vocab)
+    builder.add_pairs([(p.source.sentences, p.target.sentences) for p in pairs])
+    batch = builder.build()
+    t_pack = time.perf_counter() - t0
+    dd = ctx.on(E.current_device())
+    from paper_1512_01641_b200.classifier import model_vector
+
+    mv = model_vector(model)
+    t0 = time.perf_counter()
+    E.mine_host(dd, mv, batch, cfg.gap_penalty, cfg.threshold, cfg.mismatch_cost, cfg.match_bonus)
+    t_mine = time.perf_counter() - t0
+    return {
+        "value": b.n_pairs / wall, "unit": UNIT, "pairs": b.n_pairs, "rows": len(out.rows),
+        "path": "align.mine_corpus(model, lexicon, DocumentPairs, MiningConfig()) -> MiningOutcome rows "
+                "(score, source sentence, target sentence)",
+        "host_cores": os.cpu_count(),
+        "stages_s": {"tokenize_pack": t_pack, "mine_host_pageable": t_mine,
+                     "rows_and_rest": max(0.0, wall - t_pack - t_mine), "total": wall},
+    }
+
+
 def run_gpu(args):
     """C1/C2/C3 (weak: every rank its own batch) and C5 (strong: 1M pairs
     split by N*M)."""
@@ -519,12 +585,15 @@ def run_gpu(args):
     del flush
     step_ms = mine_ms + compact_ms
     e2e = None
+    e2e_pg = 0.0
     if not args.no_e2e:
         e2e_s, e2e_steps, h2d, d2h = time_e2e(R, dd, model, batch, K, args.warmup, stream, gap, thr, mism, bonus)
+        if not strong:
+            e2e_pg = time_e2e_pageable(R, dd, model, batch, e2e_steps, stream, gap, thr, mism, bonus)
     else:
         e2e_s, e2e_steps, h2d, d2h = 0.0, 0, 0, 0
     per = R.gather([step_ms, mine_ms, nw_ms, score_ms, e2e_s, float(batch.n_pairs), float(batch.n_cells),
-                    float(total_matches)])
+                    float(total_matches), e2e_pg])
     R.barrier()
     if R.rank != 0:
         R.close()
@@ -545,6 +614,10 @@ def run_gpu(args):
                     "output buffers" + ("; per rank: the shared base sentences + its pair descriptors" if strong
                                        else ""),
         }
+        if e2e_pg:
+            e2e["pageable_inputs"] = {"value": pairs_all * e2e_steps / max(cols[8]),
+                                      "path": "bimine_mine_host on the generator's pageable numpy arrays (staged "
+                                              "through page-locked memory inside the library)"}
     plan = db.plan
     nw_launches = (1 if plan.n_large < batch.n_pairs else 0) + (3 if plan.n_large else 0)
     launches_per_step = 1 + (plan.n_long > 0) + nw_launches + 2
@@ -552,6 +625,9 @@ def run_gpu(args):
     if R.world == 1 and not strong:
         roofline = _roofline(algorithmic_bytes(batch), score_max / K)
         _attach_traffic(roofline, f"C{args.config}:{batch.n_pairs}")
+    api = None
+    if R.world == 1 and not strong and args.config == 2 and not args.no_e2e:
+        api = api_e2e(corpus)
     cpu = None
     if R.world == 1 and not args.no_cpu:
         cpu = cpu_baseline_field(cpu_baselines(2 if strong else args.config, None if strong else args.pairs,
@@ -587,6 +663,7 @@ def run_gpu(args):
                      "cells": [int(c[6]) for c in per]},
         "imbalance": (max(cols[0]) / (sum(cols[0]) / len(cols[0]))) if cols[0] else None,
         "e2e": e2e,
+        "api_e2e": api,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": clocks,
@@ -768,7 +845,7 @@ def run_tuning(args):
 def main(argv=None):
     args = parse(argv)
     rank, world, _ = dist_env()
-    if world > 1 and args.gpus != world:
+    if world > 1 and args.gpus != world and args.impl == "b200":
         sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
         return 2
     if world == 1 and args.gpus > 1 and args.impl == "b200":

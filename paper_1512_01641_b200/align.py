@@ -13,11 +13,11 @@ GPU through libbimine_b200.so:
   kernel, NW + traceback + threshold filter, compaction in input order
   (uploads overlapped with the scoring).
 
-``mine_corpus`` packs all pairs into one batch (pairs whose sentences do
-not tokenise are reported as failures with the reference's message and
-skipped, align.py:396-399/441-447) and shards pairs over
-``min(config.workers, visible GPUs)`` devices; output order is input
-order for every worker count.  The A* engines (align.py:203-320) are not
+``mine_corpus`` tokenises and packs the pairs in chunks (pairs whose
+sentences do not tokenise, or that a device limit rejects, are reported as
+failures with the reference's message and skipped, align.py:396-399/441-447),
+mines chunk k on GPU k mod min(config.workers, visible GPUs) while the next
+chunk is packed; output order is input order for every worker count.  The A* engines (align.py:203-320) are not
 part of the GPU path: requesting them raises ``NotImplementedError``.
 """
 
@@ -31,7 +31,7 @@ import numpy as np
 
 from . import engine as _engine
 from .classifier import model_vector
-from .packing import BatchBuilder, PackedBatch
+from .packing import BatchBuilder, PackedBatch, pack_documents
 
 ENGINES = ("nw", "nw_wavefront", "astar_constrained")
 GPU_ENGINES = ("nw", "nw_wavefront")
@@ -242,60 +242,102 @@ def _shard_bounds(weights: np.ndarray, parts: int) -> list[tuple[int, int]]:
     return [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
 
 
+CHUNK_PAIRS = 16_384  # pairs tokenised / mined per chunk of mine_corpus
+
+
+def _chunk_bounds(n: int, min_chunks: int) -> list[tuple[int, int]]:
+    k = max(min_chunks, -(-n // CHUNK_PAIRS), 1)
+    k = min(k, max(n, 1))
+    cuts = [n * c // k for c in range(k + 1)]
+    return [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+
+
+def _mine_chunk(model, lexicon, pd, config: MiningConfig, device: int, topic_ids, lo: int):
+    """Mine one packed chunk on `device`; returns (rows, failures) of the
+    chunk, rows in input order.  A device-side limit (BimineError) must not
+    abort the corpus: the chunk is then mined pair by pair and the pairs
+    that still fail are reported (align.py:396-399, 441-447)."""
+    import operator
+
+    import torch
+
+    from ._native import BimineError
+
+    keep = np.flatnonzero(pd.ok)
+    failed: dict[int, str] = {}
+    with torch.cuda.device(device):
+        try:
+            counts, matches = _mine_packed(model, lexicon, pd.batch, config, device=device)
+            counts = counts.astype(np.int64)
+        except BimineError:
+            counts, parts = np.zeros(keep.size, dtype=np.int64), []
+            for b in range(keep.size):
+                try:
+                    c, m = _mine_packed(model, lexicon, pd.batch.select([b]), config, device=device)
+                    counts[b] = int(c[0])
+                    parts.append(m.copy())
+                except BimineError as exc:
+                    failed[lo + int(keep[b])] = f"pair {topic_ids[lo + int(keep[b])]}: {exc}"
+            matches = np.concatenate(parts) if parts else np.zeros(0, dtype=_native_match_dtype())
+    # rows: every match's sentences by index into the chunk's sentence list
+    if matches.shape[0] == 0:
+        return [], failed
+    owner = np.repeat(keep, counts)  # input pair (within the chunk) of each match
+    src_idx = pd.start[owner] + matches["i"].astype(np.int64)
+    tgt_idx = pd.start[owner] + pd.n_src[owner] + matches["j"].astype(np.int64)
+    sents = pd.sentences
+    if src_idx.shape[0] == 1:
+        srcs, tgts = [sents[int(src_idx[0])]], [sents[int(tgt_idx[0])]]
+    else:
+        srcs = operator.itemgetter(*src_idx.tolist())(sents)
+        tgts = operator.itemgetter(*tgt_idx.tolist())(sents)
+    return list(zip(matches["score"].tolist(), srcs, tgts)), failed
+
+
+def _native_match_dtype():
+    from . import _native as N
+
+    return N.MATCH_DTYPE
+
+
 def mine_corpus(model, lexicon, pairs: Sequence, config: MiningConfig, engine: str = "nw_wavefront") -> MiningOutcome:
     """Mine document pairs; output follows input order for any ``workers``.
 
-    ``config.workers`` > 1 shards the pairs over that many visible GPUs
-    (contiguous ranges balanced by cell count, one host thread per
-    device); results are concatenated in shard order, which is input
-    order.  Failing pairs are reported and skipped.
+    The pairs are tokenised and packed in chunks (the next chunk is packed on
+    the host while the previous ones mine on the GPUs); ``config.workers``
+    sets the minimum number of chunks ("shards"), which go round-robin to
+    the visible GPUs, one host thread per device.  Results are assembled in
+    input order.  Failing pairs -- untokenisable sentences, or a document a
+    device limit rejects -- are reported and skipped, never raised.
     """
     _check_engine(engine)
     ctx = _engine.lexicon_context(lexicon)
-    builder = BatchBuilder(ctx.vocab)
-    index_of: list[int] = []  # batch pair -> input pair
+    n = len(pairs)
+    import torch
+
+    _engine.current_device()  # loud: no library or no GPU
+    n_dev = max(1, min(config.workers, torch.cuda.device_count()))
+    chunks = _chunk_bounds(n, config.workers)
+    topic_ids = [p.topic_id for p in pairs]
     errors: dict[int, str] = {}
-    results = builder.add_pairs([(p.source.sentences, p.target.sentences) for p in pairs])
-    for k, (pair, res) in enumerate(zip(pairs, results)):
-        if isinstance(res, str):
-            errors[k] = f"pair {pair.topic_id}: {res}"
-        else:
-            index_of.append(k)
-    batch = builder.build()
-    per_pair: list = [None] * len(pairs)
-    if batch.n_pairs:
-        import torch
-
-        n_dev = max(1, min(config.workers, torch.cuda.device_count()))
-        weights = batch.pair_n.astype(np.int64) * batch.pair_m.astype(np.int64)
-        shards = _shard_bounds(weights, n_dev)
-
-        def run(shard_dev):
-            (lo, hi), dev = shard_dev
-            sub = batch if (lo, hi) == (0, batch.n_pairs) else batch.select(range(lo, hi))
-            with torch.cuda.device(dev):
-                counts, matches = _mine_packed(model, lexicon, sub, config, device=dev)
-            return lo, counts, matches
-
-        jobs = [(s, d) for d, s in enumerate(shards)]
-        if len(jobs) == 1:
-            results = [run(jobs[0])]
-        else:
-            with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
-                results = list(ex.map(run, jobs))
-        for lo, counts, matches in results:
-            score, ii, jj = matches["score"].tolist(), matches["i"].tolist(), matches["j"].tolist()
-            pos = 0
-            for b, c in enumerate(counts.tolist()):
-                per_pair[index_of[lo + b]] = (score[pos : pos + c], ii[pos : pos + c], jj[pos : pos + c])
-                pos += c
-    rows: list[tuple[float, str, str]] = []
-    failures: list[tuple[str, str]] = []
-    for k, pair in enumerate(pairs):
-        if k in errors:
-            failures.append((pair.topic_id, errors[k]))
-            continue
-        src, tgt = pair.source.sentences, pair.target.sentences
-        score, ii, jj = per_pair[k]
-        rows.extend(zip(score, [src[i] for i in ii], [tgt[j] for j in jj]))
-    return MiningOutcome(rows=tuple(rows), failures=tuple(failures))
+    pools = [ThreadPoolExecutor(max_workers=1) for _ in range(n_dev)]  # a device's chunks in order
+    futures = []
+    try:
+        for c, (lo, hi) in enumerate(chunks):
+            pd = pack_documents(ctx.vocab, [(p.source.sentences, p.target.sentences) for p in pairs[lo:hi]])
+            for k, msg in pd.errors.items():
+                errors[lo + k] = f"pair {topic_ids[lo + k]}: {msg}"
+            if pd.batch is None:
+                continue
+            futures.append(pools[c % n_dev].submit(_mine_chunk, model, lexicon, pd, config, c % n_dev, topic_ids,
+                                                   lo))
+        rows: list[tuple[float, str, str]] = []
+        for fut in futures:
+            chunk_rows, failed = fut.result()
+            rows.extend(chunk_rows)
+            errors.update(failed)
+    finally:
+        for pool in pools:
+            pool.shutdown(wait=True)
+    failures = tuple((topic_ids[k], errors[k]) for k in sorted(errors))
+    return MiningOutcome(rows=tuple(rows), failures=failures)

@@ -17,6 +17,9 @@
 #include <cstdio>
 #include <map>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
+#include <future>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -116,9 +119,180 @@ struct UploadGate {
   const int32_t *ready;  // grows as pieces land
   const int32_t *need;   // per pair: the counter value its data need
   cudaEvent_t all;
+  std::function<void()> before_all;  // host side: `all` is recorded once this returns
 };
 thread_local const UploadGate *tl_gate = nullptr;
-cudaError_t gate_wait_all(cudaStream_t st) { return tl_gate ? cudaStreamWaitEvent(st, tl_gate->all, 0) : cudaSuccess; }
+cudaError_t gate_wait_all(cudaStream_t st) {
+  if (!tl_gate) return cudaSuccess;
+  if (tl_gate->before_all) tl_gate->before_all();
+  return cudaStreamWaitEvent(st, tl_gate->all, 0);
+}
+
+// ---- pageable host input staged through page-locked memory ----------------
+// A cudaMemcpyAsync from pageable memory is synchronous and goes through the
+// driver's own small staging buffer.  Pageable arrays are instead copied by
+// a few host threads into a ring of page-locked slots, each slot's H2D
+// issued as soon as it is full and the slot reused once that copy is done.
+bool is_pageable(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+class MemcpyPool {  // fork-join memcpy over a few persistent threads
+ public:
+  static MemcpyPool &get() {
+    static MemcpyPool pool;
+    return pool;
+  }
+  void copy(void *dst, const void *src, size_t bytes) {
+    if (bytes < ((size_t)1 << 20) || n_ == 0) {
+      memcpy(dst, src, bytes);
+      return;
+    }
+    std::lock_guard<std::mutex> op(op_mu_);  // one copy at a time (several host threads may stage)
+    std::unique_lock<std::mutex> lk(mu_);
+    dst_ = (char *)dst;
+    src_ = (const char *)src;
+    bytes_ = bytes;
+    pending_ = n_;
+    ++gen_;
+    cv_.notify_all();
+    // this thread takes the last part
+    const size_t part = (bytes + n_) / (n_ + 1), lo = std::min(bytes, part * n_);
+    lk.unlock();
+    memcpy((char *)dst + lo, (const char *)src + lo, bytes - lo);
+    lk.lock();
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  MemcpyPool() {
+    const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+    n_ = (int)std::min(7u, std::max(1u, hc / 4));
+    for (int k = 0; k < n_; ++k) threads_.emplace_back([this, k] { run(k); });
+  }
+  ~MemcpyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto &t : threads_) t.join();
+  }
+  void run(int k) {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(mu_);
+    while (true) {
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (stop_) return;
+      char *dst = dst_;
+      const char *src = src_;
+      const size_t bytes = bytes_, part = (bytes + n_) / (n_ + 1);
+      lk.unlock();
+      const size_t lo = std::min(bytes, part * k), hi = std::min(bytes, part * (k + 1));
+      if (hi > lo) memcpy(dst + lo, src + lo, hi - lo);
+      lk.lock();
+      if (--pending_ == 0) done_.notify_all();
+    }
+  }
+  std::mutex op_mu_, mu_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> threads_;
+  int n_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+  char *dst_ = nullptr;
+  const char *src_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+class Stager {  // H2D on `st`: pinned sources directly, pageable ones through the ring
+ public:
+  static constexpr int kSlots = 4;
+  static constexpr size_t kSlotBytes = (size_t)32 << 20;
+  Stager(cudaStream_t st, int device) : st_(st), dev_(device) {}
+  ~Stager() {
+    for (auto &e : ev_)
+      if (e) cudaEventDestroy(e);
+    if (lease_) lease_->mu.unlock();
+  }
+  cudaError_t copy(void *dst, const void *src, size_t bytes, bool pageable) {
+    if (!bytes) return cudaSuccess;
+    if (!pageable) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st_);
+    cudaError_t e = ensure();
+    for (size_t off = 0; off < bytes && e == cudaSuccess; off += kSlotBytes) {
+      const size_t n = std::min(kSlotBytes, bytes - off);
+      const int k = next_++ % kSlots;
+      if (used_[k]) e = cudaEventSynchronize(ev_[k]);  // the slot's previous copy is done
+      if (e != cudaSuccess) break;
+      char *slot = lease_->p + (size_t)k * kSlotBytes;
+      MemcpyPool::get().copy(slot, (const char *)src + off, n);
+      e = cudaMemcpyAsync((char *)dst + off, slot, n, cudaMemcpyHostToDevice, st_);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_[k], st_);
+      used_[k] = true;
+    }
+    return e;
+  }
+
+ private:
+  // one page-locked ring per device, leased for a whole upload (calls on
+  // one device stage one after the other)
+  struct Ring {
+    std::mutex mu;
+    char *p = nullptr;
+  };
+  static Ring &ring_of(int dev) {
+    static std::mutex mu;
+    static std::map<int, Ring *> rings;
+    std::lock_guard<std::mutex> lk(mu);
+    Ring *&r = rings[dev];
+    if (!r) r = new Ring();  // process lifetime
+    return *r;
+  }
+  cudaError_t ensure() {
+    if (!lease_) {
+      Ring &r = ring_of(dev_);
+      r.mu.lock();
+      lease_ = &r;
+      // events are recorded on st_ and never outlive it; the ring's last
+      // copies completed before the previous lease ended (see ~Stager use)
+      if (!r.p && cudaMallocHost((void **)&r.p, kSlots * kSlotBytes) != cudaSuccess) {
+        r.p = nullptr;
+        return cudaErrorMemoryAllocation;
+      }
+    }
+    for (auto &e : ev_)
+      if (!e) {
+        const cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        if (r != cudaSuccess) return r;
+      }
+    return cudaSuccess;
+  }
+
+ public:
+  // the ring may be reused by the next lease only once its copies are done
+  cudaError_t drain() {
+    cudaError_t e = cudaSuccess;
+    for (int k = 0; k < kSlots; ++k)
+      if (used_[k] && e == cudaSuccess) e = cudaEventSynchronize(ev_[k]);
+    return e;
+  }
+
+ private:
+  cudaStream_t st_;
+  int dev_;
+  Ring *lease_ = nullptr;
+  cudaEvent_t ev_[kSlots] = {};
+  bool used_[kSlots] = {};
+  int next_ = 0;
+};
 
 // a device word the long-sentence kernel reports overflows in (one per
 // device: one process may drive several GPUs, one host thread each)
@@ -946,39 +1120,68 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
 #ifdef BIMINE_E2E_PROFILE
   cudaEventRecord(pe[0], st);
 #endif
-  // ---- uploads, issued before any host-side analysis
+  // ---- uploads, issued before any host-side analysis.  Pinned inputs are
+  //      enqueued at once; pageable ones are staged through page-locked
+  //      memory by an uploader thread (bumping the same device counter), so
+  //      that the analysis below and the gated score launch run meanwhile.
   cudaError_t e = cudaMemsetAsync(arena + o_ready, 0, 4, st);
   e = e ? e : cudaEventRecord(ev_start, st);  // arena + ready counter exist
   e = e ? e : cudaStreamWaitEvent(cs, ev_start, 0);
-  {
-    auto H2D = [&](size_t o, const void *src, size_t bytes) {
-      if (e == cudaSuccess && bytes) e = cudaMemcpyAsync(arena + o, src, bytes, cudaMemcpyHostToDevice, cs);
+  const bool pg_pairs = is_pageable(h->pair_src) || is_pageable(h->pair_n) || is_pageable(h->pair_tgt) ||
+                        is_pageable(h->pair_m) || is_pageable(h->pair_sim_off);
+  const bool pg_sent = is_pageable(h->sent_len) || is_pageable(h->sent_uniq) || is_pageable(h->sent_chars);
+  const bool pg_tok = is_pageable(h->tokens);
+  const bool staged = pg_pairs || pg_sent || pg_tok;
+  int dev_id = 0;
+  cudaGetDevice(&dev_id);
+  std::promise<cudaError_t> phase1;  // sentence arrays, offsets scan and ev_scan enqueued
+  std::future<cudaError_t> phase1_done = phase1.get_future();
+  cudaError_t up_err = cudaSuccess;
+  auto upload = [&, dev_id, e0 = e]() {
+    cudaSetDevice(dev_id);
+    Stager sg(cs, dev_id);
+    cudaError_t ue = e0;
+    auto H2D = [&](size_t o, const void *src, size_t bytes, bool pg) {
+      if (ue == cudaSuccess && bytes) ue = sg.copy(arena + o, src, bytes, pg);
     };
-    H2D(o_psrc, h->pair_src, 8 * P);
-    H2D(o_pn, h->pair_n, 4 * P);
-    H2D(o_ptgt, h->pair_tgt, 8 * P);
-    H2D(o_pm, h->pair_m, 4 * P);
-    H2D(o_psim, h->pair_sim_off, 8 * P);
-    H2D(o_outoff, out_off, 8 * P);
-    H2D(o_slen, h->sent_len, 4 * S);
-    H2D(o_suniq, h->sent_uniq, 4 * S);
-    H2D(o_schar, h->sent_chars, 4 * S);
-    if (e == cudaSuccess)
-      e = offsets_from_lengths((const int32_t *)(arena + o_slen), (int64_t *)(arena + o_soff), S, arena + o_scan,
-                               &scan_bytes, cs);
-    e = e ? e : cudaEventRecord(ev_scan, cs);
-    H2D(o_ready, &ready_vals[0], 4);  // 1: pairs and sentences are in place
+    H2D(o_psrc, h->pair_src, 8 * P, pg_pairs);
+    H2D(o_pn, h->pair_n, 4 * P, pg_pairs);
+    H2D(o_ptgt, h->pair_tgt, 8 * P, pg_pairs);
+    H2D(o_pm, h->pair_m, 4 * P, pg_pairs);
+    H2D(o_psim, h->pair_sim_off, 8 * P, pg_pairs);
+    H2D(o_outoff, out_off, 8 * P, false);
+    H2D(o_slen, h->sent_len, 4 * S, pg_sent);
+    H2D(o_suniq, h->sent_uniq, 4 * S, pg_sent);
+    H2D(o_schar, h->sent_chars, 4 * S, pg_sent);
+    if (ue == cudaSuccess)
+      ue = offsets_from_lengths((const int32_t *)(arena + o_slen), (int64_t *)(arena + o_soff), S, arena + o_scan,
+                                &scan_bytes, cs);
+    ue = ue ? ue : cudaEventRecord(ev_scan, cs);
+    H2D(o_ready, &ready_vals[0], 4, false);  // 1: pairs and sentences are in place
+    phase1.set_value(ue);
     for (int j = 0; j < nt; ++j) {
-      H2D(o_tok + 4 * tcut[j], h->tokens + tcut[j], 4 * (tcut[j + 1] - tcut[j]));
-      H2D(o_ready, &ready_vals[j + 1], 4);  // j + 2: token pieces 0..j
+      H2D(o_tok + 4 * tcut[j], h->tokens + tcut[j], 4 * (tcut[j + 1] - tcut[j]), pg_tok);
+      H2D(o_ready, &ready_vals[j + 1], 4, false);  // j + 2: token pieces 0..j
     }
-    e = e ? e : cudaEventRecord(ev_all, cs);
-#ifdef BIMINE_E2E_PROFILE
-    cudaEventRecord(pe[1], cs);
-    h_enq = hclock() - h0;
-#endif
+    ue = ue ? ue : cudaEventRecord(ev_all, cs);
+    const cudaError_t de = sg.drain();  // the ring is free for the next upload
+    up_err = ue ? ue : de;
+  };
+  std::thread uploader;
+  if (staged) {
+    uploader = std::thread(upload);
+  } else {
+    upload();
   }
+  auto join_uploader = [&]() {
+    if (uploader.joinable()) uploader.join();
+  };
+#ifdef BIMINE_E2E_PROFILE
+  cudaEventRecord(pe[1], cs);
+  h_enq = hclock() - h0;
+#endif
   auto abort_with = [&](int code, const std::string &msg) {
+    join_uploader();
     cudaStreamSynchronize(cs);
     cudaFreeAsync(arena, st);
     cudaStreamSynchronize(st);
@@ -1061,7 +1264,8 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     if (ci[k].rc != BIMINE_OK) return abort_with(ci[k].rc, ci[k].err);
   bool packed = true;
   for (int k = 0; k < nc; ++k) packed = packed && ci[k].packed;
-  e = cudaStreamWaitEvent(st, ev_scan, 0);
+  e = phase1_done.get();  // the uploader has enqueued the offsets scan
+  e = e ? e : cudaStreamWaitEvent(st, ev_scan, 0);
   if (!packed && e == cudaSuccess)  // the caller's own layout: overwrite the rebuilt offsets
     e = cudaMemcpyAsync(arena + o_soff, h->sent_tok_off, 8 * S, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return abort_with(BIMINE_E_CUDA, std::string("bimine_mine_host: ") + cudaGetErrorString(e));
@@ -1118,18 +1322,23 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     d.pair_m = (const int32_t *)(arena + o_pm);
     d.pair_sim_off = (const int64_t *)(arena + o_psim);
     plan.work = (const int64_t *)(arena + o_work);
-    const UploadGate gate{(const int32_t *)(arena + o_ready), (const int32_t *)(arena + o_need), ev_all};
+    const UploadGate gate{(const int32_t *)(arena + o_ready), (const int32_t *)(arena + o_need), ev_all,
+                          join_uploader};
     tl_gate = &gate;
     rc = bimine_mine_batch(dict, model, &d, &plan, gap, threshold, mismatch, bonus, (double *)(arena + o_sim),
                            (const int64_t *)(arena + o_outoff), (bimine_match *)(arena + o_slots),
                            (int32_t *)(arena + o_counts), nullptr, stream);
     tl_gate = nullptr;
+    join_uploader();
+    if (rc == BIMINE_OK && up_err != cudaSuccess)
+      rc = fail(BIMINE_E_CUDA, std::string("bimine_mine_host H2D: ") + cudaGetErrorString(up_err));
     // (every later launch on st follows NW, which waited for all uploads)
 #ifdef BIMINE_E2E_PROFILE
     cudaEventRecord(pe[2], st);
     h_mine = hclock() - h0;
 #endif
   } else {
+    join_uploader();
     rc = fail(BIMINE_E_CUDA, std::string("bimine_mine_host H2D: ") + cudaGetErrorString(e));
   }
   if (rc == BIMINE_OK)

@@ -24,6 +24,7 @@
 // would; (3) threads patch the new ids in, count distinct tokens per
 // sentence and copy their tokens to the output.
 #include <algorithm>
+#include <cstddef>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -219,8 +220,22 @@ struct TokRange {
 // Per sentence, two passes: split + lowercase + hash every token and
 // prefetch its home slot, then resolve them (the table is far larger than
 // the caches; the prefetches overlap the misses).
-void tokenize_range(const bimine_vocab &v, const unsigned char *buf, const int64_t *off, TokRange &r,
-                    int32_t *len_out, int32_t *chars_out) {
+// Sentences as one buffer + offsets, or as one pointer + length each.
+struct BufSentences {
+  const unsigned char *buf;
+  const int64_t *off;
+  const unsigned char *ptr(int64_t k) const { return buf + off[k]; }
+  int64_t len(int64_t k) const { return off[k + 1] - off[k]; }
+};
+struct PtrSentences {
+  const unsigned char *const *p;
+  const int64_t *n;
+  const unsigned char *ptr(int64_t k) const { return p[k]; }
+  int64_t len(int64_t k) const { return n[k]; }
+};
+
+template <class Sent>
+void tokenize_range(const bimine_vocab &v, const Sent &sent, TokRange &r, int32_t *len_out, int32_t *chars_out) {
   std::vector<char> low;  // the sentence's words, each zero-padded (16 + round-up to 8)
   struct Tok {
     uint64_t hash;
@@ -229,8 +244,8 @@ void tokenize_range(const bimine_vocab &v, const unsigned char *buf, const int64
   std::vector<Tok> toks;
   std::vector<unsigned char> lat;  // a Latin sentence, lowered
   for (int64_t k = r.k0; k < r.k1; ++k) {
-    const unsigned char *p = buf + off[k];
-    int64_t L = off[k + 1] - off[k];
+    const unsigned char *p = sent.ptr(k);
+    int64_t L = sent.len(k);
     chars_out[k] = (int32_t)L;
     bool ascii = true;
     for (int64_t x = 0; x < L; ++x)
@@ -342,20 +357,34 @@ int bimine_vocab_word(const bimine_vocab *v, int32_t id, const char **ptr, int64
   return BIMINE_OK;
 }
 
-int bimine_tokenize_batch(bimine_vocab *v, const char *buf, const int64_t *off, int64_t n, int32_t *tokens,
-                          int64_t cap, int64_t *n_tokens, int32_t *len_out, int32_t *uniq_out, int32_t *chars_out) {
-  if (!v || !n_tokens || (n > 0 && (!buf || !off || !len_out || !uniq_out || !chars_out)))
-    return BIMINE_E_ARG;
+}  // extern "C"
+
+namespace {
+
+// The three phases over `n` sentences split into ranges of about `bytes_of`
+// bytes each (>= 256 KB per thread).
+template <class Sent, class Prefix>
+int tokenize_sentences(bimine_vocab *v, const Sent &sent, int64_t n, Prefix prefix_bytes, int32_t *tokens,
+                       int64_t cap, int64_t *n_tokens, int32_t *len_out, int32_t *uniq_out, int32_t *chars_out) {
   *n_tokens = 0;
   if (n <= 0) return BIMINE_OK;
-  // contiguous sentence ranges of about equal bytes, >= 256 KB each
-  const int64_t bytes = off[n] - off[0];
+  const int64_t bytes = prefix_bytes(n);
   const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(host_threads(), bytes >> 18));
   std::vector<TokRange> R(nt);
   for (int t = 0; t < nt; ++t) {
     R[t].k0 = t == 0 ? 0 : R[t - 1].k1;
-    R[t].k1 = t == nt - 1 ? n
-                          : std::lower_bound(off + R[t].k0, off + n, off[0] + bytes * (t + 1) / nt) - off;
+    if (t == nt - 1) {
+      R[t].k1 = n;
+    } else {  // first sentence whose byte prefix reaches the thread's share
+      int64_t lo = R[t].k0, hi = n;
+      const int64_t want = bytes * (t + 1) / nt;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if (prefix_bytes(mid) < want) lo = mid + 1;
+        else hi = mid;
+      }
+      R[t].k1 = lo;
+    }
   }
   auto parallel = [&](auto &&fn) {
     if (nt == 1) return fn(R[0]);
@@ -364,8 +393,7 @@ int bimine_tokenize_batch(bimine_vocab *v, const char *buf, const int64_t *off, 
     fn(R[0]);
     for (auto &th : pool) th.join();
   };
-  const unsigned char *ubuf = (const unsigned char *)buf;
-  parallel([&](TokRange &r) { tokenize_range(*v, ubuf, off, r, len_out, chars_out); });
+  parallel([&](TokRange &r) { tokenize_range(*v, sent, r, len_out, chars_out); });
   int64_t total = 0;
   for (TokRange &r : R) {
     r.out_off = total;
@@ -380,6 +408,50 @@ int bimine_tokenize_batch(bimine_vocab *v, const char *buf, const int64_t *off, 
   parallel([&](TokRange &r) { finish_range(r, len_out, uniq_out, tokens); });
   *n_tokens = total;
   return BIMINE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bimine_tokenize_batch(bimine_vocab *v, const char *buf, const int64_t *off, int64_t n, int32_t *tokens,
+                          int64_t cap, int64_t *n_tokens, int32_t *len_out, int32_t *uniq_out, int32_t *chars_out) {
+  if (!v || !n_tokens || (n > 0 && (!buf || !off || !len_out || !uniq_out || !chars_out)))
+    return BIMINE_E_ARG;
+  const BufSentences sent{(const unsigned char *)buf, off};
+  return tokenize_sentences(v, sent, n, [&](int64_t k) { return off[k] - off[0]; }, tokens, cap, n_tokens, len_out,
+                            uniq_out, chars_out);
+}
+
+int bimine_tokenize_strobjs(bimine_vocab *v, const int64_t *obj, int64_t n, int64_t data_off, int64_t len_off,
+                            int32_t *tokens, int64_t cap, int64_t *n_tokens, int32_t *len_out, int32_t *uniq_out,
+                            int32_t *chars_out) {
+  if (!v || !n_tokens || (n > 0 && (!obj || !len_out || !uniq_out || !chars_out)) || data_off <= 0 || len_off < 0)
+    return BIMINE_E_ARG;
+  std::vector<const unsigned char *> ptrs((size_t)std::max<int64_t>(n, 1));
+  std::vector<int64_t> lens((size_t)std::max<int64_t>(n, 1)), prefix((size_t)n + 1, 0);
+  for (int64_t k = 0; k < n; ++k) {
+    const char *o = (const char *)(intptr_t)obj[k];
+    int64_t L;
+    memcpy(&L, o + len_off, 8);
+    ptrs[k] = (const unsigned char *)o + data_off;
+    lens[k] = L;
+    prefix[k + 1] = prefix[k] + L;
+  }
+  if (prefix[n] / 2 + n + 1 > cap) return BIMINE_E_LIMIT;
+  const PtrSentences sent{ptrs.data(), lens.data()};
+  return tokenize_sentences(v, sent, n, [&](int64_t k) { return prefix[k]; }, tokens, cap, n_tokens, len_out,
+                            uniq_out, chars_out);
+}
+
+int bimine_tokenize_ptrs(bimine_vocab *v, const char *const *ptrs, const int64_t *lens, int64_t n,
+                         const int64_t *len_prefix, int32_t *tokens, int64_t cap, int64_t *n_tokens,
+                         int32_t *len_out, int32_t *uniq_out, int32_t *chars_out) {
+  if (!v || !n_tokens || (n > 0 && (!ptrs || !lens || !len_prefix || !len_out || !uniq_out || !chars_out)))
+    return BIMINE_E_ARG;
+  const PtrSentences sent{(const unsigned char *const *)ptrs, lens};
+  return tokenize_sentences(v, sent, n, [&](int64_t k) { return len_prefix[k]; }, tokens, cap, n_tokens, len_out,
+                            uniq_out, chars_out);
 }
 
 }  // extern "C"

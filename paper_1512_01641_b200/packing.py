@@ -45,6 +45,37 @@ class Vocabulary:
         return np.fromiter((self.get(w) for w in words), dtype=np.int32)
 
 
+def _ascii_layout() -> tuple[int, int] | None:
+    """(character offset, length offset) inside a compact ASCII str object
+    (CPython's PyASCIIObject header), found by probing strings of several
+    lengths; None if the layout is not recognised (the encode path is used
+    then)."""
+    import ctypes
+    import struct
+
+    try:
+        data, lens = set(), set()
+        for probe in ("bimine\x01probe\x02layout", "x" * 37 + "\x03", "\x04" * 5 + "q" * 300):
+            raw = ctypes.string_at(id(probe), 512)
+            data.add(raw.find(probe.encode("ascii")))
+            lens.add(next((o for o in range(8, 64, 8) if struct.unpack_from("<q", raw, o)[0] == len(probe)), -1))
+        d, n = (data.pop() if len(data) == 1 else -1), (lens.pop() if len(lens) == 1 else -1)
+        return (d, n) if 0 < d <= 128 and 0 < n < d else None
+    except Exception:  # pragma: no cover - unusual interpreters
+        return None
+
+
+_ASCII_LAYOUT = _ascii_layout()
+
+
+def _str_objects(strings: list[str]):
+    """The strings' object addresses when every one is an exact, compact
+    ASCII str (the tokenizer then reads them in place), else None."""
+    if _ASCII_LAYOUT is None or not all(map(str.isascii, strings)) or set(map(type, strings)) != {str}:
+        return None
+    return np.fromiter(map(id, strings), dtype=np.int64, count=len(strings))
+
+
 def _utf8_offsets(strings: list[str]) -> tuple[bytes, np.ndarray]:
     """The strings' UTF-8 bytes back to back, and their byte offsets."""
     off = np.zeros(len(strings) + 1, dtype=np.int64)
@@ -98,19 +129,30 @@ class NativeVocabulary:
 
     def tokenize(self, sentences: list[str]):
         """(tokens int32, len, uniq, chars) per sentence with the reference's
-        tokenize(); a sentence with no token has len 0."""
+        tokenize(); a sentence with no token has len 0.  ASCII sentences are
+        read in place (their str storage); others go through one UTF-8
+        buffer."""
         N = self._N
         n = len(sentences)
-        data, off = _utf8_offsets(sentences)
-        cap = len(data) // 2 + n + 1
-        tokens = np.empty(cap, dtype=np.int32)
         lens = np.empty(max(n, 1), dtype=np.int32)
         uniq = np.empty(max(n, 1), dtype=np.int32)
         chars = np.empty(max(n, 1), dtype=np.int32)
         nt = np.zeros(1, dtype=np.int64)
-        N.check(self._L.bimine_tokenize_batch(self._h, data, N.ptr(off, N._i64p), n, N.ptr(tokens, N._i32p), cap,
-                                              N.ptr(nt, N._i64p), N.ptr(lens, N._i32p), N.ptr(uniq, N._i32p),
-                                              N.ptr(chars, N._i32p)))
+        objs = _str_objects(sentences) if n else None
+        if objs is not None:
+            cap = sum(map(len, sentences)) // 2 + n + 1
+            tokens = np.empty(cap, dtype=np.int32)
+            N.check(self._L.bimine_tokenize_strobjs(self._h, N.ptr(objs, N._i64p), n, _ASCII_LAYOUT[0],
+                                                    _ASCII_LAYOUT[1], N.ptr(tokens, N._i32p), cap,
+                                                    N.ptr(nt, N._i64p), N.ptr(lens, N._i32p), N.ptr(uniq, N._i32p),
+                                                    N.ptr(chars, N._i32p)))
+        else:
+            data, off = _utf8_offsets(sentences)
+            cap = len(data) // 2 + n + 1
+            tokens = np.empty(cap, dtype=np.int32)
+            N.check(self._L.bimine_tokenize_batch(self._h, data, N.ptr(off, N._i64p), n, N.ptr(tokens, N._i32p),
+                                                  cap, N.ptr(nt, N._i64p), N.ptr(lens, N._i32p),
+                                                  N.ptr(uniq, N._i32p), N.ptr(chars, N._i32p)))
         tokens, lens, uniq, chars = tokens[: int(nt[0])], lens[:n], uniq[:n], chars[:n]
         slow = np.flatnonzero(lens < 0)
         if slow.size:  # code points >= U+0180 (or U+0130): Python's Unicode rules, same vocabulary
@@ -278,19 +320,77 @@ def profile_ids(sentence: str, vocab: Vocabulary) -> list[int]:
     return [get(t) for t in tokens]
 
 
+@dataclass
+class PackedDocuments:
+    """Result of pack_documents: the batch of the pairs that tokenise, and
+    the bookkeeping to map matches back to sentence text."""
+
+    batch: PackedBatch | None  # None when no pair tokenises
+    sentences: list  # every input sentence, pair by pair: its source then its target sentences
+    start: np.ndarray  # [P + 1] first sentence of input pair k in `sentences`
+    n_src: np.ndarray  # [P] source sentence count per input pair
+    ok: np.ndarray  # [P] bool: input pair k is in the batch
+    errors: dict  # input pair -> the reference's ValueError message
+
+
+def pack_documents(vocab, pairs) -> PackedDocuments:
+    """Tokenise and pack many (source_sentences, target_sentences) at once
+    (one native tokenizer call; a pair whose sentence does not tokenise is
+    left out with the message the reference raises for it, align.py:109-119)."""
+    import itertools
+
+    P = len(pairs)
+    ns = np.fromiter((len(x[0]) for x in pairs), dtype=np.int64, count=P)
+    nt = np.fromiter((len(x[1]) for x in pairs), dtype=np.int64, count=P)
+    flat = list(itertools.chain.from_iterable(itertools.chain(x[0], x[1]) for x in pairs))
+    start = np.zeros(P + 1, dtype=np.int64)
+    np.cumsum(ns + nt, out=start[1:])
+    if getattr(vocab, "native", False):
+        tokens, lens, uniq, chars = vocab.tokenize(flat)
+    else:  # the dict vocabulary: the Python rules sentence by sentence
+        ids = []
+        for sent in flat:
+            ids.append(np.asarray([vocab.get(t) for t in tokenize(sent)], dtype=np.int32))
+        lens = np.fromiter(map(len, ids), dtype=np.int32, count=len(ids))
+        uniq = np.fromiter((len(set(x.tolist())) for x in ids), dtype=np.int32, count=len(ids))
+        chars = np.fromiter(map(len, flat), dtype=np.int32, count=len(flat))
+        tokens = np.concatenate(ids) if ids else np.zeros(0, np.int32)
+    lens = lens[: len(flat)]
+    zero = np.zeros(len(flat) + 1, dtype=np.int64)
+    np.cumsum(lens == 0, out=zero[1:])
+    ok = (ns > 0) & (nt > 0) & (zero[start[1:]] == zero[start[:-1]])
+    errors = {}
+    for k in np.flatnonzero(~ok).tolist():  # the reference's messages
+        if not ns[k] or not nt[k]:
+            errors[k] = "both sentence sequences must be non-empty"
+            continue
+        bad = int(start[k]) + int(np.flatnonzero(lens[start[k]: start[k + 1]] == 0)[0])
+        side, index = ("source", bad - start[k]) if bad - start[k] < ns[k] else ("target", bad - start[k] - ns[k])
+        errors[k] = f"{side} sentence {index}: untokenizable sentence: {flat[bad]!r}"
+    keep = np.flatnonzero(ok)
+    batch = None
+    if keep.size:
+        if keep.size == P:
+            tok, sl, su, sc = tokens, lens, uniq[: len(flat)], chars[: len(flat)]
+            first = start[:-1]
+        else:
+            sent_keep = np.repeat(ok, ns + nt)
+            tok = tokens[np.repeat(sent_keep, lens)]
+            sl, su, sc = lens[sent_keep], uniq[: len(flat)][sent_keep], chars[: len(flat)][sent_keep]
+            first = np.zeros(keep.size, dtype=np.int64)
+            np.cumsum((ns + nt)[keep][:-1], out=first[1:])
+        batch = PackedBatch.from_token_lengths(tok, sl, sc, first, ns[keep], first + ns[keep], nt[keep],
+                                               sent_uniq=su)
+    return PackedDocuments(batch=batch, sentences=flat, start=start, n_src=ns, ok=ok, errors=errors)
+
+
 class BatchBuilder:
     """Accumulates document pairs (as sentence strings) into a PackedBatch."""
 
     def __init__(self, vocab) -> None:
         self.vocab = vocab
-        self.tok_chunks: list[np.ndarray] = []
-        self.sent_len: list[int] = []
-        self.sent_uniq: list[int] = []
-        self.sent_chars: list[int] = []
-        self.pair_src: list[int] = []
-        self.pair_n: list[int] = []
-        self.pair_tgt: list[int] = []
-        self.pair_m: list[int] = []
+        self.parts: list[PackedBatch] = []
+        self.n_pairs = 0
 
     def _profiles(self, sentences: Sequence[str], side: str) -> list[list[int]]:
         out = []
@@ -305,82 +405,44 @@ class BatchBuilder:
         """Tokenise and append one pair; raises ValueError with the
         reference's messages (align.py:109-119) and leaves the builder
         unchanged on error.  Returns the pair's index in the batch."""
-        if not source or not target:
-            raise ValueError("both sentence sequences must be non-empty")
-        src = self._profiles(source, "source")
-        tgt = self._profiles(target, "target")
-        first = len(self.sent_len)
-        for ids, text in zip(src + tgt, list(source) + list(target)):
-            self.tok_chunks.append(np.asarray(ids, dtype=np.int32))
-            self.sent_len.append(len(ids))
-            self.sent_uniq.append(len(set(ids)))
-            self.sent_chars.append(len(text))
-        self.pair_src.append(first)
-        self.pair_n.append(len(src))
-        self.pair_tgt.append(first + len(src))
-        self.pair_m.append(len(tgt))
-        return len(self.pair_n) - 1
+        [res] = self.add_pairs([(source, target)])
+        if isinstance(res, str):
+            raise ValueError(res)
+        return res
 
     def add_pairs(self, pairs) -> list:
         """Append many (source_sentences, target_sentences) at once.  Returns,
         per input pair, its batch index or the ValueError message the
-        reference would raise for it (the pair is then not appended).
-        With a native vocabulary the sentences are tokenised in one call."""
-        if not getattr(self.vocab, "native", False):
-            out = []
-            for src, tgt in pairs:
-                try:
-                    out.append(self.add_pair(src, tgt))
-                except ValueError as exc:
-                    out.append(str(exc))
-            return out
+        reference would raise for it (the pair is then not appended)."""
         if not pairs:
             return []
-        pairs = [(list(src), list(tgt)) for src, tgt in pairs]
-        flat = [x for src, tgt in pairs for x in src + tgt]
-        tokens, lens, uniq, chars = self.vocab.tokenize(flat)
-        P = len(pairs)
-        ns = np.fromiter((len(src) for src, _ in pairs), dtype=np.int64, count=P)
-        nt = np.fromiter((len(tgt) for _, tgt in pairs), dtype=np.int64, count=P)
-        start = np.zeros(P + 1, dtype=np.int64)
-        np.cumsum(ns + nt, out=start[1:])
-        zero = np.zeros(len(flat) + 1, dtype=np.int64)
-        np.cumsum(lens == 0, out=zero[1:])
-        ok = (ns > 0) & (nt > 0) & (zero[start[1:]] == zero[start[:-1]])
-        out: list = [None] * P
-        for k in np.flatnonzero(~ok).tolist():  # the reference's messages
-            if not ns[k] or not nt[k]:
-                out[k] = "both sentence sequences must be non-empty"
-                continue
-            bad = int(start[k]) + int(np.flatnonzero(lens[start[k] : start[k + 1]] == 0)[0])
-            side, index = ("source", bad - start[k]) if bad - start[k] < ns[k] else ("target", bad - start[k] - ns[k])
-            out[k] = f"{side} sentence {index}: untokenizable sentence: {flat[bad]!r}"
-        keep = np.flatnonzero(ok)
-        first = len(self.sent_len) + np.concatenate(([0], np.cumsum((ns + nt)[keep])[:-1])) if keep.size else keep
-        for k, b, f, n_, m_ in zip(keep.tolist(), range(len(self.pair_n), len(self.pair_n) + keep.size),
-                                   first.tolist(), ns[keep].tolist(), nt[keep].tolist()):
-            out[k] = b
-            self.pair_src.append(f)
-            self.pair_n.append(n_)
-            self.pair_tgt.append(f + n_)
-            self.pair_m.append(m_)
-        sent_keep = np.repeat(ok, ns + nt)
-        self.sent_len.extend(lens[sent_keep].tolist())
-        self.sent_uniq.extend(uniq[sent_keep].tolist())
-        self.sent_chars.extend(chars[sent_keep].tolist())
-        self.tok_chunks.append(tokens if sent_keep.all() else tokens[np.repeat(sent_keep, lens)])
+        pd = pack_documents(self.vocab, pairs)
+        out: list = [None] * len(pairs)
+        for k, msg in pd.errors.items():
+            out[k] = msg
+        for b, k in enumerate(np.flatnonzero(pd.ok).tolist()):
+            out[k] = self.n_pairs + b
+        if pd.batch is not None:
+            self.parts.append(pd.batch)
+            self.n_pairs += pd.batch.n_pairs
         return out
 
     def build(self) -> PackedBatch:
+        if len(self.parts) == 1:
+            return self.parts[0]
+        if not self.parts:
+            z32, z64 = np.zeros(0, np.int32), np.zeros(0, np.int64)
+            return PackedBatch(z32, z64, z32, z32, z32, z64, z32, z64, z32, z64)
+        s_base = np.cumsum([0] + [p.n_sentences for p in self.parts[:-1]])
         return PackedBatch.from_token_lengths(
-            np.concatenate(self.tok_chunks) if self.tok_chunks else np.zeros(0, np.int32),
-            np.asarray(self.sent_len, dtype=np.int32),
-            np.asarray(self.sent_chars, dtype=np.int32),
-            np.asarray(self.pair_src, dtype=np.int64),
-            np.asarray(self.pair_n, dtype=np.int32),
-            np.asarray(self.pair_tgt, dtype=np.int64),
-            np.asarray(self.pair_m, dtype=np.int32),
-            sent_uniq=np.asarray(self.sent_uniq, dtype=np.int32),
+            np.concatenate([p.tokens for p in self.parts]),
+            np.concatenate([p.sent_len for p in self.parts]),
+            np.concatenate([p.sent_chars for p in self.parts]),
+            np.concatenate([p.pair_src + b for p, b in zip(self.parts, s_base)]),
+            np.concatenate([p.pair_n for p in self.parts]),
+            np.concatenate([p.pair_tgt + b for p, b in zip(self.parts, s_base)]),
+            np.concatenate([p.pair_m for p in self.parts]),
+            sent_uniq=np.concatenate([p.sent_uniq for p in self.parts]),
         )
 
 

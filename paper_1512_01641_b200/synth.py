@@ -153,6 +153,10 @@ class SynthCorpus:
         ids = b.tokens[o : o + int(b.sent_len[sent])]
         return " ".join(self.dictionary.words(ids)) + "."
 
+    def all_sentences(self) -> list[str]:
+        """Every sentence's text (sentence_text for all, vectorised)."""
+        return render_sentences(self.batch.tokens, self.batch.sent_len, self.dictionary)
+
     def pair_sentences(self, pair: int) -> tuple[list[str], list[str]]:
         b = self.batch
         s0, n = int(b.pair_src[pair]), int(b.pair_n[pair])
@@ -297,6 +301,35 @@ def make_corpus(
         pair_m=m.astype(np.int32),
     )
     return SynthCorpus(dictionary=d, batch=batch, ref_off=ref_off, ref_i=ref_i, ref_j=ref_j)
+
+
+def render_sentences(tokens: np.ndarray, sent_len: np.ndarray, d: SynthDictionary) -> list[str]:
+    """" ".join(words) + "." per sentence, built as one ASCII buffer."""
+    S = d.n_words
+    t = np.asarray(tokens, dtype=np.int64)
+    prefix = np.where(t < S, ord("s"), np.where(t < 2 * S, ord("t"), ord("x"))).astype(np.uint8)
+    num = np.where(t < S, t, np.where(t < 2 * S, t - S, t - 2 * S))
+    nd = _digits(num)
+    width = 1 + nd + 1  # prefix, digits, then " " or "."
+    start = np.zeros(t.shape[0] + 1, dtype=np.int64)
+    np.cumsum(width, out=start[1:])
+    buf = np.empty(int(start[-1]), dtype=np.uint8)
+    buf[start[:-1]] = prefix
+    rest = num.copy()
+    pos = start[:-1] + nd  # the last digit
+    for k in range(int(nd.max(initial=1))):  # digits from the right
+        sel = np.flatnonzero(nd > k) if k else slice(None)
+        q, r = np.divmod(rest[sel], 10)
+        buf[pos[sel] - k] = (ord("0") + r).astype(np.uint8)
+        rest[sel] = q
+    last = np.zeros(t.shape[0], dtype=bool)
+    ends = np.cumsum(sent_len) - 1
+    last[ends[sent_len > 0]] = True
+    buf[start[1:] - 1] = np.where(last, ord("."), ord(" "))
+    text = buf.tobytes().decode("ascii")
+    sent_start = start[np.concatenate([[0], np.cumsum(sent_len)[:-1]])].tolist()
+    sent_end = start[np.cumsum(sent_len)].tolist()
+    return [text[a:b] for a, b in zip(sent_start, sent_end)]
 
 
 def _chars(tokens: np.ndarray, sent_len: np.ndarray, d: SynthDictionary) -> np.ndarray:

@@ -425,27 +425,6 @@ def test_tune_trials_agree_with_per_trial_recomputation():
     assert res == want
 
 
-def test_fused_nw_tail_matches_standalone(monkeypatch):
-    """BIMINE_FUSE_NW=1 (NW in the score kernel's tail) gives the same matches."""
-    import subprocess, sys, os
-    code = (
-        "import sys; sys.path[:0]=['.','oracle','tests'];"
-        "import numpy as np, helpers as H, oracle;"
-        "from paper_1512_01641_b200 import synth, engine as E;"
-        "from paper_1512_01641_b200.classifier import model_vector;"
-        "c=synth.make_config(2, n_pairs=60); d=c.dictionary; m=model_vector(H.synth_model());"
-        "ctx=E.LexiconContext(vocab=None, coo=(d.src,d.tgt,d.prob), devices={});"
-        "cnt,mt,_=E.mine_host(ctx.on(0), m, c.batch, 2.0, 0.5, -1.0, 1.0);"
-        "wc,wr=oracle.mine_batch(oracle.OracleDict(d.src,d.tgt,d.prob), m, c.batch);"
-        "assert np.array_equal(cnt,wc); assert np.array_equal(mt.view(np.uint8), np.concatenate(wr).view(np.uint8));"
-        "print('ok')"
-    )
-    env = dict(os.environ, BIMINE_FUSE_NW="1")
-    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
-                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-2000:]
-
-
 @pytest.mark.parametrize("layout", ["reversed_with_gaps", "one_gap"])
 def test_mine_host_unpacked_sentence_offsets(layout):
     """bimine_mine_host rebuilds sent_tok_off from sent_len on the device
