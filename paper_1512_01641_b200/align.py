@@ -23,6 +23,8 @@ part of the GPU path: requesting them raises ``NotImplementedError``.
 
 from __future__ import annotations
 
+import contextlib
+import gc
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 from typing import Sequence
@@ -311,6 +313,22 @@ def mine_corpus(model, lexicon, pairs: Sequence, config: MiningConfig, engine: s
     device limit rejects -- are reported and skipped, never raised.
     """
     _check_engine(engine)
+    with _no_gc():  # the rows are ~10^5 - 10^7 fresh tuples: no collector passes while they are built
+        return _mine_corpus(model, lexicon, pairs, config)
+
+
+@contextlib.contextmanager
+def _no_gc():
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        yield
+    finally:
+        if was:
+            gc.enable()
+
+
+def _mine_corpus(model, lexicon, pairs: Sequence, config: MiningConfig) -> MiningOutcome:
     ctx = _engine.lexicon_context(lexicon)
     n = len(pairs)
     import torch

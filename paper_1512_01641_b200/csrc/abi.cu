@@ -173,7 +173,8 @@ class MemcpyPool {  // fork-join memcpy over a few persistent threads
  private:
   MemcpyPool() {
     const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
-    n_ = (int)std::min(7u, std::max(1u, hc / 4));
+    const char *v = getenv("BIMINE_STAGE_THREADS");  // helper threads (the caller copies too)
+    n_ = v ? std::max(0, std::min(63, atoi(v))) : (int)std::min(7u, std::max(1u, hc / 4));
     for (int k = 0; k < n_; ++k) threads_.emplace_back([this, k] { run(k); });
   }
   ~MemcpyPool() {
