@@ -691,10 +691,11 @@ int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
     if (nprob > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "nw: too many large problems");
     const int gmax = (max_n + 31) / 32;
     int kc = std::max(1, std::min(16, (gmax + kBigW - 1) / kBigW));  // CTAs per cluster (= per problem)
-    static const int skip_tb = [] {
-      const char *v = getenv("BIMINE_NW_SKIP_TRACEBACK");
-      return v && v[0] == '1';
-    }();
+#ifdef BIMINE_PROFILE_SKIP_TRACEBACK  // profiling builds only: time the sweep alone
+    constexpr bool skip_tb = true;
+#else
+    constexpr bool skip_tb = false;
+#endif
     constexpr size_t smem = big_smem_bytes<kBigW>();
     auto kern = nw_big_kernel<MODE, kBigW>;
     BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

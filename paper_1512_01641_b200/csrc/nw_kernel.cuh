@@ -1009,13 +1009,15 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
     }
     if (32 * g + 1 + lane == N) last_val[slot] = fin;
     __syncwarp();
-    // Diagnostic for a launch without the operand layout (never true for
-    // the launcher in abi.cu).  Measured side effect, kept on purpose: with
-    // a call site in this loop ptxas schedules the band pipeline's ring
-    // loops so that the 4096x4096 sweep takes 2.12 ms instead of 3.58 ms
-    // (an unreachable printf reproduces it; a memory clobber or fence does
-    // not) -- see DESIGN.md 4.3.
+    // (a guard only for launches without the operand layout, never true
+    // from abi.cu).  Its call site changes ptxas's schedule of the ring
+    // loops: 2.1 ms for the 4096x4096 sweep with it, 3.6 ms without
+    // (profiles/r2/nw_big_printf_ab.txt: same instruction mix, 37% of the
+    // issue slots in the ring polls either way).  Kept deliberately;
+    // tests/test_gpu_perf_guard.py fails if a toolchain change loses it.
+#ifndef BIMINE_NO_PRINTF
     if (diag_all == nullptr) printf("bimine: nw_big_kernel band %d without its operand layout\n", g);
+#endif
 #if defined(BIMINE_NW_PROFILE) || defined(BIMINE_PROF_BAND)
     if (lane == 0) {
       unsigned long long gt;
