@@ -134,8 +134,8 @@ int64_t bimine_dict_entries(const bimine_dict *dict);
  *   large ids pairs with N > 64 or M > 64, ascending (their NW runs on
  *             the cluster kernel; every other pair's on one warp)
  * work_host (capacity work_cap int64) receives 3 * n_tiles tile triples,
- * then n_long pair ids, then n_large pair ids; plan->work_len is the length
- * needed
+ * then n_long pair ids, then n_large pair ids, then the large pairs' (N, M);
+ * plan->work_len is the length needed
  * (BIMINE_E_ARG if work_cap is smaller).  The caller uploads
  * work_host[0 : work_len] and sets plan->work to the device copy. */
 typedef struct bimine_plan {
@@ -146,8 +146,11 @@ typedef struct bimine_plan {
   int32_t long_max_n, long_max_m;
   int64_t n_large;             /* pairs not in the one-CTA-per-pair launch */
   int64_t n_cells;             /* extent of sim: max pair_sim_off + N * M  */
-  int64_t work_len;            /* 3 * n_tiles + n_long + n_large          */
+  int64_t work_len;            /* 3 * n_tiles + n_long + 3 * n_large      */
   const int64_t *work;         /* device copy of work_host (set by caller)*/
+  const int64_t *work_host;    /* optional: the host array itself (the NW
+                                  launch then sizes the large pairs'
+                                  scratch without a device round trip)    */
 } bimine_plan;
 
 int bimine_plan_batch(const bimine_batch *batch_host, int64_t *work_host,

@@ -81,6 +81,7 @@ class CPlan(ctypes.Structure):
         ("n_cells", ctypes.c_int64),
         ("work_len", ctypes.c_int64),
         ("work", _vp),
+        ("work_host", _vp),
     ]
 
 

@@ -515,11 +515,16 @@ int bimine_plan_batch(const bimine_batch *b, int64_t *work, int64_t work_cap, bi
   P.n_tiles = t;
   P.n_long = (int64_t)longs.size();
   P.n_large = (int64_t)larges.size();
-  P.work_len = 3 * P.n_tiles + P.n_long + P.n_large;
+  P.work_len = 3 * P.n_tiles + P.n_long + 3 * P.n_large;
   *plan = P;
   if (P.work_len > work_cap) return fail(BIMINE_E_ARG, "bimine_plan_batch: work_cap < plan->work_len");
   for (int64_t k = 0; k < P.n_long; ++k) work[3 * P.n_tiles + k] = longs[k];
-  for (int64_t k = 0; k < P.n_large; ++k) work[3 * P.n_tiles + P.n_long + k] = larges[k];
+  int64_t *lw = work + 3 * P.n_tiles + P.n_long;
+  for (int64_t k = 0; k < P.n_large; ++k) {
+    lw[k] = larges[k];
+    lw[P.n_large + 2 * k] = b->pair_n[larges[k]];
+    lw[P.n_large + 2 * k + 1] = b->pair_m[larges[k]];
+  }
   return BIMINE_OK;
 }
 
@@ -657,8 +662,12 @@ int bimine_score_batch(const bimine_dict *dict, const double *model, const bimin
 // ------------------------------------------------------------------------
 namespace {
 
+// host_ids / host_dims (optional, host memory): the problems' pair ids and
+// (N, M), so that the large-problem path sizes its scratch without a device
+// round trip (one setting per problem)
 template <int MODE>
-int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
+int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st, const int64_t *host_ids = nullptr,
+              const int64_t *host_dims = nullptr) {
   if (A.n_problems == 0) return BIMINE_OK;
   const int row_d = ((max_m + 1) + 1) & ~1;  // doubles, even
   const int64_t dir_w = (MODE == kNwTable) ? 0 : (lean_dir_words16(max_n, max_m) + 1) / 2;  // u32 words
@@ -686,7 +695,6 @@ int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
   if (MODE != kNwTable) {
     // large problems: K CTAs each (16 warps pipelined over row bands per CTA);
     // K > 1 only while every CTA of the launch can be resident at once
-    const int64_t stride = (lean_dir_words16(max_n, max_m) + 1) / 2;  // u32 words per problem (worst case)
     const int64_t nprob = A.n_problems;
     if (nprob > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "nw: too many large problems");
     const int gmax = (max_n + 31) / 32;
@@ -708,110 +716,127 @@ int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st) {
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    while (kc > 1) {  // the largest cluster the device schedules for this kernel
-      attr[0].val.clusterDim.x = (unsigned)kc;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.gridDim = dim3((unsigned)kc, 1, 1);
-      int ok = 0;
-      if (cudaOccupancyMaxActiveClusters(&ok, kern, &cfg) == cudaSuccess && ok > 0) break;
-      cudaGetLastError();
-      --kc;
+    {  // the largest cluster the device schedules for this kernel (queried once per device and size)
+      static std::mutex mu;
+      static std::map<std::pair<int, int>, int> best;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = best.find({dev, kc});
+      if (it != best.end()) {
+        kc = it->second;
+      } else {
+        const int want = kc;
+        while (kc > 1) {
+          attr[0].val.clusterDim.x = (unsigned)kc;
+          attr[0].val.clusterDim.y = 1;
+          attr[0].val.clusterDim.z = 1;
+          cfg.gridDim = dim3((unsigned)kc, 1, 1);
+          int ok = 0;
+          if (cudaOccupancyMaxActiveClusters(&ok, kern, &cfg) == cudaSuccess && ok > 0) break;
+          cudaGetLastError();
+          --kc;
+        }
+        best[{dev, want}] = kc;
+      }
     }
     attr[0].val.clusterDim.x = (unsigned)kc;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     if (nprob * kc > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "nw: too many large problems");
     cfg.gridDim = dim3((unsigned)(nprob * kc), 1, 1);
-    // diagonal layout of every distinct pair among the problems: without a
-    // problem list (problems = pairs x settings, in order) at a uniform
-    // per-pair stride and without any host round trip; with one, the
-    // distinct pairs are gathered on the host
-    const int64_t dstride_u = (int64_t)gmax * nw_diag_steps(max_m) * 32;
-    const int64_t npairs_u = nprob / A.n_settings;
-    const bool uniform = !A.problem_ids && npairs_u * dstride_u <= ((int64_t)1 << 29);  // <= 4 GiB
-    double *diag = nullptr;
-    int64_t *d_pairs = nullptr, *d_pair_doff = nullptr, *d_doff = nullptr;
-    int64_t diag_stride = 0;
-    if (uniform) {
-      if (npairs_u > 65535 || gmax > 65535) return fail(BIMINE_E_LIMIT, "nw: large problem too tall");
-      BIMINE_CUDA(cudaMallocAsync((void **)&diag, sizeof(double) * std::max<int64_t>(npairs_u * dstride_u, 1), st));
-      diag_stride = dstride_u;
-      const int64_t per_band = nw_diag_steps(max_m) * 32;
-      const dim3 grid((unsigned)std::min<int64_t>((per_band + 255) / 256, 64), (unsigned)gmax, (unsigned)npairs_u);
-      nw_diag_kernel<<<grid, 256, 0, st>>>(A.sim, A.sim_off, A.pair_n, A.pair_m, nullptr, nullptr, dstride_u,
-                                           A.mismatch, A.bonus - A.mismatch, diag);  // one IEEE subtraction, as fsub
-      BIMINE_CUDA(cudaGetLastError());
-    } else {
-      std::vector<int64_t> ids(nprob);
-      if (A.problem_ids) {
-        BIMINE_CUDA(cudaMemcpyAsync(ids.data(), A.problem_ids, sizeof(int64_t) * nprob, cudaMemcpyDeviceToHost, st));
-        BIMINE_CUDA(cudaStreamSynchronize(st));
-      } else {
-        for (int64_t k = 0; k < nprob; ++k) ids[k] = k;
-      }
+    // per-problem scratch: exact offsets from the caller's host plan (ids and
+    // (N, M) of every problem; a pair's operand layout shared by its
+    // problems), else uniform strides from max_n / max_m computed on the
+    // device -- no host round trip either way
+    const bool exact = host_dims && host_ids && A.n_settings == 1;
+    int64_t nd = 0, dtotal = 0, dirtotal = 0, rowtotal = 0;
+    int gmax_d = 1, mmax = 1;
+    std::vector<int64_t> offs;
+    int64_t dir_stride = 0, rows_stride = 0, diag_stride = 0;
+    if (exact) {
       std::vector<int64_t> dpairs, dslot(nprob);
       {
         std::unordered_map<int64_t, int64_t> seen;
         for (int64_t k = 0; k < nprob; ++k) {
-          const int64_t pr = ids[k] / A.n_settings;
+          const int64_t pr = host_ids[k];
           auto it = seen.find(pr);
           if (it == seen.end()) it = seen.emplace(pr, (int64_t)dpairs.size()).first, dpairs.push_back(pr);
           dslot[k] = it->second;
         }
       }
-      std::vector<int32_t> pn(dpairs.size()), pm(dpairs.size());
-      for (size_t k = 0; k < dpairs.size(); ++k) {
-        BIMINE_CUDA(cudaMemcpyAsync(&pn[k], A.pair_n + dpairs[k], sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        BIMINE_CUDA(cudaMemcpyAsync(&pm[k], A.pair_m + dpairs[k], sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      // [distinct pairs] | pair diag offsets | per problem: diag, dirs, rows
+      nd = (int64_t)dpairs.size();
+      offs.resize(2 * nd + 3 * nprob);
+      int64_t *h_pairs = offs.data(), *h_pdoff = h_pairs + nd, *h_doff = h_pdoff + nd, *h_dir = h_doff + nprob,
+              *h_rows = h_dir + nprob;
+      std::vector<int64_t> first_prob(nd, -1);
+      for (int64_t k = 0; k < nprob; ++k)
+        if (first_prob[dslot[k]] < 0) first_prob[dslot[k]] = k;
+      for (int64_t q = 0; q < nd; ++q) {
+        const int n = (int)host_dims[2 * first_prob[q]], m = (int)host_dims[2 * first_prob[q] + 1];
+        h_pairs[q] = dpairs[q];
+        h_pdoff[q] = dtotal;
+        gmax_d = std::max(gmax_d, (n + 31) / 32);
+        mmax = std::max(mmax, m);
+        dtotal += (int64_t)((n + 31) / 32) * nw_diag_steps(m) * 32;
       }
-      BIMINE_CUDA(cudaStreamSynchronize(st));
-      int64_t dtotal = 0;
-      int gmax_d = 1;
-      std::vector<int64_t> pair_doff(dpairs.size()), doff(nprob);
-      for (size_t k = 0; k < dpairs.size(); ++k) {
-        pair_doff[k] = dtotal;
-        const int g = (pn[k] + 31) / 32;
-        gmax_d = std::max(gmax_d, g);
-        dtotal += (int64_t)g * nw_diag_steps(pm[k]) * 32;
+      for (int64_t k = 0; k < nprob; ++k) {
+        const int n = (int)host_dims[2 * k], m = (int)host_dims[2 * k + 1];
+        h_doff[k] = h_pdoff[dslot[k]];
+        h_dir[k] = dirtotal;
+        dirtotal += (lean_dir_words16(n, m) + 1) / 2;
+        h_rows[k] = rowtotal;
+        rowtotal += 2 * ((int64_t)m + 1);
       }
-      for (int64_t k = 0; k < nprob; ++k) doff[k] = pair_doff[dslot[k]];
-      if (gmax_d > 65535 || (int64_t)dpairs.size() > 65535) return fail(BIMINE_E_LIMIT, "nw: large problem too tall");
-      BIMINE_CUDA(cudaMallocAsync((void **)&diag, sizeof(double) * std::max<int64_t>(dtotal, 1), st));
-      BIMINE_CUDA(cudaMallocAsync((void **)&d_pairs, sizeof(int64_t) * dpairs.size(), st));
-      BIMINE_CUDA(cudaMallocAsync((void **)&d_pair_doff, sizeof(int64_t) * dpairs.size(), st));
-      BIMINE_CUDA(cudaMallocAsync((void **)&d_doff, sizeof(int64_t) * nprob, st));
-      BIMINE_CUDA(cudaMemcpyAsync(d_pairs, dpairs.data(), sizeof(int64_t) * dpairs.size(), cudaMemcpyHostToDevice, st));
-      BIMINE_CUDA(cudaMemcpyAsync(d_pair_doff, pair_doff.data(), sizeof(int64_t) * dpairs.size(), cudaMemcpyHostToDevice, st));
-      BIMINE_CUDA(cudaMemcpyAsync(d_doff, doff.data(), sizeof(int64_t) * nprob, cudaMemcpyHostToDevice, st));
-      const int mmax = *std::max_element(pm.begin(), pm.end());
+    } else {
+      gmax_d = (max_n + 31) / 32;
+      mmax = max_m;
+      nd = A.problem_ids ? nprob : nprob / A.n_settings;  // listed problems: a layout each
+      dir_stride = (lean_dir_words16(max_n, max_m) + 1) / 2;
+      rows_stride = 2 * ((int64_t)max_m + 1);
+      diag_stride = (int64_t)gmax_d * nw_diag_steps(max_m) * 32;
+      dtotal = nd * diag_stride;
+      dirtotal = nprob * dir_stride;
+      rowtotal = nprob * rows_stride;
+    }
+    double *diag = nullptr, *lastv = nullptr;
+    int64_t *d_offs = nullptr;
+    uint32_t *dirs = nullptr;
+    double2 *rows = nullptr;
+    BIMINE_CUDA(cudaMallocAsync((void **)&diag, sizeof(double) * std::max<int64_t>(dtotal, 1), st));
+    BIMINE_CUDA(cudaMallocAsync((void **)&d_offs, sizeof(int64_t) * (2 * nd + 3 * nprob), st));
+    BIMINE_CUDA(cudaMallocAsync((void **)&dirs, sizeof(uint32_t) * std::max<int64_t>(dirtotal, 1), st));
+    BIMINE_CUDA(cudaMallocAsync((void **)&lastv, sizeof(double) * nprob, st));
+    BIMINE_CUDA(cudaMallocAsync((void **)&rows, sizeof(double2) * std::max<int64_t>(rowtotal, 1), st));
+    if (exact) {  // (pageable: the call returns once `offs` is copied)
+      BIMINE_CUDA(cudaMemcpyAsync(d_offs, offs.data(), sizeof(int64_t) * offs.size(), cudaMemcpyHostToDevice, st));
+    } else {
+      uniform_offsets_kernel<<<(unsigned)std::min<int64_t>((nprob + 255) / 256, 4096), 256, 0, st>>>(
+          A.problem_ids, nprob, A.n_settings, nd, dir_stride, rows_stride, diag_stride, d_offs);
+      BIMINE_CUDA(cudaGetLastError());
+    }
+    BIMINE_CUDA(cudaMemsetAsync(rows, 0xff, sizeof(double2) * std::max<int64_t>(rowtotal, 1), st));
+    const int64_t *dd_pairs = d_offs, *dd_pdoff = d_offs + nd, *dd_doff = dd_pdoff + nd, *dd_dir = dd_doff + nprob,
+                  *dd_rows = dd_dir + nprob;
+    {
       const int64_t per_band = nw_diag_steps(mmax) * 32;
-      const dim3 grid((unsigned)std::min<int64_t>((per_band + 255) / 256, 64), (unsigned)gmax_d, (unsigned)dpairs.size());
-      nw_diag_kernel<<<grid, 256, 0, st>>>(A.sim, A.sim_off, A.pair_n, A.pair_m, d_pairs, d_pair_doff, 0, A.mismatch,
+      const dim3 grid((unsigned)std::min<int64_t>((per_band + 255) / 256, 64), (unsigned)std::min(gmax_d, 65535),
+                      (unsigned)std::min<int64_t>(nd, 65535));
+      nw_diag_kernel<<<grid, 256, 0, st>>>(A.sim, A.sim_off, A.pair_n, A.pair_m, dd_pairs, dd_pdoff, nd, A.mismatch,
                                            A.bonus - A.mismatch, diag);  // one IEEE subtraction, as fsub
       BIMINE_CUDA(cudaGetLastError());
     }
-    uint32_t *dirs = nullptr;
-    double *lastv = nullptr;
-    BIMINE_CUDA(cudaMallocAsync((void **)&dirs, sizeof(uint32_t) * stride * nprob, st));
-    BIMINE_CUDA(cudaMallocAsync((void **)&lastv, sizeof(double) * nprob, st));
-    // wrap-around rows: [2][max_m + 1] tagged slots per problem, tags -1
-    const int64_t rows_stride = 2 * ((int64_t)max_m + 1);
-    double2 *rows = nullptr;
-    BIMINE_CUDA(cudaMallocAsync((void **)&rows, sizeof(double2) * rows_stride * nprob, st));
-    BIMINE_CUDA(cudaMemsetAsync(rows, 0xff, sizeof(double2) * rows_stride * nprob, st));
-    BIMINE_CUDA(cudaLaunchKernelEx(&cfg, kern, A, dirs, stride, rows, rows_stride, lastv, (const double *)diag,
-                                   (const int64_t *)d_doff, diag_stride));
+    BIMINE_CUDA(cudaLaunchKernelEx(&cfg, kern, A, dirs, dd_dir, rows, dd_rows, lastv, (const double *)diag, dd_doff));
     if (MODE != kNwTable && !skip_tb)
-      nw_big_traceback_kernel<MODE><<<(unsigned)nprob, 32, 0, st>>>(A, dirs, stride, lastv);
+      nw_big_traceback_kernel<MODE><<<(unsigned)std::min<int64_t>(nprob, 1 << 20), 32, 0, st>>>(A, dirs, dd_dir,
+                                                                                                    lastv, nprob);
     const cudaError_t e = cudaGetLastError();
     cudaFreeAsync(dirs, st);
     cudaFreeAsync(rows, st);
     cudaFreeAsync(lastv, st);
     cudaFreeAsync(diag, st);
-    cudaFreeAsync(d_pairs, st);
-    cudaFreeAsync(d_pair_doff, st);
-    cudaFreeAsync(d_doff, st);
+    cudaFreeAsync(d_offs, st);
     if (e != cudaSuccess) return fail(BIMINE_E_CUDA, std::string("nw_big_kernel: ") + cudaGetErrorString(e));
     return BIMINE_OK;
   }
@@ -904,9 +929,12 @@ int bimine_mine_batch(const bimine_dict *dict, const double *model, const bimine
   }
   if (plan->n_large > 0) {
     NwArgs Al = A;
-    Al.problem_ids = plan->work + 3 * plan->n_tiles + plan->n_long;
+    const int64_t at = 3 * plan->n_tiles + plan->n_long;
+    Al.problem_ids = plan->work + at;
     Al.n_problems = plan->n_large;
-    rc = launch_nw<kNwMine>(Al, plan->max_n, plan->max_m, st);
+    const int64_t *hw = plan->work_host;
+    rc = launch_nw<kNwMine>(Al, plan->max_n, plan->max_m, st, hw ? hw + at : nullptr,
+                            hw ? hw + at + plan->n_large : nullptr);
   }
   return rc;
 }
@@ -967,13 +995,32 @@ int bimine_agreement_batch(const bimine_match *matches_dev, const int64_t *out_o
   const int mk = std::max(1, max_k), mr = std::max(1, max_r);
   A.row_doubles_per_warp = ((mr + 1) + 1) & ~1;
   const int64_t dw = (int64_t)(mk + 1) * ((mr >> 4) + 1);
-  const size_t per_block = (size_t)kNwWarpsPerBlock * (A.row_doubles_per_warp * 8 + dw * 4);
-  if (per_block > kNwSmemPerBlockMax) return fail(BIMINE_E_LIMIT, "bimine_agreement_batch: lists too long");
-  A.dir_words_per_warp = (int)dw;
-  BIMINE_CUDA(cudaFuncSetAttribute(agree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per_block));
-  agree_kernel<<<(unsigned)((n + kNwWarpsPerBlock - 1) / kNwWarpsPerBlock), kNwWarpsPerBlock * 32, per_block,
-                 as_stream(stream)>>>(A);
-  BIMINE_CUDA(cudaGetLastError());
+  A.dir_words_per_warp = dw;
+  A.g_rows = nullptr;
+  A.g_dirs = nullptr;
+  cudaStream_t st = as_stream(stream);
+  const size_t per_warp = (size_t)A.row_doubles_per_warp * 8 + (size_t)dw * 4;
+  const size_t per_block = (size_t)kNwWarpsPerBlock * per_warp;
+  if (per_block <= kNwSmemPerBlockMax) {
+    BIMINE_CUDA(cudaFuncSetAttribute(agree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per_block));
+    agree_kernel<<<(unsigned)((n + kNwWarpsPerBlock - 1) / kNwWarpsPerBlock), kNwWarpsPerBlock * 32, per_block,
+                   st>>>(A);
+    BIMINE_CUDA(cudaGetLastError());
+    return BIMINE_OK;
+  }
+  // long lists: each launched warp gets a global scratch slot (<= ~2 GiB in all)
+  int64_t warps = std::min<int64_t>(n, (int64_t)num_sms() * 16);
+  warps = std::max<int64_t>(1, std::min<int64_t>(warps, (int64_t)(((size_t)2 << 30) / per_warp)));
+  const int64_t blocks = (warps + kNwWarpsPerBlock - 1) / kNwWarpsPerBlock;
+  const int64_t slots = blocks * kNwWarpsPerBlock;
+  char *scratch = nullptr;
+  BIMINE_CUDA(cudaMallocAsync((void **)&scratch, per_warp * slots + 16, st));
+  A.g_rows = (double *)scratch;
+  A.g_dirs = (uint32_t *)(scratch + (size_t)A.row_doubles_per_warp * 8 * slots);
+  agree_kernel<<<(unsigned)blocks, kNwWarpsPerBlock * 32, 0, st>>>(A);
+  const cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return fail(BIMINE_E_CUDA, std::string("agree_kernel: ") + cudaGetErrorString(e));
   return BIMINE_OK;
 }
 
@@ -1060,7 +1107,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   // pinned staging: slot offsets [P] | per-pair need [P] (int32) | ready values [nt + 1] | merged work
   int64_t work_bound = 0;
   for (int64_t p = 0; p < P; ++p)
-    work_bound += 1 + 3 * (int64_t)((h->pair_n[p] + kPairMax - 1) / kPairMax) * ((h->pair_m[p] + kPairMax - 1) / kPairMax);
+    work_bound += 3 + 3 * (int64_t)((h->pair_n[p] + kPairMax - 1) / kPairMax) * ((h->pair_m[p] + kPairMax - 1) / kPairMax);
   const int64_t n_stage = P + (P + 1) / 2 + (nt + 2) / 2 + 1 + std::max<int64_t>(work_bound, 1);
   int64_t *staging = (int64_t *)pinned_scratch(sizeof(int64_t) * n_stage);
   if (!staging) return fail(BIMINE_E_CUDA, "bimine_mine_host: pinned staging allocation failed");
@@ -1212,7 +1259,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
       c.packed = ok;
     }
     const int64_t p0 = cut[k], p1 = cut[k + 1];
-    int64_t wcap = p1 - p0;
+    int64_t wcap = 3 * (p1 - p0);
     for (int64_t p = p0; p < p1; ++p) {
       const int32_t n = h->pair_n[p], m = h->pair_m[p];
       wcap += 3 * (int64_t)((n + kPairMax - 1) / kPairMax) * ((m + kPairMax - 1) / kPairMax);
@@ -1290,9 +1337,9 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     plan.n_large += q.n_large;
     plan.n_cells = std::max(plan.n_cells, q.n_cells);
   }
-  plan.work_len = 3 * plan.n_tiles + plan.n_long + plan.n_large;
+  plan.work_len = 3 * plan.n_tiles + plan.n_long + 3 * plan.n_large;
   {
-    int64_t t = 0, l = 3 * plan.n_tiles, g = l + plan.n_long;
+    int64_t t = 0, l = 3 * plan.n_tiles, g = l + plan.n_long, gd = g + plan.n_large;
     for (int k = 0; k < nc; ++k) {
       const bimine_plan &q = ci[k].plan;
       const int64_t *w = ci[k].work.data(), p0 = cut[k];
@@ -1302,7 +1349,12 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
         work[3 * t + 2] = w[3 * x + 2];
       }
       for (int64_t x = 0; x < q.n_long; ++x) work[l++] = w[3 * q.n_tiles + x] + p0;
-      for (int64_t x = 0; x < q.n_large; ++x) work[g++] = w[3 * q.n_tiles + q.n_long + x] + p0;
+      const int64_t *lw = w + 3 * q.n_tiles + q.n_long;
+      for (int64_t x = 0; x < q.n_large; ++x) {
+        work[g++] = lw[x] + p0;
+        work[gd++] = lw[q.n_large + 2 * x];
+        work[gd++] = lw[q.n_large + 2 * x + 1];
+      }
     }
   }
   e = cudaMemcpyAsync(arena + o_work, work, 8 * plan.work_len, cudaMemcpyHostToDevice, st);
@@ -1324,6 +1376,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     d.pair_m = (const int32_t *)(arena + o_pm);
     d.pair_sim_off = (const int64_t *)(arena + o_psim);
     plan.work = (const int64_t *)(arena + o_work);
+    plan.work_host = work;
     const UploadGate gate{(const int32_t *)(arena + o_ready), (const int32_t *)(arena + o_need), ev_all,
                           join_uploader};
     tl_gate = &gate;

@@ -560,22 +560,41 @@ struct AgreeArgs {
   const int64_t *ref_off;  // [pairs] first pair
   const int32_t *ref_len;  // [pairs]
   int32_t *matched;        // [problems]
-  int dir_words_per_warp;
-  int row_doubles_per_warp;
+  int64_t dir_words_per_warp;
+  int64_t row_doubles_per_warp;
+  double *g_rows;          // global scratch per launched warp (null: shared memory)
+  uint32_t *g_dirs;
 };
 
 __device__ __forceinline__ bool agree_eq(const bimine_match *cand, const int32_t *ref, int a, int b) {
   return cand[a].i == ref[2 * b] && cand[a].j == ref[2 * b + 1];
 }
 
+__device__ void agree_problem(const AgreeArgs &A, int64_t q, double *rowbuf, uint32_t *dirs);
+
+// Warps loop over (pair, setting) problems; each warp's row buffer and
+// direction table sit in dynamic shared memory, or (lists too long for it)
+// in a global scratch slot per launched warp.
 __global__ void __launch_bounds__(128) agree_kernel(const AgreeArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  if (q >= A.n_problems) return;
-  double *rowbuf = (double *)smem_raw + (size_t)warp * A.row_doubles_per_warp;
-  uint32_t *dirs = (uint32_t *)((double *)smem_raw + (size_t)(blockDim.x >> 5) * A.row_doubles_per_warp) +
-                   (size_t)warp * A.dir_words_per_warp;
+  const int warp = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  double *rowbuf;
+  uint32_t *dirs;
+  if (A.g_rows) {
+    rowbuf = A.g_rows + gw * A.row_doubles_per_warp;
+    dirs = A.g_dirs + gw * A.dir_words_per_warp;
+  } else {
+    rowbuf = (double *)smem_raw + (size_t)warp * A.row_doubles_per_warp;
+    dirs = (uint32_t *)((double *)smem_raw + (size_t)(blockDim.x >> 5) * A.row_doubles_per_warp) +
+           (size_t)warp * A.dir_words_per_warp;
+  }
+  for (int64_t q = gw; q < A.n_problems; q += nw) agree_problem(A, q, rowbuf, dirs);
+}
+
+__device__ void agree_problem(const AgreeArgs &A, int64_t q, double *rowbuf, uint32_t *dirs) {
+  const int lane = threadIdx.x & 31;
   const int64_t pair = q / A.n_settings;
   const int K = A.counts[q];
   const int R = A.ref_len[pair];
@@ -652,6 +671,7 @@ __global__ void __launch_bounds__(128) agree_kernel(const AgreeArgs A) {
     }
     A.matched[q] = m;
   }
+  __syncwarp();  // the warp's scratch is reused by its next problem
 }
 
 }  // namespace bimine
@@ -848,24 +868,49 @@ __global__ void __launch_bounds__(256) nw_diag_kernel(const double *__restrict__
                                                        const int32_t *__restrict__ pair_n,
                                                        const int32_t *__restrict__ pair_m,
                                                        const int64_t *__restrict__ pairs,
-                                                       const int64_t *__restrict__ diag_off, int64_t diag_stride,
+                                                       const int64_t *__restrict__ diag_off, int64_t n_pairs,
                                                        double mismatch, double span, double *__restrict__ diag_all) {
-  const int64_t ps = blockIdx.z;
-  const int g = blockIdx.y;
-  const int64_t pair = pairs ? pairs[ps] : ps;  // null: pairs 0, 1, ... at a uniform stride
-  const int N = pair_n[pair], M = pair_m[pair];
-  if (32 * g >= N) return;
-  const double *__restrict__ sim = sim_all + sim_off[pair];
-  const int64_t S = nw_diag_steps(M);
-  double *__restrict__ out = diag_all + (diag_off ? diag_off[ps] : ps * diag_stride) + (int64_t)g * S * 32;
-  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < S * 32; x += (int64_t)gridDim.x * blockDim.x) {
-    const int l = (int)(x & 31);
-    const int64_t st = x >> 5;
-    const int a = 32 * g + 1 + l;
-    const int64_t b = st - l + 1;
-    double v = 0.0;
-    if (a <= N && b >= 1 && b <= M) v = fadd(mismatch, fmul(sim[(int64_t)(N - a) * M + (M - b)], span));
-    out[x] = v;
+  for (int64_t ps = blockIdx.z; ps < n_pairs; ps += gridDim.z) {  // distinct pairs
+    const int64_t pair = pairs[ps];
+    const int N = pair_n[pair], M = pair_m[pair];
+    const double *__restrict__ sim = sim_all + sim_off[pair];
+    const int64_t S = nw_diag_steps(M);
+    for (int g = blockIdx.y; 32 * g < N; g += gridDim.y) {
+      double *__restrict__ out = diag_all + diag_off[ps] + (int64_t)g * S * 32;
+      for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < S * 32;
+           x += (int64_t)gridDim.x * blockDim.x) {
+        const int l = (int)(x & 31);
+        const int64_t st = x >> 5;
+        const int a = 32 * g + 1 + l;
+        const int64_t b = st - l + 1;
+        double v = 0.0;
+        if (a <= N && b >= 1 && b <= M) v = fadd(mismatch, fmul(sim[(int64_t)(N - a) * M + (M - b)], span));
+        out[x] = v;
+      }
+    }
+  }
+}
+
+// Uniform per-problem scratch offsets (the layout of launch_nw's exact
+// host offsets: [layouts] pair ids | layout offsets | per problem: layout,
+// directions, wrap rows).  Listed problems get a layout each; without a
+// list, problem q = pair * n_settings + setting shares its pair's.
+__global__ void uniform_offsets_kernel(const int64_t *__restrict__ ids, int64_t n, int32_t n_settings, int64_t nd,
+                                       int64_t dir_stride, int64_t rows_stride, int64_t diag_stride,
+                                       int64_t *__restrict__ offs) {
+  int64_t *pairs = offs, *pdoff = offs + nd, *doff = pdoff + nd, *dir = doff + n, *rows = dir + n;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t layout = ids ? k : k / n_settings;
+    if (ids) {
+      pairs[k] = ids[k] / n_settings;
+      pdoff[k] = k * diag_stride;
+    } else if (k % n_settings == 0) {
+      pairs[layout] = layout;
+      pdoff[layout] = layout * diag_stride;
+    }
+    doff[k] = layout * diag_stride;
+    dir[k] = k * dir_stride;
+    rows[k] = k * rows_stride;
   }
 }
 
@@ -927,10 +972,10 @@ struct BotRemote {  // lane 31 writes ring 0 of the next CTA of the cluster
 };
 
 template <int MODE, int W>
-__global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t *g_dirs_all, int64_t dir_stride,
-                                                        double2 *g_rows, int64_t rows_stride, double *last_val,
-                                                        const double *diag_all, const int64_t *diag_off,
-                                                        int64_t diag_stride) {
+__global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t *g_dirs_all,
+                                                        const int64_t *dir_off, double2 *g_rows,
+                                                        const int64_t *rows_off, double *last_val,
+                                                        const double *diag_all, const int64_t *diag_off) {
   extern __shared__ __align__(16) unsigned char big_smem[];
   BigRing *rings = (BigRing *)big_smem;  // [W], ring w feeds warp w
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -943,12 +988,12 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
   const double gap = nw_gap(A, q, setting);
   const double ng = -gap, mismatch = A.mismatch, span = fsub(A.bonus, A.mismatch);
   const int G = (N + 31) >> 5, G8 = nw_groups(M);
-  uint16_t *dirs = (uint16_t *)(g_dirs_all + slot * dir_stride);  // [G][G8][32]
-  double2 *wrap = g_rows + slot * rows_stride;                // [2][M+1] tagged, pre-filled with tag -1
+  uint16_t *dirs = (uint16_t *)(g_dirs_all + dir_off[slot]);  // [G][G8][32]
+  double2 *wrap = g_rows + rows_off[slot];                    // [2][M+1] tagged, pre-filled with tag -1
   const long long W1 = (long long)M + 1;
   const int per_round = W * K;
-  // [G][nw_diag_steps(M)][32], per pair: listed offsets, or a uniform stride per pair index
-  const double *__restrict__ diag = diag_all + (diag_off ? diag_off[slot] : pair * diag_stride);
+  // [G][nw_diag_steps(M)][32]: the problem's pair's block of the operand layout
+  const double *__restrict__ diag = diag_all + diag_off[slot];
   const int64_t dstride = nw_diag_steps(M) * 32;
 #if defined(BIMINE_NW_PROFILE) || defined(BIMINE_PROF_ENTRY)
   if (threadIdx.x == 0) {
@@ -1037,9 +1082,20 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
 // Traceback + threshold filter of large problems (one warp per problem),
 // over the 2-bit directions the band pipeline wrote.
 template <int MODE>
+__device__ void nw_big_traceback_one(const NwArgs &A, const uint32_t *g_dirs_all, const int64_t *dir_off,
+                                     const double *last_val, int64_t slot);
+
+template <int MODE>
 __global__ void __launch_bounds__(32) nw_big_traceback_kernel(const NwArgs A, const uint32_t *g_dirs_all,
-                                                                int64_t dir_stride, const double *last_val) {
-  const int64_t slot = blockIdx.x;
+                                                                const int64_t *dir_off, const double *last_val,
+                                                                int64_t n_slots) {
+  for (int64_t slot = blockIdx.x; slot < n_slots; slot += gridDim.x) nw_big_traceback_one<MODE>(A, g_dirs_all,
+                                                                                                dir_off, last_val, slot);
+}
+
+template <int MODE>
+__device__ void nw_big_traceback_one(const NwArgs &A, const uint32_t *g_dirs_all, const int64_t *dir_off,
+                                     const double *last_val, int64_t slot) {
   const int lane = threadIdx.x & 31, warp = 0;
   const int64_t q = A.problem_ids ? A.problem_ids[slot] : slot;
   const int64_t pair = q / A.n_settings;
@@ -1047,7 +1103,7 @@ __global__ void __launch_bounds__(32) nw_big_traceback_kernel(const NwArgs A, co
   const int N = A.pair_n[pair], M = A.pair_m[pair];
   const double *__restrict__ sim = A.sim + A.sim_off[pair];
   const int G8 = nw_groups(M);
-  const uint16_t *dirs = (const uint16_t *)(g_dirs_all + slot * dir_stride);  // [G][G8][32]
+  const uint16_t *dirs = (const uint16_t *)(g_dirs_all + dir_off[slot]);  // [G][G8][32]
   const double s_last = last_val[slot];
   if (MODE == kNwTable) return;
   // ---- traceback on warp 0: lane 0 walks, the warp stages 16 direction

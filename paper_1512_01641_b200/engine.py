@@ -115,8 +115,10 @@ class DeviceBatch:
             self.t[f] = a.to(f"cuda:{device}", non_blocking=pinned)
         self.struct = N.batch_struct_device(self.t, batch.n_pairs, batch.n_sentences, batch.n_tokens)
         self.plan, work = plan_batch(batch)
+        self.work_host = work  # kept alive: plan.work_host points into it
         self.t["work"] = torch.from_numpy(work).to(f"cuda:{device}")
         self.plan.work = self.t["work"].data_ptr() if work.size else None
+        self.plan.work_host = work.ctypes.data if work.size else None
         self.max_n, self.max_m = int(self.plan.max_n), int(self.plan.max_m)
         cap = batch.match_capacity()
         self.capacity = int(cap[-1])
@@ -128,7 +130,7 @@ def plan_batch(batch: PackedBatch):
     L = N.load(require_gpu=False)
     n = batch.pair_n.astype(np.int64)
     m = batch.pair_m.astype(np.int64)
-    cap = int(2 * batch.n_pairs + 3 * np.sum(((n + 63) // 64) * ((m + 63) // 64)))
+    cap = int(3 * batch.n_pairs + 3 * np.sum(((n + 63) // 64) * ((m + 63) // 64)))
     work = np.zeros(max(cap, 1), dtype=np.int64)
     plan = N.CPlan()
     cb = N.batch_struct_host(batch)

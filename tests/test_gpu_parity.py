@@ -360,7 +360,8 @@ def test_plan_tiles_for_large_pairs():
     plan, work = E.plan_batch(corpus.batch)
     assert plan.n_tiles == 3 * 3 * 2 and plan.n_long == 0
     assert work[: 3 * plan.n_tiles].reshape(-1, 3)[:, 0].tolist() == [0] * 6 + [1] * 6 + [2] * 6
-    assert plan.n_large == 3 and work[3 * plan.n_tiles:].tolist() == [0, 1, 2]
+    assert plan.n_large == 3 and work[3 * plan.n_tiles:3 * plan.n_tiles + 3].tolist() == [0, 1, 2]
+    assert work[3 * plan.n_tiles + 3:].tolist() == [130, 65] * 3  # the large pairs' (N, M)
     _synth_check(corpus)
 
 

@@ -174,3 +174,51 @@ def test_single_device_more_than_2e31_tokens():
         assert np.array_equal(allm[r], first), r
     del big, matches
     torch.cuda.empty_cache()
+
+
+def test_agreement_beyond_shared_memory_cap():
+    """alignment_agreement (tuning.py:60-82) on device for lists whose
+    direction table exceeds shared memory (500 candidates x 400 references:
+    ~221 KB per warp): the global-scratch path, against the oracle's NW on
+    the 0/1 equality matrix."""
+    from paper_1512_01641_b200 import _native as N
+
+    rng = np.random.default_rng(11)
+    P, S = 3, 2
+    K, R = 500, 400
+    dev = "cuda:0"
+    cand_lists, ref_lists = [], []
+    for p in range(P * S):
+        ii = np.sort(rng.choice(900, K, replace=False))
+        jj = np.sort(rng.choice(900, K, replace=False))
+        cand_lists.append(list(zip(ii.tolist(), jj.tolist())))
+    for p in range(P):
+        base = cand_lists[p * S]
+        keep = sorted(rng.choice(K, 250, replace=False).tolist())
+        extra = [(int(a), int(b)) for a, b in zip(rng.integers(0, 900, R - 250), rng.integers(0, 900, R - 250))]
+        ref_lists.append(sorted([base[k] for k in keep] + extra))
+    slots = np.zeros(P * S * K, dtype=N.MATCH_DTYPE)
+    for q, lst in enumerate(cand_lists):
+        slots["i"][q * K:(q + 1) * K] = [a for a, _ in lst]
+        slots["j"][q * K:(q + 1) * K] = [b for _, b in lst]
+    out_off = np.arange(P * S, dtype=np.int64) * K
+    counts = np.full(P * S, K, dtype=np.int32)
+    ref_ij = np.array([x for r in ref_lists for pr in r for x in pr], dtype=np.int32)
+    ref_off = np.arange(P, dtype=np.int64) * R
+    ref_len = np.full(P, R, dtype=np.int32)
+    t = {k: torch.from_numpy(v).to(dev) for k, v in dict(slots=slots.view(np.uint8), out_off=out_off, counts=counts,
+                                                         ref_ij=ref_ij, ref_off=ref_off, ref_len=ref_len).items()}
+    matched = torch.empty(P * S, dtype=torch.int32, device=dev)
+    L = N.load()
+    N.check(L.bimine_agreement_batch(t["slots"].data_ptr(), t["out_off"].data_ptr(), t["counts"].data_ptr(), P, S,
+                                     t["ref_ij"].data_ptr(), t["ref_off"].data_ptr(), t["ref_len"].data_ptr(), K, R,
+                                     matched.data_ptr(), E.stream_ptr()))
+    got = matched.cpu().numpy()
+    for q in range(P * S):
+        cand, ref = cand_lists[q], ref_lists[q // S]
+        eq = np.array([[1.0 if a == b else 0.0 for b in ref] for a in cand])
+        codes, si, sj, _ = oracle.nw_align(eq, -1.0, 1.0, 1.0)
+        want = int(((codes == 0) & (eq[si, sj] == 1.0)).sum())
+        assert got[q] == want, (q, got[q], want)
+        if q % S == 0:  # the setting whose candidates the references were drawn from
+            assert want > 100
