@@ -587,6 +587,7 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
     return fail(BIMINE_E_LIMIT, "bimine_score_batch: a sentence has more than 4096 distinct or 16384 total tokens");
   if (b->n_pairs > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: more than 2^31-1 pairs per call");
   if (plan->work_len > 0 && !plan->work) return fail(BIMINE_E_ARG, "bimine_score_batch: plan.work not set");
+  pool_setup();  // stream-ordered scratch stays cached (no remapping per call)
   const BatchDev bd = to_dev(*b);
   const DictDev dd = DictDev{dict->n_rows, dict->row_ptr, dict->tgt, dict->prob, dict->rowdesc, dict->ent};
   const Model md = to_model(model);
@@ -669,6 +670,7 @@ template <int MODE>
 int launch_nw(NwArgs A, int32_t max_n, int32_t max_m, cudaStream_t st, const int64_t *host_ids = nullptr,
               const int64_t *host_dims = nullptr) {
   if (A.n_problems == 0) return BIMINE_OK;
+  pool_setup();
   const int row_d = ((max_m + 1) + 1) & ~1;  // doubles, even
   const int64_t dir_w = (MODE == kNwTable) ? 0 : (lean_dir_words16(max_n, max_m) + 1) / 2;  // u32 words
   const size_t per_warp = (size_t)row_d * 8 + (size_t)dir_w * 4;
@@ -982,6 +984,7 @@ int bimine_agreement_batch(const bimine_match *matches_dev, const int64_t *out_o
     return fail(BIMINE_E_ARG, "bimine_agreement_batch: bad arguments");
   const int64_t n = n_pairs * n_settings;
   if (n == 0) return BIMINE_OK;
+  pool_setup();
   AgreeArgs A;
   A.matches = matches_dev;
   A.out_off = out_off_dev;
