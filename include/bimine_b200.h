@@ -166,7 +166,7 @@ int bimine_score_batch(const bimine_dict *dict, const double *model,
                        const bimine_batch *batch_dev, const bimine_plan *plan,
                        double *sim_dev, void *stream);
 
-/* ---- the fused mining step ---------------------------------------------
+/* ---- the mining step (score + NW + filter, one call) --------------------
  * build_score_matrix + nw_align + filter_by_threshold for every pair of a
  * device batch under one setting: sim_dev receives the score matrices
  * (written once); then one NW + traceback + filter launch for the pairs of
