@@ -454,19 +454,25 @@ def time_nw_and_score(R, dd, model, db, sim, out, steps, stream, flush, gap, thr
     return nw_ms, score_ms
 
 
+def pinned_batch(R, batch):
+    """The batch's arrays copied into page-locked memory (a streaming
+    caller's input buffers)."""
+    from paper_1512_01641_b200.packing import PackedBatch
+
+    pinned = {}
+    for f in ("tokens", "sent_tok_off", "sent_len", "sent_uniq", "sent_chars", "pair_src", "pair_n",
+              "pair_tgt", "pair_m", "pair_sim_off"):
+        pinned[f] = R.torch.from_numpy(np.ascontiguousarray(getattr(batch, f))).pin_memory().numpy()
+    return PackedBatch(**pinned, token_bytes=batch.token_bytes)
+
+
 def time_e2e(R, dd, model, batch, steps, warmup, stream, gap, thr, mism, bonus):
     """The same step end to end through bimine_mine_host: host batch in
     (pinned), counts + compacted matches out."""
     from paper_1512_01641_b200 import engine as E
-    from paper_1512_01641_b200.packing import PackedBatch
 
     torch = R.torch
-    pinned = {}
-    for f in ("tokens", "sent_tok_off", "sent_len", "sent_uniq", "sent_chars", "pair_src", "pair_n",
-              "pair_tgt", "pair_m", "pair_sim_off"):
-        a = torch.from_numpy(np.ascontiguousarray(getattr(batch, f))).pin_memory()
-        pinned[f] = a.numpy()
-    pb = PackedBatch(**pinned)
+    pb = pinned_batch(R, batch)
     n_steps = max(20, steps) if batch.n_pairs <= 20_000 else max(3, steps)
     outbuf = {}  # a streaming caller's host output buffers, refilled every step
     for _ in range(max(3, warmup) if batch.n_pairs <= 20_000 else 1):
@@ -585,15 +591,21 @@ def run_gpu(args):
     del flush
     step_ms = mine_ms + compact_ms
     e2e = None
-    e2e_pg = 0.0
+    e2e_pg = e2e_32 = 0.0
+    h2d_32 = 0
     if not args.no_e2e:
-        e2e_s, e2e_steps, h2d, d2h = time_e2e(R, dd, model, batch, K, args.warmup, stream, gap, thr, mism, bonus)
+        # the headline e2e uploads the compact wire form (24-bit ids) when the
+        # vocabulary allows it; int32 ids and pageable inputs beside it
+        wire = batch.with_24bit_tokens() if int(batch.tokens.max(initial=0)) < (1 << 24) else batch
+        e2e_s, e2e_steps, h2d, d2h = time_e2e(R, dd, model, wire, K, args.warmup, stream, gap, thr, mism, bonus)
+        if wire is not batch:
+            e2e_32, _, h2d_32, _ = time_e2e(R, dd, model, batch, K, args.warmup, stream, gap, thr, mism, bonus)
         if not strong:
             e2e_pg = time_e2e_pageable(R, dd, model, batch, e2e_steps, stream, gap, thr, mism, bonus)
     else:
         e2e_s, e2e_steps, h2d, d2h = 0.0, 0, 0, 0
     per = R.gather([step_ms, mine_ms, nw_ms, score_ms, e2e_s, float(batch.n_pairs), float(batch.n_cells),
-                    float(total_matches), e2e_pg])
+                    float(total_matches), e2e_pg, e2e_32])
     R.barrier()
     if R.rank != 0:
         R.close()
@@ -610,10 +622,13 @@ def run_gpu(args):
             "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h,
             "steps": e2e_steps,
-            "path": "bimine_mine_host (C ABI): pinned host inputs, results copied into reused page-locked host "
-                    "output buffers" + ("; per rank: the shared base sentences + its pair descriptors" if strong
-                                       else ""),
+            "path": "bimine_mine_host (C ABI): pinned host inputs (token ids in the 24-bit wire form, "
+                    "bimine_batch.token_bytes = 3), results copied into reused page-locked host output buffers"
+                    + ("; per rank: the shared base sentences + its pair descriptors" if strong else ""),
         }
+        if e2e_32:
+            e2e["int32_tokens"] = {"value": pairs_all * e2e_steps / max(cols[9]), "h2d_bytes_per_step": h2d_32,
+                                   "path": "the same call with int32 token ids"}
         if e2e_pg:
             e2e["pageable_inputs"] = {"value": pairs_all * e2e_steps / max(cols[8]),
                                       "path": "bimine_mine_host on the generator's pageable numpy arrays (staged "

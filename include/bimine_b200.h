@@ -61,7 +61,9 @@ typedef struct bimine_batch {
   int64_t n_pairs;
   int64_t n_sentences;
   int64_t n_tokens;
-  const int32_t *tokens;       /* [n_tokens] ids, sentences back to back          */
+  const int32_t *tokens;       /* [n_tokens] ids, sentences back to back; with
+                                  token_bytes == 3: 3 * n_tokens bytes, each id
+                                  little-endian in 24 bits (ids < 2^24)          */
   const int64_t *sent_tok_off; /* [n_sentences] first token of each sentence      */
   const int32_t *sent_len;     /* [n_sentences] token count (>= 1)                */
   const int32_t *sent_uniq;    /* [n_sentences] distinct token count              */
@@ -71,6 +73,8 @@ typedef struct bimine_batch {
   const int64_t *pair_tgt;     /* [n_pairs] index of the first target sentence    */
   const int32_t *pair_m;       /* [n_pairs] target sentence count M (>= 1)        */
   const int64_t *pair_sim_off; /* [n_pairs] offset of the row-major N x M block   */
+  int32_t token_bytes;         /* 4 (or 0): int32 ids; 3: packed 24-bit ids (the
+                                  upload of bimine_mine_host shrinks by a quarter) */
 } bimine_batch;
 
 /* Bilingual dictionary in CSR form over source ids (Lexicon,

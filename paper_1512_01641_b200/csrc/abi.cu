@@ -604,7 +604,9 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
     const int64_t cells = plan->n_cells;
     BIMINE_CUDA(cudaMallocAsync((void **)&A.aux, sizeof(uint16_t) * std::max<int64_t>(cells, 1), st));
     const size_t smem = kPairSmemBytes;
-    auto kern = features ? pair_kernel<true> : pair_kernel<false>;
+    const bool packed = b->token_bytes == 3;
+    auto kern = features ? (packed ? pair_kernel<true, true> : pair_kernel<true, false>)
+                         : (packed ? pair_kernel<false, true> : pair_kernel<false, false>);
     BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     // one launch: the tiles of pairs larger than 64x64, then one CTA per pair
@@ -1145,7 +1147,10 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     off = o + bytes;
     return o;
   };
-  const size_t o_tok = carve(4 * T), o_soff = carve(8 * S), o_slen = carve(4 * S), o_suniq = carve(4 * S),
+  if (h->token_bytes != 0 && h->token_bytes != 3 && h->token_bytes != 4)
+    return fail(BIMINE_E_ARG, "bimine_mine_host: token_bytes must be 3 or 4");
+  const int tb = h->token_bytes == 3 ? 3 : 4;  // bytes per token id on the wire and on the device
+  const size_t o_tok = carve((size_t)tb * T + 4), o_soff = carve(8 * S), o_slen = carve(4 * S), o_suniq = carve(4 * S),
                o_schar = carve(4 * S), o_psrc = carve(8 * P), o_pn = carve(4 * P), o_ptgt = carve(8 * P),
                o_pm = carve(4 * P), o_psim = carve(8 * P), o_outoff = carve(8 * P), o_sim = carve(8 * cells),
                o_slots = carve(sizeof(bimine_match) * cap), o_counts = carve(4 * P), o_base = carve(8 * P),
@@ -1212,7 +1217,8 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     H2D(o_ready, &ready_vals[0], 4, false);  // 1: pairs and sentences are in place
     phase1.set_value(ue);
     for (int j = 0; j < nt; ++j) {
-      H2D(o_tok + 4 * tcut[j], h->tokens + tcut[j], 4 * (tcut[j + 1] - tcut[j]), pg_tok);
+      H2D(o_tok + (size_t)tb * tcut[j], (const char *)h->tokens + (size_t)tb * tcut[j],
+          (size_t)tb * (tcut[j + 1] - tcut[j]), pg_tok);
       H2D(o_ready, &ready_vals[j + 1], 4, false);  // j + 2: token pieces 0..j
     }
     ue = ue ? ue : cudaEventRecord(ev_all, cs);
@@ -1369,6 +1375,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     d.n_sentences = S;
     d.n_tokens = T;
     d.tokens = (const int32_t *)(arena + o_tok);
+    d.token_bytes = tb;
     d.sent_tok_off = (const int64_t *)(arena + o_soff);
     d.sent_len = (const int32_t *)(arena + o_slen);
     d.sent_uniq = (const int32_t *)(arena + o_suniq);

@@ -11,9 +11,37 @@ namespace bimine {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Token ids as int32, or packed little-endian in 3 bytes each
+// (bimine_batch.token_bytes == 3): tokens[k] reads either (one uniform
+// branch per load).
+struct TokenView {
+  const int32_t *t32;
+  bool packed;
+  __device__ __forceinline__ int32_t operator[](int64_t k) const {
+    if (packed) {
+      const uint8_t *q = reinterpret_cast<const uint8_t *>(t32) + 3 * k;
+      return (int32_t)((uint32_t)__ldg(q) | ((uint32_t)__ldg(q + 1) << 8) | ((uint32_t)__ldg(q + 2) << 16));
+    }
+    return t32[k];
+  }
+};
+
+// The same with the width fixed at compile time (kernels instantiated per form).
+template <bool kPacked>
+struct TokenViewT {
+  const int32_t *t32;
+  __device__ __forceinline__ int32_t operator[](int64_t k) const {
+    if (kPacked) {
+      const uint8_t *q = reinterpret_cast<const uint8_t *>(t32) + 3 * k;
+      return (int32_t)((uint32_t)__ldg(q) | ((uint32_t)__ldg(q + 1) << 8) | ((uint32_t)__ldg(q + 2) << 16));
+    }
+    return t32[k];
+  }
+};
+
 // Device-side copy of the batch descriptor (all device pointers).
 struct BatchDev {
-  const int32_t *tokens;
+  TokenView tokens;
   const int64_t *sent_tok_off;
   const int32_t *sent_len;
   const int32_t *sent_uniq;
@@ -53,7 +81,7 @@ struct Model {
 };
 
 inline BatchDev to_dev(const bimine_batch &b) {
-  return BatchDev{b.tokens, b.sent_tok_off, b.sent_len, b.sent_uniq, b.sent_chars,
+  return BatchDev{TokenView{b.tokens, b.token_bytes == 3}, b.sent_tok_off, b.sent_len, b.sent_uniq, b.sent_chars,
                   b.pair_src, b.pair_n, b.pair_tgt, b.pair_m, b.pair_sim_off, b.n_pairs};
 }
 

@@ -203,8 +203,9 @@ __host__ __device__ inline bool pair_is_small(int n, int m, int max_len) {
   return n <= kPairMax && m <= kPairMax && max_len <= kPairMaxLen;
 }
 
-// kFeatures: also write the six features per cell (bimine_features_batch)
-template <bool kFeatures>
+// kFeatures: also write the six features per cell (bimine_features_batch);
+// kPacked: the batch's token ids are in the 24-bit form
+template <bool kFeatures, bool kPacked>
 __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PairSmem &S = *reinterpret_cast<PairSmem *>(smem_raw);
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
   const int N = min(kPairMax, Nfull - i0), M = min(kPairMax, Mfull - j0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t s_first = A.b.pair_src[p] + i0, t_first = A.b.pair_tgt[p] + j0;
-  const int32_t *__restrict__ tokens = A.b.tokens;
+  const TokenViewT<kPacked> tokens{A.b.tokens.t32};
   const uint64_t *__restrict__ rowdesc = A.d.rowdesc;
   const DictEntry *__restrict__ dent = A.d.ent;
   const int64_t n_rows = A.d.n_rows;

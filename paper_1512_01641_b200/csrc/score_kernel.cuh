@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const ScoreArgs
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int hbits = A.hash_bits;
   const int hslots = 1 << hbits;
-  const int32_t *__restrict__ tokens = A.b.tokens;
+  const TokenView tokens = A.b.tokens;
   const int64_t *__restrict__ row_ptr = A.d.row_ptr;
   const int32_t *__restrict__ dtgt = A.d.tgt;
   const double *__restrict__ dprob = A.d.prob;

@@ -113,7 +113,8 @@ class DeviceBatch:
             if pinned:
                 a = a.pin_memory()
             self.t[f] = a.to(f"cuda:{device}", non_blocking=pinned)
-        self.struct = N.batch_struct_device(self.t, batch.n_pairs, batch.n_sentences, batch.n_tokens)
+        self.struct = N.batch_struct_device(self.t, batch.n_pairs, batch.n_sentences, batch.n_tokens,
+                                            batch.token_bytes)
         self.plan, work = plan_batch(batch)
         self.work_host = work  # kept alive: plan.work_host points into it
         self.t["work"] = torch.from_numpy(work).to(f"cuda:{device}")
@@ -465,7 +466,7 @@ class DeviceTuner:
 
 def _torch_dtype(a: np.ndarray):
     torch = _torch()
-    return {np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64}[a.dtype]
+    return {np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64, np.dtype(np.uint8): torch.uint8}[a.dtype]
 
 
 def tune_device(dd: DeviceDictionary, model_vec: np.ndarray, batch: PackedBatch, thresholds, gaps,

@@ -222,3 +222,35 @@ def test_agreement_beyond_shared_memory_cap():
         assert got[q] == want, (q, got[q], want)
         if q % S == 0:  # the setting whose candidates the references were drawn from
             assert want > 100
+
+
+def test_24bit_token_ids_mine_identically():
+    """bimine_mine_host and the device-resident score path read 24-bit
+    packed ids (the compact upload form) with the same results as int32,
+    including ids at the 8/16/24-bit boundaries (a remapped vocabulary)."""
+    c = synth.make_config(2, n_pairs=300)
+    b = c.batch
+    model = model_vector(H.synth_model())
+    dd = _dd(c)
+    c32, m32, s32 = E.mine_host(dd, model, b, GAP, THRESHOLD, MISMATCH, BONUS, want_sim=True)
+    c32, m32, s32 = c32.copy(), m32.copy(), s32.copy()
+    p = b.with_24bit_tokens()
+    c24, m24, s24 = E.mine_host(dd, model, p, GAP, THRESHOLD, MISMATCH, BONUS, want_sim=True)
+    assert np.array_equal(c24, c32) and np.array_equal(m24.view(np.uint8), m32.view(np.uint8))
+    assert np.array_equal(s24.view(np.uint64), s32.view(np.uint64))
+    sim = torch.empty(b.n_cells, dtype=torch.float64, device="cuda:0")
+    E.score_device(dd, model, E.DeviceBatch(p, 0), sim)
+    assert np.array_equal(sim.cpu().numpy().view(np.uint64), s32.view(np.uint64))
+    # ids near 2^24: a bijective remap of every id used (dictionary included) keeps the scores
+    d = c.dictionary
+    used = np.unique(np.concatenate([b.tokens, d.src, d.tgt]))
+    hi = (1 << 24) - 1 - np.arange(used.size, dtype=np.int64)
+    hi[: min(3, hi.size)] = [0, 255, 256][: min(3, hi.size)]
+    remap = dict(zip(used.tolist(), hi.tolist()))
+    f = np.vectorize(remap.__getitem__, otypes=[np.int32])
+    rb = PackedBatch(**{**{k: getattr(b, k) for k in ("sent_tok_off", "sent_len", "sent_uniq", "sent_chars",
+                                                        "pair_src", "pair_n", "pair_tgt", "pair_m", "pair_sim_off")},
+                        "tokens": f(b.tokens)})
+    rdd = E.LexiconContext(vocab=None, coo=(f(d.src), f(d.tgt), d.prob), devices={}).on(0)
+    cr, mr, sr = E.mine_host(rdd, model, rb.with_24bit_tokens(), GAP, THRESHOLD, MISMATCH, BONUS, want_sim=True)
+    assert np.array_equal(sr.view(np.uint64), s32.view(np.uint64)) and np.array_equal(cr, c32)

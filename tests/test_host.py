@@ -2,6 +2,7 @@
 restatement, the C ABI surface, configuration and sharding logic."""
 
 import ctypes
+import dataclasses
 import os
 import re
 import subprocess
@@ -331,3 +332,19 @@ def test_native_and_python_builders_agree():
     for w in set(pv):
         inv[nb.vocab.get(w)] = w
     assert [inv[t] for t in a.tokens.tolist()] == [pv[t] for t in b.tokens.tolist()]
+
+
+def test_24bit_token_form_round_trip():
+    from paper_1512_01641_b200 import synth
+
+    b = synth.make_config(2, n_pairs=20).batch
+    p = b.with_24bit_tokens()
+    assert p.token_bytes == 3 and p.tokens.dtype == np.uint8 and p.tokens.size == 3 * b.n_tokens
+    assert p.n_tokens == b.n_tokens and p.nbytes() == b.nbytes() - b.n_tokens
+    assert np.array_equal(p.int32_tokens(), b.tokens)
+    edge = dataclasses.replace(b, tokens=np.array([0, 1, (1 << 24) - 1, 1 << 23, 255, 256] +
+                                                  [7] * (b.n_tokens - 6), dtype=np.int32))
+    assert np.array_equal(edge.with_24bit_tokens().int32_tokens(), edge.tokens)
+    for bad in (-1, 1 << 24):
+        with pytest.raises(ValueError):
+            dataclasses.replace(b, tokens=np.full(b.n_tokens, bad, dtype=np.int32)).with_24bit_tokens()
