@@ -1080,6 +1080,48 @@ int bimine_nw_fill_wavefront(double *dp, const double *sim, int64_t n, int64_t m
 // end to end from host buffers
 // ------------------------------------------------------------------------
 
+// Under lazy module loading (CUDA_MODULE_LOADING=LAZY, the CUDA 12 default)
+// a kernel is loaded at its first launch, and that load can wait for the
+// device to go idle.  bimine_mine_host's score kernel waits on copies still
+// in flight, so a first launch of another kernel while it waits (NW,
+// compaction, the offsets scan) risks a deadlock -- seen on B200 with an
+// earlier-launched score kernel.  Every kernel the path can launch is loaded
+// here first, once per device.
+cudaError_t preload_kernels(cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<int, bool> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return cudaSuccess;
+  const void *fns[] = {
+      (const void *)pair_kernel<false, false>, (const void *)pair_kernel<false, true>,
+      (const void *)pair_kernel<true, false>, (const void *)pair_kernel<true, true>,
+      (const void *)score_kernel, (const void *)build_term_tables,
+      (const void *)nw_kernel<kNwMine>, (const void *)nw_kernel<kNwSteps>, (const void *)nw_kernel<kNwTable>,
+      (const void *)nw_big_kernel<kNwMine, kBigW>, (const void *)nw_big_kernel<kNwSteps, kBigW>,
+      (const void *)nw_big_kernel<kNwTable, kBigW>, (const void *)nw_big_traceback_kernel<kNwMine>,
+      (const void *)nw_big_traceback_kernel<kNwSteps>, (const void *)nw_big_traceback_kernel<kNwTable>,
+      (const void *)nw_diag_kernel, (const void *)uniform_offsets_kernel, (const void *)scan_counts_kernel,
+      (const void *)gather_matches_kernel, (const void *)agree_kernel};
+  cudaFuncAttributes fa;
+  for (const void *f : fns) {
+    const cudaError_t e = cudaFuncGetAttributes(&fa, f);  // loads the kernel
+    if (e != cudaSuccess) return e;
+  }
+  // CUB's scan kernels are not nameable here: one scan of one length loads them
+  size_t bytes = 0;
+  cudaError_t e = offsets_from_lengths(nullptr, nullptr, 1, nullptr, &bytes, st);
+  char *buf = nullptr;
+  e = e ? e : cudaMallocAsync((void **)&buf, 64 + bytes, st);
+  e = e ? e : cudaMemsetAsync(buf, 0, 64, st);
+  e = e ? e : offsets_from_lengths((const int32_t *)buf, (int64_t *)(buf + 8), 1, buf + 64, &bytes, st);
+  if (buf) cudaFreeAsync(buf, st);
+  e = e ? e : cudaStreamSynchronize(st);
+  if (e == cudaSuccess) done[dev] = true;
+  return e;
+}
+
 int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_batch *h, double gap,
                      double threshold, double mismatch, double bonus, int32_t *counts_host,
                      bimine_match *matches_host, int64_t capacity, int64_t *total_host, double *sim_host,
@@ -1090,6 +1132,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   if (P == 0) return BIMINE_OK;
   pool_setup();
   cudaStream_t st = as_stream(stream);
+  BIMINE_CUDA(preload_kernels(st));
   // Uploads start at once on a copy stream: pair and sentence arrays, then
   // the tokens in `nt` equal pieces, a device counter bumped after each
   // (1 = pairs + sentences, 1 + j = token pieces 0..j-1).  Meanwhile host
