@@ -288,23 +288,15 @@ int bimine_tokenize_batch(bimine_vocab *vocab, const char *buf,
                           int64_t cap, int64_t *n_tokens, int32_t *len_out,
                           int32_t *uniq_out, int32_t *chars_out);
 /* The same with sentence k at ptrs[k] (lens[k] bytes) -- e.g. the caller's
- * own string storage, no concatenated copy; len_prefix[k] = sum of lens[0:k]
- * for k in 0..n (sizes the thread ranges). */
-/* The same over Python str objects the caller keeps alive (every one an
- * exact, compact ASCII str): obj[k] is the object's address, its length a
- * 64-bit integer at obj[k] + len_off, its characters at obj[k] + data_off
- * (CPython's PyASCIIObject, offsets probed by the caller).  Capacity needed
- * for tokens: sum(lengths) / 2 + n + 1. */
-int bimine_tokenize_strobjs(bimine_vocab *vocab, const int64_t *obj, int64_t n,
-                            int64_t data_off, int64_t len_off, int32_t *tokens,
-                            int64_t cap, int64_t *n_tokens, int32_t *len_out,
-                            int32_t *uniq_out, int32_t *chars_out);
+ * own string storage, no concatenated copy (the Python package passes the
+ * characters of compact ASCII str objects in place, csrc/pyhost.c);
+ * len_prefix[k] = sum of lens[0:k] for k in 0..n (sizes the thread
+ * ranges). */
 int bimine_tokenize_ptrs(bimine_vocab *vocab, const char *const *ptrs,
                          const int64_t *lens, int64_t n,
                          const int64_t *len_prefix, int32_t *tokens,
                          int64_t cap, int64_t *n_tokens, int32_t *len_out,
                          int32_t *uniq_out, int32_t *chars_out);
-
 /* Like bimine_score_batch, and also writes the six features of every cell
  * (extract_features / features_from_profiles, classifier.py:62-112) to
  * features_dev[6 * (pair_sim_off + i * M + j) + k], k = token ratio,

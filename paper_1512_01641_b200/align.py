@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import contextlib
 import gc
+import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 from typing import Sequence
@@ -245,6 +246,15 @@ def _shard_bounds(weights: np.ndarray, parts: int) -> list[tuple[int, int]]:
 
 
 CHUNK_PAIRS = 16_384  # pairs tokenised / mined per chunk of mine_corpus
+# stage timer of mine_corpus (bench.py's api_e2e): None, or a dict that
+# accumulates seconds per stage -- "pack" (tokenise + pack), "mine"
+# (bimine_mine_host), "rows" (result tuples)
+STAGE_TIMES: dict | None = None
+
+
+def _stage(name: str, t0: float) -> None:
+    if STAGE_TIMES is not None:
+        STAGE_TIMES[name] = STAGE_TIMES.get(name, 0.0) + time.perf_counter() - t0
 
 
 def _chunk_bounds(n: int, min_chunks: int) -> list[tuple[int, int]]:
@@ -259,14 +269,13 @@ def _mine_chunk(model, lexicon, pd, config: MiningConfig, device: int, topic_ids
     chunk, rows in input order.  A device-side limit (BimineError) must not
     abort the corpus: the chunk is then mined pair by pair and the pairs
     that still fail are reported (align.py:396-399, 441-447)."""
-    import operator
-
     import torch
 
     from ._native import BimineError
 
     keep = np.flatnonzero(pd.ok)
     failed: dict[int, str] = {}
+    t0 = time.perf_counter()
     with torch.cuda.device(device):
         try:
             counts, matches = _mine_packed(model, lexicon, pd.batch, config, device=device)
@@ -281,19 +290,20 @@ def _mine_chunk(model, lexicon, pd, config: MiningConfig, device: int, topic_ids
                 except BimineError as exc:
                     failed[lo + int(keep[b])] = f"pair {topic_ids[lo + int(keep[b])]}: {exc}"
             matches = np.concatenate(parts) if parts else np.zeros(0, dtype=_native_match_dtype())
+    _stage("mine", t0)
     # rows: every match's sentences by index into the chunk's sentence list
+    # (built natively, csrc/pyhost.c: ~10^5 - 10^7 tuples)
     if matches.shape[0] == 0:
         return [], failed
-    owner = np.repeat(keep, counts)  # input pair (within the chunk) of each match
-    src_idx = pd.start[owner] + matches["i"].astype(np.int64)
-    tgt_idx = pd.start[owner] + pd.n_src[owner] + matches["j"].astype(np.int64)
-    sents = pd.sentences
-    if src_idx.shape[0] == 1:
-        srcs, tgts = [sents[int(src_idx[0])]], [sents[int(tgt_idx[0])]]
-    else:
-        srcs = operator.itemgetter(*src_idx.tolist())(sents)
-        tgts = operator.itemgetter(*tgt_idx.tolist())(sents)
-    return list(zip(matches["score"].tolist(), srcs, tgts)), failed
+    t0 = time.perf_counter()
+    from .packing import _pyhost
+
+    first = pd.start[keep]
+    rows = _pyhost().build_rows(np.ascontiguousarray(matches), np.ascontiguousarray(counts, dtype=np.int64),
+                                np.ascontiguousarray(first, dtype=np.int64),
+                                np.ascontiguousarray(first + pd.n_src[keep], dtype=np.int64), pd.sentences)
+    _stage("rows", t0)
+    return rows, failed
 
 
 def _native_match_dtype():
@@ -342,7 +352,9 @@ def _mine_corpus(model, lexicon, pairs: Sequence, config: MiningConfig) -> Minin
     futures = []
     try:
         for c, (lo, hi) in enumerate(chunks):
+            t0 = time.perf_counter()
             pd = pack_documents(ctx.vocab, [(p.source.sentences, p.target.sentences) for p in pairs[lo:hi]])
+            _stage("pack", t0)
             for k, msg in pd.errors.items():
                 errors[lo + k] = f"pair {topic_ids[lo + k]}: {msg}"
             if pd.batch is None:

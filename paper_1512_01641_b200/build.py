@@ -3,9 +3,11 @@
     python -m paper_1512_01641_b200.build
 
 One nvcc invocation over csrc/abi.cu (which includes every kernel
-header).  The .so is written next to this file so it travels to the GPU
-box with the repository snapshot; the product loads it with ctypes and
-fails loudly when it is absent (see _native.py).
+header) and csrc/host_text.cpp; and the small CPython extension _pyhost
+(csrc/pyhost.c, gcc against the interpreter's headers).  Both are written
+next to this file so they travel to the GPU box with the repository
+snapshot; the product loads the library with ctypes and fails loudly when
+it is absent (see _native.py).
 """
 
 from __future__ import annotations
@@ -13,6 +15,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+import sysconfig
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -44,7 +47,25 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+PYHOST_SRC = os.path.join(CSRC, "pyhost.c")
+PYHOST = os.path.join(HERE, "_pyhost" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
+
+
+def build_pyhost(force: bool = False) -> str:
+    if not force and os.path.exists(PYHOST) and os.path.getmtime(PYHOST) >= os.path.getmtime(PYHOST_SRC):
+        return PYHOST
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-Wall", "-shared", "-fPIC", "-I" + sysconfig.get_paths()["include"],
+           PYHOST_SRC, "-o", PYHOST + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("gcc failed building _pyhost")
+    os.replace(PYHOST + ".tmp", PYHOST)
+    return PYHOST
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_pyhost(force)
     if not force and not stale():
         return LIB
     cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]

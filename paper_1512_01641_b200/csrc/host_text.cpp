@@ -29,8 +29,15 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <chrono>
+#include <cstdio>
 #include <thread>
+#include <new>
+#include <utility>
 #include <vector>
+
+#include <emmintrin.h>
+#include <sys/mman.h>
 
 #include "../../include/bimine_b200.h"
 
@@ -109,6 +116,45 @@ constexpr bool is_space(unsigned char c) {
   return c == ' ' || (c >= '\t' && c <= '\r') || (c >= 0x1c && c <= 0x1f);
 }
 
+// byte classes of the split: 1 = whitespace, 2 = punctuation
+struct ByteClass {
+  uint8_t c[256] = {};
+  constexpr ByteClass() {
+    const char *P = "!\"#$%&'()*+,-./:;<=>?@[\\]^_`{|}~";
+    for (int i = 0; P[i]; ++i) c[(unsigned char)P[i]] = 2;
+    for (int i = 0; i < 256; ++i)
+      if (is_space((unsigned char)i)) c[i] = 1;
+  }
+};
+constexpr ByteClass kClass;
+
+// A-Z -> a-z in each byte of w (other bytes, UTF-8 included, unchanged)
+inline uint64_t lower8(uint64_t w) {
+  const uint64_t h = w & 0x7F7F7F7F7F7F7F7Full;
+  const uint64_t ge_a = h + 0x3F3F3F3F3F3F3F3Full;  // high bit: >= 'A'
+  const uint64_t gt_z = h + 0x2525252525252525ull;  // high bit: > 'Z'
+  return w | (((ge_a ^ gt_z) & ~w & 0x8080808080808080ull) >> 2);
+}
+
+// the low n bytes of w (n in 0..8)
+inline uint64_t low_bytes(uint64_t w, uint32_t n) { return n >= 8 ? w : w & ((1ull << (8 * n)) - 1); }
+
+// hash_words of a word of n <= 16 bytes given as its two zero-padded words
+inline uint64_t hash_keys(uint64_t k0, uint64_t k1, uint32_t n) {
+  uint64_t h = 0x243F6A8885A308D3ull ^ ((uint64_t)n * 0x9E3779B97F4A7C15ull);
+  if (n > 0) {
+    h = (h ^ k0) * 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 31;
+  }
+  if (n > 8) {
+    h = (h ^ k1) * 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 31;
+  }
+  h ^= h >> 30;
+  h *= 0x94D049BB133111EBull;
+  return h ^ (h >> 29);
+}
+
 struct PunctTable {
   bool p[256] = {};
   constexpr PunctTable() {
@@ -136,7 +182,35 @@ struct bimine_vocab {
     uint32_t len;
     uint64_t key[2];  // first 16 bytes of the word, zero-padded
   };
-  std::vector<Slot> slots = std::vector<Slot>(1u << 16, Slot{0, -1, 0, {0, 0}});
+  // the slot array, 2 MB aligned and on transparent huge pages where the
+  // kernel allows: lookups are random over tens of MB, and with 4 KB pages
+  // nearly every one also missed the TLB
+  struct Slots {
+    Slot *p = nullptr;
+    size_t n = 0;
+    explicit Slots(size_t count) : n(count) {
+      const size_t bytes = ((count * sizeof(Slot)) + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);
+      p = static_cast<Slot *>(aligned_alloc(2u << 20, bytes));
+      if (!p) throw std::bad_alloc();
+#ifdef MADV_HUGEPAGE
+      madvise(p, bytes, MADV_HUGEPAGE);
+#endif
+      for (size_t i = 0; i < count; ++i) p[i] = Slot{0, -1, 0, {0, 0}};
+    }
+    Slots(const Slots &) = delete;
+    Slots &operator=(const Slots &) = delete;
+    ~Slots() { free(p); }
+    void swap(Slots &o) {
+      std::swap(p, o.p);
+      std::swap(n, o.n);
+    }
+    size_t size() const { return n; }
+    Slot &operator[](size_t i) { return p[i]; }
+    const Slot &operator[](size_t i) const { return p[i]; }
+    const Slot *begin() const { return p; }
+    const Slot *end() const { return p + n; }
+  };
+  Slots slots{1u << 16};
   size_t mask = (1u << 16) - 1;
   std::vector<const char *> word_ptr;  // id -> bytes in `blocks`
   std::vector<uint32_t> word_len;
@@ -152,6 +226,12 @@ struct bimine_vocab {
     uint64_t k0, k1;
     memcpy(&k0, w, 8);
     memcpy(&k1, w + 8, 8);
+    return find_keys(h, k0, k1, n, w);
+  }
+
+  // k0, k1: the word's first 16 bytes, zero-padded; w: the whole word
+  // (read only beyond byte 16)
+  int32_t find_keys(uint64_t h, uint64_t k0, uint64_t k1, uint32_t n, const char *w) const {
     for (size_t i = h & mask;; i = (i + 1) & mask) {
       const Slot &s = slots[i];
       if (s.id < 0) return -1;
@@ -184,7 +264,7 @@ struct bimine_vocab {
   }
 
   void grow() {
-    std::vector<Slot> old(slots.size() * 2, Slot{0, -1, 0, {0, 0}});
+    Slots old(slots.size() * 2);
     old.swap(slots);
     mask = slots.size() - 1;
     for (const Slot &s : old)
@@ -234,26 +314,100 @@ struct PtrSentences {
   int64_t len(int64_t k) const { return n[k]; }
 };
 
+// Whitespace bitmap of p[0, L): bit x of sp[x / 64] set when p[x] is
+// whitespace or x >= L (up to the end of the last word); returns false if
+// a byte is >= 0x80.  SSE2, 16 bytes per step.
+inline bool space_bitmap(const unsigned char *p, int64_t L, std::vector<uint64_t> &sp) {
+  const size_t nw = (size_t)(L >> 6) + 1;
+  if (sp.size() < nw) sp.resize(nw);
+  const __m128i c32 = _mm_set1_epi8(32), c9 = _mm_set1_epi8(9), c4 = _mm_set1_epi8(4), c28 = _mm_set1_epi8(28),
+                c3 = _mm_set1_epi8(3);
+  uint32_t hi = 0;
+  for (size_t w = 0; w < nw; ++w) {
+    uint64_t m = 0;
+    for (int q = 0; q < 4; ++q) {
+      const int64_t x = (int64_t)(w * 64 + q * 16);
+      __m128i v;
+      uint32_t tail = 0;  // positions >= L
+      if (x + 16 <= L) {
+        v = _mm_loadu_si128(reinterpret_cast<const __m128i *>(p + x));
+      } else {
+        alignas(16) unsigned char t[16] = {};
+        if (x < L) memcpy(t, p + x, (size_t)(L - x));
+        v = _mm_load_si128(reinterpret_cast<const __m128i *>(t));
+        tail = x >= L ? 0xFFFFu : (0xFFFFu << (L - x)) & 0xFFFFu;
+      }
+      hi |= (uint32_t)_mm_movemask_epi8(v);
+      const __m128i t1 = _mm_sub_epi8(v, c9), t2 = _mm_sub_epi8(v, c28);
+      const __m128i sp16 = _mm_or_si128(_mm_cmpeq_epi8(v, c32),
+                                        _mm_or_si128(_mm_cmpeq_epi8(_mm_min_epu8(t1, c4), t1),
+                                                     _mm_cmpeq_epi8(_mm_min_epu8(t2, c3), t2)));
+      m |= (uint64_t)(((uint32_t)_mm_movemask_epi8(sp16) | tail) & 0xFFFFu) << (q * 16);
+    }
+    sp[w] = m;
+  }
+  return hi == 0;
+}
+
+// first x' >= x whose bit in sp equals `want` (a bit past L is always set)
+inline int64_t next_bit(const uint64_t *sp, int64_t x, bool want) {
+  size_t w = (size_t)(x >> 6);
+  uint64_t m = (want ? sp[w] : ~sp[w]) & (~0ull << (x & 63));
+  while (!m) {
+    ++w;
+    m = want ? sp[w] : ~sp[w];
+  }
+  return (int64_t)(w * 64) + __builtin_ctzll(m);
+}
+
 template <class Sent>
 void tokenize_range(const bimine_vocab &v, const Sent &sent, TokRange &r, int32_t *len_out, int32_t *chars_out) {
-  std::vector<char> low;  // the sentence's words, each zero-padded (16 + round-up to 8)
+  // a token: its hash and first 16 bytes (lowered, zero-padded); a word
+  // longer than 16 bytes also has a lowered, padded copy in `low`
   struct Tok {
-    uint64_t hash;
-    uint32_t off, len;
+    uint64_t hash, k0, k1;
+    uint32_t len, off;
   };
-  std::vector<Tok> toks;
+  // two sentences in flight: sentence k is split (its vocabulary slots
+  // prefetched) before sentence k - 1's tokens are looked up
+  std::vector<Tok> toks[2];
+  std::vector<char> low[2];
   std::vector<unsigned char> lat;  // a Latin sentence, lowered
+  std::vector<uint64_t> sp;
+  {
+    int64_t bytes = 0;
+    for (int64_t k = r.k0; k < r.k1; ++k) bytes += sent.len(k);
+    r.tok.reserve((size_t)(bytes / 4 + (r.k1 - r.k0)));
+  }
+  auto resolve = [&](int64_t k, int par) {
+    const std::vector<Tok> &tk = toks[par];
+    for (const Tok &t : tk) {
+      const char *lw = t.len > 16 ? low[par].data() + t.off : nullptr;
+      int32_t id = v.find_keys(t.hash, t.k0, t.k1, t.len, lw);
+      if (id < 0) {  // the padded word for the insert phase
+        const uint32_t wo = (uint32_t)r.words.size(), padn = ((t.len + 7) & ~7u) + 16;
+        r.words.resize(wo + padn, 0);
+        char *w = r.words.data() + wo;
+        if (lw) {
+          memcpy(w, lw, padn);
+        } else {
+          memcpy(w, &t.k0, 8);
+          memcpy(w + 8, &t.k1, 8);
+        }
+        r.miss.push_back({t.hash, wo, t.len});
+        id = -(int32_t)r.miss.size();
+      }
+      r.tok.push_back(id);
+    }
+    len_out[k] = (int32_t)tk.size();
+  };
+  int64_t pending = -1;  // sentence whose tokens await lookup, in toks[cur ^ 1]
+  int cur = 0;
   for (int64_t k = r.k0; k < r.k1; ++k) {
     const unsigned char *p = sent.ptr(k);
     int64_t L = sent.len(k);
     chars_out[k] = (int32_t)L;
-    bool ascii = true;
-    for (int64_t x = 0; x < L; ++x)
-      if (p[x] >= 0x80) {
-        ascii = false;
-        break;
-      }
-    if (!ascii) {
+    if (!space_bitmap(p, L, sp)) {
       const int64_t cps = lower_latin_sentence(p, L, lat);
       if (cps < 0) {
         len_out[k] = -1;  // the caller applies the Unicode rules
@@ -262,61 +416,78 @@ void tokenize_range(const bimine_vocab &v, const Sent &sent, TokRange &r, int32_
       chars_out[k] = (int32_t)cps;  // len(text): code points
       p = lat.data();
       L = (int64_t)lat.size();
+      space_bitmap(p, L, sp);  // (whitespace is ASCII after lowering)
     }
-    low.resize((size_t)L + 12 * (size_t)(L + 1) + 32);  // <= (L+1)/2 tokens, each its bytes + <= 23
-    toks.clear();
-    uint32_t lo = 0;
-    int64_t x = 0;
-    while (x < L) {
-      while (x < L && is_space(p[x])) ++x;
+    std::vector<Tok> &tk = toks[cur];
+    std::vector<char> &lo = low[cur];
+    tk.clear();
+    lo.clear();
+    for (int64_t x = next_bit(sp.data(), 0, false); x < L; x = next_bit(sp.data(), x, false)) {
       int64_t a = x;
-      while (x < L && !is_space(p[x])) ++x;
+      x = next_bit(sp.data(), x, true);
       int64_t b = x;
-      while (a < b && kPunct.p[p[a]]) ++a;
-      while (b > a && kPunct.p[p[b - 1]]) --b;
-      if (b > a) {
-        const uint32_t n = (uint32_t)(b - a);
-        char *w = low.data() + lo;
+      while (a < b && kClass.c[p[a]] == 2) ++a;
+      while (b > a && kClass.c[p[b - 1]] == 2) --b;
+      if (b == a) continue;
+      const uint32_t n = (uint32_t)(b - a);
+      uint64_t k0, k1;
+      if (a + 16 <= L) {
+        memcpy(&k0, p + a, 8);
+        memcpy(&k1, p + a + 8, 8);
+      } else {
+        unsigned char t[16] = {};
+        memcpy(t, p + a, (size_t)std::min<int64_t>(16, L - a));
+        memcpy(&k0, t, 8);
+        memcpy(&k1, t + 8, 8);
+      }
+      k0 = lower8(low_bytes(k0, n));
+      k1 = n > 8 ? lower8(low_bytes(k1, n - 8)) : 0;
+      Tok t{0, k0, k1, n, 0};
+      if (n <= 16) {
+        t.hash = hash_keys(k0, k1, n);
+      } else {  // a long word: lowered, padded copy
+        t.off = (uint32_t)lo.size();
+        lo.resize(lo.size() + ((n + 7) & ~7u) + 16, 0);
+        char *w = lo.data() + t.off;
         for (uint32_t i = 0; i < n; ++i) {
           const unsigned char c = p[a + i];
           w[i] = (char)((unsigned)(c - 'A') < 26u ? c | 0x20 : c);
         }
-        memset(w + n, 0, 16);
-        const uint64_t h = hash_words(w, n);
-        __builtin_prefetch(v.slot_of(h));
-        toks.push_back({h, lo, n});
-        lo += ((n + 7) & ~7u) + 16;
+        t.hash = hash_words(w, n);
       }
+      __builtin_prefetch(v.slot_of(t.hash));
+      tk.push_back(t);
     }
-    for (const Tok &t : toks) {
-      int32_t id = v.find(t.hash, low.data() + t.off, t.len);
-      if (id < 0) {
-        const uint32_t wo = (uint32_t)r.words.size();
-        const char *w = low.data() + t.off;
-        r.words.insert(r.words.end(), w, w + ((t.len + 7) & ~7u) + 16);
-        r.miss.push_back({t.hash, wo, t.len});
-        id = -(int32_t)r.miss.size();
-      }
-      r.tok.push_back(id);
-    }
-    len_out[k] = (int32_t)toks.size();
+    if (pending >= 0) resolve(pending, cur ^ 1);
+    pending = k;
+    cur ^= 1;
   }
+  if (pending >= 0) resolve(pending, cur ^ 1);
 }
 
-void finish_range(TokRange &r, const int32_t *len_out, int32_t *uniq_out, int32_t *tokens) {
+// ids, and distinct ids per sentence by a per-thread stamp per id
+void finish_range(TokRange &r, const int32_t *len_out, int32_t *uniq_out, int32_t *tokens, int32_t n_ids) {
   int32_t *dst = tokens + r.out_off;
   const int32_t *src = r.tok.data();
-  std::vector<int32_t> scratch;
+  std::vector<uint32_t> stamp((size_t)std::max(n_ids, 1), 0u);
+  uint32_t tag = 0;
   for (int64_t k = r.k0; k < r.k1; ++k) {
     const int32_t n = len_out[k];
     if (n < 0) {
       uniq_out[k] = 0;
       continue;
     }
-    for (int32_t i = 0; i < n; ++i) dst[i] = src[i] >= 0 ? src[i] : r.resolved[-src[i] - 1];
-    scratch.assign(dst, dst + n);
-    std::sort(scratch.begin(), scratch.end());
-    uniq_out[k] = (int32_t)(std::unique(scratch.begin(), scratch.end()) - scratch.begin());
+    ++tag;
+    int32_t u = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      const int32_t id = src[i] >= 0 ? src[i] : r.resolved[-src[i] - 1];
+      dst[i] = id;
+      if (stamp[id] != tag) {
+        stamp[id] = tag;
+        ++u;
+      }
+    }
+    uniq_out[k] = u;
     dst += n;
     src += n;
   }
@@ -393,7 +564,14 @@ int tokenize_sentences(bimine_vocab *v, const Sent &sent, int64_t n, Prefix pref
     fn(R[0]);
     for (auto &th : pool) th.join();
   };
+#ifdef BIMINE_TOK_PROFILE
+  auto clk = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double c0 = clk();
+#endif
   parallel([&](TokRange &r) { tokenize_range(*v, sent, r, len_out, chars_out); });
+#ifdef BIMINE_TOK_PROFILE
+  const double c1 = clk();
+#endif
   int64_t total = 0;
   for (TokRange &r : R) {
     r.out_off = total;
@@ -405,7 +583,14 @@ int tokenize_sentences(bimine_vocab *v, const Sent &sent, int64_t n, Prefix pref
     for (size_t i = 0; i < r.miss.size(); ++i)
       r.resolved[i] = v->get(r.miss[i].hash, r.words.data() + r.miss[i].off, r.miss[i].len);
   }
-  parallel([&](TokRange &r) { finish_range(r, len_out, uniq_out, tokens); });
+#ifdef BIMINE_TOK_PROFILE
+  const double c2 = clk();
+#endif
+  const int32_t n_ids = v->size();
+  parallel([&](TokRange &r) { finish_range(r, len_out, uniq_out, tokens, n_ids); });
+#ifdef BIMINE_TOK_PROFILE
+  fprintf(stderr, "tokenize: %d threads, split %.1f ms, insert %.1f ms, finish %.1f ms\n", nt, c1 - c0, c2 - c1, clk() - c2);
+#endif
   *n_tokens = total;
   return BIMINE_OK;
 }
@@ -420,27 +605,6 @@ int bimine_tokenize_batch(bimine_vocab *v, const char *buf, const int64_t *off, 
     return BIMINE_E_ARG;
   const BufSentences sent{(const unsigned char *)buf, off};
   return tokenize_sentences(v, sent, n, [&](int64_t k) { return off[k] - off[0]; }, tokens, cap, n_tokens, len_out,
-                            uniq_out, chars_out);
-}
-
-int bimine_tokenize_strobjs(bimine_vocab *v, const int64_t *obj, int64_t n, int64_t data_off, int64_t len_off,
-                            int32_t *tokens, int64_t cap, int64_t *n_tokens, int32_t *len_out, int32_t *uniq_out,
-                            int32_t *chars_out) {
-  if (!v || !n_tokens || (n > 0 && (!obj || !len_out || !uniq_out || !chars_out)) || data_off <= 0 || len_off < 0)
-    return BIMINE_E_ARG;
-  std::vector<const unsigned char *> ptrs((size_t)std::max<int64_t>(n, 1));
-  std::vector<int64_t> lens((size_t)std::max<int64_t>(n, 1)), prefix((size_t)n + 1, 0);
-  for (int64_t k = 0; k < n; ++k) {
-    const char *o = (const char *)(intptr_t)obj[k];
-    int64_t L;
-    memcpy(&L, o + len_off, 8);
-    ptrs[k] = (const unsigned char *)o + data_off;
-    lens[k] = L;
-    prefix[k + 1] = prefix[k] + L;
-  }
-  if (prefix[n] / 2 + n + 1 > cap) return BIMINE_E_LIMIT;
-  const PtrSentences sent{ptrs.data(), lens.data()};
-  return tokenize_sentences(v, sent, n, [&](int64_t k) { return prefix[k]; }, tokens, cap, n_tokens, len_out,
                             uniq_out, chars_out);
 }
 

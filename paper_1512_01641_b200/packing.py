@@ -46,35 +46,11 @@ class Vocabulary:
         return np.fromiter((self.get(w) for w in words), dtype=np.int32)
 
 
-def _ascii_layout() -> tuple[int, int] | None:
-    """(character offset, length offset) inside a compact ASCII str object
-    (CPython's PyASCIIObject header), found by probing strings of several
-    lengths; None if the layout is not recognised (the encode path is used
-    then)."""
-    import ctypes
-    import struct
+def _pyhost():
+    """The CPython helper module (csrc/pyhost.c), built with the library."""
+    from . import _pyhost as m
 
-    try:
-        data, lens = set(), set()
-        for probe in ("bimine\x01probe\x02layout", "x" * 37 + "\x03", "\x04" * 5 + "q" * 300):
-            raw = ctypes.string_at(id(probe), 512)
-            data.add(raw.find(probe.encode("ascii")))
-            lens.add(next((o for o in range(8, 64, 8) if struct.unpack_from("<q", raw, o)[0] == len(probe)), -1))
-        d, n = (data.pop() if len(data) == 1 else -1), (lens.pop() if len(lens) == 1 else -1)
-        return (d, n) if 0 < d <= 128 and 0 < n < d else None
-    except Exception:  # pragma: no cover - unusual interpreters
-        return None
-
-
-_ASCII_LAYOUT = _ascii_layout()
-
-
-def _str_objects(strings: list[str]):
-    """The strings' object addresses when every one is an exact, compact
-    ASCII str (the tokenizer then reads them in place), else None."""
-    if _ASCII_LAYOUT is None or not all(map(str.isascii, strings)) or set(map(type, strings)) != {str}:
-        return None
-    return np.fromiter(map(id, strings), dtype=np.int64, count=len(strings))
+    return m
 
 
 def _utf8_offsets(strings: list[str]) -> tuple[bytes, np.ndarray]:
@@ -139,14 +115,16 @@ class NativeVocabulary:
         uniq = np.empty(max(n, 1), dtype=np.int32)
         chars = np.empty(max(n, 1), dtype=np.int32)
         nt = np.zeros(1, dtype=np.int64)
-        objs = _str_objects(sentences) if n else None
-        if objs is not None:
-            cap = sum(map(len, sentences)) // 2 + n + 1
+        ptrs, blen, prefix = (np.empty(max(n, 1), dtype=np.int64), np.empty(max(n, 1), dtype=np.int64),
+                              np.empty(n + 1, dtype=np.int64))
+        if n and type(sentences) is list and _pyhost().str_view(sentences, ptrs, blen, prefix):
+            # every sentence a compact ASCII str: read in place
+            cap = int(prefix[n]) // 2 + n + 1
             tokens = np.empty(cap, dtype=np.int32)
-            N.check(self._L.bimine_tokenize_strobjs(self._h, N.ptr(objs, N._i64p), n, _ASCII_LAYOUT[0],
-                                                    _ASCII_LAYOUT[1], N.ptr(tokens, N._i32p), cap,
-                                                    N.ptr(nt, N._i64p), N.ptr(lens, N._i32p), N.ptr(uniq, N._i32p),
-                                                    N.ptr(chars, N._i32p)))
+            N.check(self._L.bimine_tokenize_ptrs(self._h, ptrs.ctypes.data, N.ptr(blen, N._i64p), n,
+                                                 N.ptr(prefix, N._i64p), N.ptr(tokens, N._i32p), cap,
+                                                 N.ptr(nt, N._i64p), N.ptr(lens, N._i32p), N.ptr(uniq, N._i32p),
+                                                 N.ptr(chars, N._i32p)))
         else:
             data, off = _utf8_offsets(sentences)
             cap = len(data) // 2 + n + 1

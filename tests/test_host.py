@@ -208,6 +208,95 @@ def test_native_tokenizer_matches_python_rules():
     assert pos == tokens.shape[0]
 
 
+def test_native_tokenizer_in_place_list():
+    """bimine_tokenize_ptrs over the sentences' own str storage (_pyhost.str_view)
+    == text.tokenize, on a list large enough to be
+    split over threads, with words of 1-40 bytes (the 8/16-byte key
+    boundaries and the long-word path) and words ending at the last byte;
+    a list holding a non-ASCII str or a str subclass takes the UTF-8 path
+    with the same ids."""
+    import random
+
+    from paper_1512_01641_b200.packing import _pyhost
+
+    v = _native_vocab()
+    rng = random.Random(11)
+    letters = "abcdefghijklmnopqrstuvwxyzABCDEFGHIJKLMNOPQRSTUVWXYZ0123456789"
+    punct = ".,;:!?'\"()[]-_"
+    space = " \t\n\x0b\x0c\r\x1c\x1d\x1e\x1f"
+
+    def sentence():
+        parts = []
+        for _ in range(rng.randint(0, 30)):
+            w = "".join(rng.choice(letters) for _ in range(rng.choice([1, 2, 7, 8, 9, 15, 16, 17, 24, 40])))
+            if rng.random() < 0.2:
+                w = rng.choice(punct) + w + rng.choice(punct) * rng.randint(1, 3)
+            parts.append(w + "".join(rng.choice(space) for _ in range(rng.randint(1, 2))))
+        s = "".join(parts)
+        return s if rng.random() < 0.5 else s.rstrip()
+
+    sents = [sentence() for _ in range(20000)]
+    assert sum(map(len, sents)) > 2 << 20  # several thread ranges
+    n = len(sents)
+    ptrs, lens, prefix = np.empty(n, np.int64), np.empty(n, np.int64), np.empty(n + 1, np.int64)
+    assert _pyhost().str_view(sents, ptrs, lens, prefix)
+    assert prefix[n] == sum(map(len, sents)) and lens.tolist() == list(map(len, sents))
+
+    class S(str):
+        pass
+
+    def check(batch):
+        tokens, lens, uniq, chars = v.tokenize(batch)
+        pos = 0
+        for s, L, U, C in zip(batch, lens.tolist(), uniq.tolist(), chars.tolist()):
+            want = tokenize(s)
+            got = tokens[pos : pos + L].tolist()
+            pos += L
+            assert [v.get(w) for w in want] == got, repr(s)
+            assert U == len(set(want)) and C == len(s)
+        assert pos == tokens.shape[0]
+
+    check(sents)
+    for odd in ("na\u00efve x", S("subclass str")):
+        batch = sents[:3000] + [odd] + sents[3000:6000]
+        m = len(batch)
+        assert not _pyhost().str_view(batch, np.empty(m, np.int64), np.empty(m, np.int64), np.empty(m + 1, np.int64))
+        check(batch)
+
+
+def test_build_rows_matches_python():
+    """_pyhost.build_rows (csrc/pyhost.c) == the rows built in Python
+    (align.py:441-447: (score, source sentence, target sentence) per match,
+    pair by pair), the same str objects; bad inputs raise."""
+    from paper_1512_01641_b200 import _native as N
+    from paper_1512_01641_b200.packing import _pyhost
+
+    _native_vocab()  # builds _pyhost too
+    rng = np.random.default_rng(3)
+    sents = [f"sentence {k}" for k in range(500)]
+    K = 40
+    n_src = rng.integers(1, 6, K)
+    n_tgt = rng.integers(1, 6, K)
+    start = np.concatenate([[0], np.cumsum(n_src + n_tgt)[:-1]]).astype(np.int64)
+    counts = np.minimum(n_src, n_tgt) - rng.integers(0, 2, K).clip(0, None)
+    counts = counts.clip(0, None).astype(np.int64)
+    m = np.empty(int(counts.sum()), dtype=N.MATCH_DTYPE)
+    want, r = [], 0
+    for k in range(K):
+        for c in range(counts[k]):
+            i, j = rng.integers(0, n_src[k]), rng.integers(0, n_tgt[k])
+            m[r] = (rng.random(), i, j)
+            want.append((float(m[r]["score"]), sents[start[k] + i], sents[start[k] + n_src[k] + j]))
+            r += 1
+    got = _pyhost().build_rows(m, counts, start, start + n_src, sents)
+    assert got == want and all(g[1] is w[1] and g[2] is w[2] for g, w in zip(got, want))
+    assert _pyhost().build_rows(m[:0], np.zeros(K, np.int64), start, start + n_src, sents) == []
+    with pytest.raises(ValueError):  # counts do not cover the matches
+        _pyhost().build_rows(m, counts + 1, start, start + n_src, sents)
+    with pytest.raises(IndexError):  # a sentence index past the list
+        _pyhost().build_rows(m, counts, start + 10_000, start + n_src, sents)
+
+
 def test_utf8_offsets_edge_cases():
     """The UTF-8 packing behind bimine_tokenize_batch: bytes back to back and
     byte offsets, for ASCII, non-ASCII, empty strings, NULs and lone

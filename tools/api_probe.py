@@ -31,12 +31,18 @@ def main():
     A.mine_corpus(model, lex, pairs[:64], A.MiningConfig())
     for ch in chunks:
         A.CHUNK_PAIRS = ch
-        best = 1e9
+        best, st = 1e9, None
         for _ in range(3):
+            A.STAGE_TIMES = {}
             t = time.perf_counter()
             out = A.mine_corpus(model, lex, pairs, A.MiningConfig())
-            best = min(best, time.perf_counter() - t)
-        print(f"chunk {ch}: {best:.3f} s = {n / best:.0f} pairs/s, {len(out.rows)} rows", flush=True)
+            w = time.perf_counter() - t
+            if w < best:
+                best, st = w, A.STAGE_TIMES
+        A.STAGE_TIMES = None
+        stages = " ".join(f"{k} {v * 1e3:.1f}" for k, v in st.items())
+        print(f"chunk {ch}: {best:.3f} s = {n / best:.0f} pairs/s, {len(out.rows)} rows; stages ms: {stages}",
+              flush=True)
 
 
 if __name__ == "__main__":
