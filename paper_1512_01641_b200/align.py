@@ -245,7 +245,7 @@ def _shard_bounds(weights: np.ndarray, parts: int) -> list[tuple[int, int]]:
     return [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
 
 
-CHUNK_PAIRS = 16_384  # pairs tokenised / mined per chunk of mine_corpus
+CHUNK_PAIRS = 5_000  # pairs tokenised / mined per chunk of mine_corpus (the next chunk packs while one mines)
 # stage timer of mine_corpus (bench.py's api_e2e): None, or a dict that
 # accumulates seconds per stage -- "pack" (tokenise + pack), "mine"
 # (bimine_mine_host), "rows" (result tuples)
@@ -298,10 +298,8 @@ def _mine_chunk(model, lexicon, pd, config: MiningConfig, device: int, topic_ids
     t0 = time.perf_counter()
     from .packing import _pyhost
 
-    first = pd.start[keep]
     rows = _pyhost().build_rows(np.ascontiguousarray(matches), np.ascontiguousarray(counts, dtype=np.int64),
-                                np.ascontiguousarray(first, dtype=np.int64),
-                                np.ascontiguousarray(first + pd.n_src[keep], dtype=np.int64), pd.sentences)
+                                keep.astype(np.int64), pd.docs)
     _stage("rows", t0)
     return rows, failed
 

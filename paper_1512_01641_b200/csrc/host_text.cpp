@@ -32,6 +32,7 @@
 #include <chrono>
 #include <cstdio>
 #include <thread>
+#include <mutex>
 #include <new>
 #include <utility>
 #include <vector>
@@ -173,9 +174,36 @@ int host_threads() {
   return n;
 }
 
+// Phase 1 state of one thread: its sentences [k0, k1).
+struct TokRange {
+  int64_t k0 = 0, k1 = 0;
+  std::vector<int32_t> tok;  // id, or -(index into miss) - 1
+  struct Miss {
+    uint64_t hash;
+    uint32_t off, len;  // in `words`
+  };
+  std::vector<Miss> miss;
+  std::vector<char> words;  // lowercased missing words, zero-padded like tokenize_range's
+  std::vector<int32_t> resolved;
+  int64_t out_off = 0;
+  void reset(int64_t a, int64_t b) {  // (buffers keep their capacity from call to call)
+    k0 = a;
+    k1 = b;
+    tok.clear();
+    miss.clear();
+    words.clear();
+    resolved.clear();
+    out_off = 0;
+  }
+};
+
 }  // namespace
 
 struct bimine_vocab {
+  // the batch tokenizer's per-thread state, kept between calls (no fresh
+  // pages to fault in per call); one tokenisation at a time per vocabulary
+  std::mutex tok_mu;
+  std::vector<TokRange> tok_ranges;
   struct Slot {
     uint64_t hash;
     int32_t id;  // -1: empty
@@ -282,20 +310,6 @@ struct bimine_vocab {
 };
 
 namespace {
-
-// Phase 1 state of one thread: its sentences [k0, k1).
-struct TokRange {
-  int64_t k0 = 0, k1 = 0;
-  std::vector<int32_t> tok;  // id, or -(index into miss) - 1
-  struct Miss {
-    uint64_t hash;
-    uint32_t off, len;  // in `words`
-  };
-  std::vector<Miss> miss;
-  std::vector<char> words;  // lowercased missing words, zero-padded like tokenize_range's
-  std::vector<int32_t> resolved;
-  int64_t out_off = 0;
-};
 
 // Per sentence, two passes: split + lowercase + hash every token and
 // prefetch its home slot, then resolve them (the table is far larger than
@@ -541,21 +555,23 @@ int tokenize_sentences(bimine_vocab *v, const Sent &sent, int64_t n, Prefix pref
   if (n <= 0) return BIMINE_OK;
   const int64_t bytes = prefix_bytes(n);
   const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(host_threads(), bytes >> 18));
-  std::vector<TokRange> R(nt);
+  std::lock_guard<std::mutex> lk(v->tok_mu);
+  std::vector<TokRange> &R = v->tok_ranges;
+  if ((int)R.size() < nt) R.resize(nt);
   for (int t = 0; t < nt; ++t) {
-    R[t].k0 = t == 0 ? 0 : R[t - 1].k1;
-    if (t == nt - 1) {
-      R[t].k1 = n;
-    } else {  // first sentence whose byte prefix reaches the thread's share
-      int64_t lo = R[t].k0, hi = n;
+    const int64_t k0 = t == 0 ? 0 : R[t - 1].k1;
+    int64_t k1 = n;
+    if (t < nt - 1) {  // first sentence whose byte prefix reaches the thread's share
+      int64_t lo = k0, hi = n;
       const int64_t want = bytes * (t + 1) / nt;
       while (lo < hi) {
         const int64_t mid = (lo + hi) / 2;
         if (prefix_bytes(mid) < want) lo = mid + 1;
         else hi = mid;
       }
-      R[t].k1 = lo;
+      k1 = lo;
     }
+    R[t].reset(k0, k1);
   }
   auto parallel = [&](auto &&fn) {
     if (nt == 1) return fn(R[0]);
@@ -573,12 +589,13 @@ int tokenize_sentences(bimine_vocab *v, const Sent &sent, int64_t n, Prefix pref
   const double c1 = clk();
 #endif
   int64_t total = 0;
-  for (TokRange &r : R) {
-    r.out_off = total;
-    total += (int64_t)r.tok.size();
+  for (int t = 0; t < nt; ++t) {
+    R[t].out_off = total;
+    total += (int64_t)R[t].tok.size();
   }
   if (total > cap) return BIMINE_E_LIMIT;  // vocabulary unchanged
-  for (TokRange &r : R) {  // serial: first-occurrence id order
+  for (int t = 0; t < nt; ++t) {  // serial: first-occurrence id order
+    TokRange &r = R[t];
     r.resolved.resize(r.miss.size());
     for (size_t i = 0; i < r.miss.size(); ++i)
       r.resolved[i] = v->get(r.miss[i].hash, r.words.data() + r.miss[i].off, r.miss[i].len);

@@ -11,17 +11,35 @@
  *       caller then encodes the sentences to one UTF-8 buffer instead.  The
  *       caller keeps the list alive while the pointers are used.
  *
- *   build_rows(matches, counts, src_first, tgt_first, sentences) -> list
+ *   docs_view(docs, ptrs, lens, prefix) -> bool
+ *       The same over a list of document pairs (source sentences, target
+ *       sentences), each a tuple or list, each side a tuple or list of str:
+ *       pair by pair, source then target sentences -- no flat list of
+ *       10^6 sentences to build and free.  False also for any other shape.
+ *
+ *   build_rows(matches, counts, pair, docs) -> list
  *       The mining rows (score, source sentence, target sentence) of
- *       align.py:441-447, in pair order: pair k owns the next counts[k]
- *       records of `matches` (bimine_match: f64 score, i32 i, i32 j), whose
- *       sentences are sentences[src_first[k] + i] and
- *       sentences[tgt_first[k] + j].
+ *       align.py:441-447, in pair order: the k-th mined pair, docs[pair[k]],
+ *       owns the next counts[k] records of `matches` (bimine_match: f64
+ *       score, i32 i, i32 j): source sentence i, target sentence j.
  */
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
 #include <stdint.h>
 #include <string.h>
+
+/* items of an exact tuple or list (borrowed), else NULL */
+static PyObject **seq_items(PyObject *o, Py_ssize_t *n) {
+  if (PyTuple_CheckExact(o)) {
+    *n = PyTuple_GET_SIZE(o);
+    return &PyTuple_GET_ITEM(o, 0);
+  }
+  if (PyList_CheckExact(o)) {
+    *n = PyList_GET_SIZE(o);
+    return ((PyListObject *)o)->ob_item;
+  }
+  return NULL;
+}
 
 static int get_buf(PyObject *o, Py_buffer *b, int writable, Py_ssize_t itemsize, const char *name) {
   if (PyObject_GetBuffer(o, b, (writable ? PyBUF_WRITABLE : 0) | PyBUF_C_CONTIGUOUS) < 0) return -1;
@@ -74,20 +92,71 @@ static PyObject *str_view(PyObject *self, PyObject *args) {
   return PyBool_FromLong(ok);
 }
 
+static PyObject *docs_view(PyObject *self, PyObject *args) {
+  PyObject *docs, *po, *lo, *xo;
+  if (!PyArg_ParseTuple(args, "O!OOO", &PyList_Type, &docs, &po, &lo, &xo)) return NULL;
+  Py_buffer bp, bl, bx;
+  if (get_buf(po, &bp, 1, 8, "ptrs") < 0) return NULL;
+  if (get_buf(lo, &bl, 1, 8, "lens") < 0) {
+    PyBuffer_Release(&bp);
+    return NULL;
+  }
+  if (get_buf(xo, &bx, 1, 8, "prefix") < 0) {
+    PyBuffer_Release(&bp);
+    PyBuffer_Release(&bl);
+    return NULL;
+  }
+  const Py_ssize_t cap = bp.len / 8 < bl.len / 8 ? bp.len / 8 : bl.len / 8;
+  int64_t *P = (int64_t *)bp.buf, *L = (int64_t *)bl.buf, *X = (int64_t *)bx.buf;
+  Py_ssize_t s = 0;
+  int ok = bx.len >= 8;
+  if (ok) X[0] = 0;
+  const Py_ssize_t nd = PyList_GET_SIZE(docs);
+  for (Py_ssize_t d = 0; ok && d < nd; ++d) {
+    Py_ssize_t two;
+    PyObject **side = seq_items(PyList_GET_ITEM(docs, d), &two);
+    if (!side || two != 2) {
+      ok = 0;
+      break;
+    }
+    for (int h = 0; ok && h < 2; ++h) {
+      Py_ssize_t m;
+      PyObject **it = seq_items(side[h], &m);
+      if (!it) {
+        ok = 0;
+        break;
+      }
+      for (Py_ssize_t k = 0; k < m; ++k, ++s) {
+        PyObject *o = it[k];
+        if (s >= cap || 8 * (s + 2) > bx.len || !PyUnicode_CheckExact(o) || !PyUnicode_IS_COMPACT_ASCII(o)) {
+          ok = 0;
+          break;
+        }
+        P[s] = (int64_t)(intptr_t)PyUnicode_DATA(o);
+        L[s] = (int64_t)PyUnicode_GET_LENGTH(o);
+        X[s + 1] = X[s] + L[s];
+      }
+    }
+  }
+  PyBuffer_Release(&bp);
+  PyBuffer_Release(&bl);
+  PyBuffer_Release(&bx);
+  return PyBool_FromLong(ok);
+}
+
 static PyObject *build_rows(PyObject *self, PyObject *args) {
-  PyObject *mo, *co, *so, *to, *list;
-  if (!PyArg_ParseTuple(args, "OOOOO!", &mo, &co, &so, &to, &PyList_Type, &list)) return NULL;
-  Py_buffer bm, bc, bs, bt;
+  PyObject *mo, *co, *qo, *docs;
+  if (!PyArg_ParseTuple(args, "OOOO!", &mo, &co, &qo, &PyList_Type, &docs)) return NULL;
+  Py_buffer bm, bc, bq;
   if (get_buf(mo, &bm, 0, 16, "matches") < 0) return NULL;
   if (get_buf(co, &bc, 0, 8, "counts") < 0) goto fail_m;
-  if (get_buf(so, &bs, 0, 8, "src_first") < 0) goto fail_c;
-  if (get_buf(to, &bt, 0, 8, "tgt_first") < 0) goto fail_s;
+  if (get_buf(qo, &bq, 0, 8, "pair") < 0) goto fail_c;
   {
-    const Py_ssize_t K = bc.len / 8, total = bm.len / 16, ns = PyList_GET_SIZE(list);
-    const int64_t *cnt = (const int64_t *)bc.buf, *sf = (const int64_t *)bs.buf, *tf = (const int64_t *)bt.buf;
+    const Py_ssize_t K = bc.len / 8, total = bm.len / 16, nd = PyList_GET_SIZE(docs);
+    const int64_t *cnt = (const int64_t *)bc.buf, *pq = (const int64_t *)bq.buf;
     const char *m = (const char *)bm.buf;
-    if (bs.len / 8 != K || bt.len / 8 != K) {
-      PyErr_SetString(PyExc_ValueError, "build_rows: counts, src_first and tgt_first differ in length");
+    if (bq.len / 8 != K) {
+      PyErr_SetString(PyExc_ValueError, "build_rows: counts and pair differ in length");
       goto fail_all;
     }
     int64_t sum = 0;
@@ -106,16 +175,24 @@ static PyObject *build_rows(PyObject *self, PyObject *args) {
     if (!out) goto fail_all;
     Py_ssize_t r = 0;
     for (Py_ssize_t k = 0; k < K; ++k) {
+      if (!cnt[k]) continue;
+      Py_ssize_t two = 0, ns = 0, nt = 0;
+      PyObject **side = pq[k] >= 0 && pq[k] < nd ? seq_items(PyList_GET_ITEM(docs, pq[k]), &two) : NULL;
+      PyObject **src = side && two == 2 ? seq_items(side[0], &ns) : NULL;
+      PyObject **tgt = side && two == 2 ? seq_items(side[1], &nt) : NULL;
+      if (!src || !tgt) {
+        PyErr_Format(PyExc_TypeError, "build_rows: docs[%lld] is not a (sentences, sentences) pair", (long long)pq[k]);
+        Py_DECREF(out);
+        goto fail_all;
+      }
       for (int64_t c = 0; c < cnt[k]; ++c, ++r) {
         double score;
         int32_t i, j;
         memcpy(&score, m + 16 * r, 8);
         memcpy(&i, m + 16 * r + 8, 4);
         memcpy(&j, m + 16 * r + 12, 4);
-        const int64_t si = sf[k] + i, ti = tf[k] + j;
-        if (i < 0 || j < 0 || si >= ns || ti >= ns) {
-          PyErr_Format(PyExc_IndexError, "build_rows: match %zd refers to sentence %lld / %lld of %zd", r,
-                       (long long)si, (long long)ti, ns);
+        if (i < 0 || j < 0 || i >= ns || j >= nt) {
+          PyErr_Format(PyExc_IndexError, "build_rows: match %zd = (%d, %d) outside a %zd x %zd pair", r, i, j, ns, nt);
           Py_DECREF(out);
           goto fail_all;
         }
@@ -126,25 +203,26 @@ static PyObject *build_rows(PyObject *self, PyObject *args) {
           Py_DECREF(out);
           goto fail_all;
         }
-        PyObject *a = PyList_GET_ITEM(list, si), *b = PyList_GET_ITEM(list, ti);
+        PyObject *a = src[i], *b = tgt[j];
         Py_INCREF(a);
         Py_INCREF(b);
         PyTuple_SET_ITEM(t, 0, f);
         PyTuple_SET_ITEM(t, 1, a);
         PyTuple_SET_ITEM(t, 2, b);
+        /* a float and two str: no cycle possible, so the collector need
+           not scan it (CPython untracks such tuples itself, but only when
+           a collection gets to them: ~10^5 rows made a 20 ms gen-0 pass) */
+        PyObject_GC_UnTrack(t);
         PyList_SET_ITEM(out, r, t);
       }
     }
     PyBuffer_Release(&bm);
     PyBuffer_Release(&bc);
-    PyBuffer_Release(&bs);
-    PyBuffer_Release(&bt);
+    PyBuffer_Release(&bq);
     return out;
   }
 fail_all:
-  PyBuffer_Release(&bt);
-fail_s:
-  PyBuffer_Release(&bs);
+  PyBuffer_Release(&bq);
 fail_c:
   PyBuffer_Release(&bc);
 fail_m:
@@ -154,6 +232,7 @@ fail_m:
 
 static PyMethodDef methods[] = {
     {"str_view", str_view, METH_VARARGS, "in-place character pointers of a list of compact ASCII str"},
+    {"docs_view", docs_view, METH_VARARGS, "in-place character pointers of document pairs' sentences"},
     {"build_rows", build_rows, METH_VARARGS, "(score, source, target) rows of compacted matches"},
     {NULL, NULL, 0, NULL}};
 

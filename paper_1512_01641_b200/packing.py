@@ -46,6 +46,22 @@ class Vocabulary:
         return np.fromiter((self.get(w) for w in words), dtype=np.int32)
 
 
+def _token_buffer(n: int) -> np.ndarray:
+    """int32 output of the tokenizer: page-locked when a GPU is present
+    (torch's caching host allocator: the block is reused call after call
+    instead of faulting in and unmapping ~10^8 fresh bytes, and the batch
+    then uploads without staging), else plain memory."""
+    if n >= (1 << 20):
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                return torch.empty(4 * n, dtype=torch.uint8, pin_memory=True).numpy().view(np.int32)
+        except Exception:  # pragma: no cover - no usable CUDA runtime
+            pass
+    return np.empty(n, dtype=np.int32)
+
+
 def _pyhost():
     """The CPython helper module (csrc/pyhost.c), built with the library."""
     from . import _pyhost as m
@@ -104,6 +120,38 @@ class NativeVocabulary:
     def get(self, word: str) -> int:
         return int(self.add_many([word])[0])
 
+    def _in_place(self, n: int, ptrs, blen, prefix):
+        """bimine_tokenize_ptrs over n sentences' own storage."""
+        N = self._N
+        lens = np.empty(max(n, 1), dtype=np.int32)
+        uniq = np.empty(max(n, 1), dtype=np.int32)
+        chars = np.empty(max(n, 1), dtype=np.int32)
+        nt = np.zeros(1, dtype=np.int64)
+        # first try room for one token per 5 characters (natural text has
+        # 5-7); denser text is refused with the vocabulary unchanged and
+        # tokenised again with the worst-case bound
+        for cap in (int(prefix[n]) // 5 + n + 1, int(prefix[n]) // 2 + n + 1):
+            tokens = _token_buffer(cap)
+            rc = self._L.bimine_tokenize_ptrs(self._h, ptrs.ctypes.data, N.ptr(blen, N._i64p), n,
+                                              N.ptr(prefix, N._i64p), N.ptr(tokens, N._i32p), cap, N.ptr(nt, N._i64p),
+                                              N.ptr(lens, N._i32p), N.ptr(uniq, N._i32p), N.ptr(chars, N._i32p))
+            if rc != N.BIMINE_E_LIMIT:
+                break
+        N.check(rc)
+        return tokens[: int(nt[0])], lens[:n], uniq[:n], chars[:n]
+
+    def tokenize_docs(self, docs, n: int):
+        """tokenize() of the n sentences of `docs`, a list of (source
+        sentences, target sentences), pair by pair, source first -- read in
+        place, without a flat list; None unless every pair is a tuple or
+        list of two tuples or lists of compact ASCII str (the caller then
+        flattens them for tokenize())."""
+        ptrs, blen, prefix = (np.empty(max(n, 1), dtype=np.int64), np.empty(max(n, 1), dtype=np.int64),
+                              np.empty(n + 1, dtype=np.int64))
+        if not (n and type(docs) is list and _pyhost().docs_view(docs, ptrs, blen, prefix)):
+            return None
+        return self._in_place(n, ptrs, blen, prefix)
+
     def tokenize(self, sentences: list[str]):
         """(tokens int32, len, uniq, chars) per sentence with the reference's
         tokenize(); a sentence with no token has len 0.  ASCII sentences are
@@ -111,27 +159,20 @@ class NativeVocabulary:
         buffer."""
         N = self._N
         n = len(sentences)
+        ptrs, blen, prefix = (np.empty(max(n, 1), dtype=np.int64), np.empty(max(n, 1), dtype=np.int64),
+                              np.empty(n + 1, dtype=np.int64))
+        if n and type(sentences) is list and _pyhost().str_view(sentences, ptrs, blen, prefix):
+            return self._in_place(n, ptrs, blen, prefix)  # every sentence a compact ASCII str
         lens = np.empty(max(n, 1), dtype=np.int32)
         uniq = np.empty(max(n, 1), dtype=np.int32)
         chars = np.empty(max(n, 1), dtype=np.int32)
         nt = np.zeros(1, dtype=np.int64)
-        ptrs, blen, prefix = (np.empty(max(n, 1), dtype=np.int64), np.empty(max(n, 1), dtype=np.int64),
-                              np.empty(n + 1, dtype=np.int64))
-        if n and type(sentences) is list and _pyhost().str_view(sentences, ptrs, blen, prefix):
-            # every sentence a compact ASCII str: read in place
-            cap = int(prefix[n]) // 2 + n + 1
-            tokens = np.empty(cap, dtype=np.int32)
-            N.check(self._L.bimine_tokenize_ptrs(self._h, ptrs.ctypes.data, N.ptr(blen, N._i64p), n,
-                                                 N.ptr(prefix, N._i64p), N.ptr(tokens, N._i32p), cap,
-                                                 N.ptr(nt, N._i64p), N.ptr(lens, N._i32p), N.ptr(uniq, N._i32p),
-                                                 N.ptr(chars, N._i32p)))
-        else:
-            data, off = _utf8_offsets(sentences)
-            cap = len(data) // 2 + n + 1
-            tokens = np.empty(cap, dtype=np.int32)
-            N.check(self._L.bimine_tokenize_batch(self._h, data, N.ptr(off, N._i64p), n, N.ptr(tokens, N._i32p),
-                                                  cap, N.ptr(nt, N._i64p), N.ptr(lens, N._i32p),
-                                                  N.ptr(uniq, N._i32p), N.ptr(chars, N._i32p)))
+        data, off = _utf8_offsets(sentences)
+        cap = len(data) // 2 + n + 1
+        tokens = np.empty(cap, dtype=np.int32)
+        N.check(self._L.bimine_tokenize_batch(self._h, data, N.ptr(off, N._i64p), n, N.ptr(tokens, N._i32p), cap,
+                                              N.ptr(nt, N._i64p), N.ptr(lens, N._i32p), N.ptr(uniq, N._i32p),
+                                              N.ptr(chars, N._i32p)))
         tokens, lens, uniq, chars = tokens[: int(nt[0])], lens[:n], uniq[:n], chars[:n]
         slow = np.flatnonzero(lens < 0)
         if slow.size:  # code points >= U+0180 (or U+0130): Python's Unicode rules, same vocabulary
@@ -325,8 +366,8 @@ class PackedDocuments:
     the bookkeeping to map matches back to sentence text."""
 
     batch: PackedBatch | None  # None when no pair tokenises
-    sentences: list  # every input sentence, pair by pair: its source then its target sentences
-    start: np.ndarray  # [P + 1] first sentence of input pair k in `sentences`
+    docs: list  # the input pairs: (source sentences, target sentences)
+    start: np.ndarray  # [P + 1] first sentence of input pair k, counting source then target sentences pair by pair
     n_src: np.ndarray  # [P] source sentence count per input pair
     ok: np.ndarray  # [P] bool: input pair k is in the batch
     errors: dict  # input pair -> the reference's ValueError message
@@ -334,28 +375,35 @@ class PackedDocuments:
 
 def pack_documents(vocab, pairs) -> PackedDocuments:
     """Tokenise and pack many (source_sentences, target_sentences) at once
-    (one native tokenizer call; a pair whose sentence does not tokenise is
-    left out with the message the reference raises for it, align.py:109-119)."""
+    (one native tokenizer call over the sentences' own storage; a pair whose
+    sentence does not tokenise is left out with the message the reference
+    raises for it, align.py:109-119)."""
     import itertools
 
+    pairs = pairs if type(pairs) is list else list(pairs)
     P = len(pairs)
     ns = np.fromiter((len(x[0]) for x in pairs), dtype=np.int64, count=P)
     nt = np.fromiter((len(x[1]) for x in pairs), dtype=np.int64, count=P)
-    flat = list(itertools.chain.from_iterable(itertools.chain(x[0], x[1]) for x in pairs))
     start = np.zeros(P + 1, dtype=np.int64)
     np.cumsum(ns + nt, out=start[1:])
-    if getattr(vocab, "native", False):
-        tokens, lens, uniq, chars = vocab.tokenize(flat)
-    else:  # the dict vocabulary: the Python rules sentence by sentence
-        ids = []
-        for sent in flat:
-            ids.append(np.asarray([vocab.get(t) for t in tokenize(sent)], dtype=np.int32))
-        lens = np.fromiter(map(len, ids), dtype=np.int32, count=len(ids))
-        uniq = np.fromiter((len(set(x.tolist())) for x in ids), dtype=np.int32, count=len(ids))
-        chars = np.fromiter(map(len, flat), dtype=np.int32, count=len(flat))
-        tokens = np.concatenate(ids) if ids else np.zeros(0, np.int32)
-    lens = lens[: len(flat)]
-    zero = np.zeros(len(flat) + 1, dtype=np.int64)
+    S = int(start[P])
+    res = vocab.tokenize_docs(pairs, S) if getattr(vocab, "native", False) else None
+    if res is not None:
+        tokens, lens, uniq, chars = res
+    else:
+        flat = list(itertools.chain.from_iterable(itertools.chain(x[0], x[1]) for x in pairs))
+        if getattr(vocab, "native", False):
+            tokens, lens, uniq, chars = vocab.tokenize(flat)
+        else:  # the dict vocabulary: the Python rules sentence by sentence
+            ids = []
+            for sent in flat:
+                ids.append(np.asarray([vocab.get(t) for t in tokenize(sent)], dtype=np.int32))
+            lens = np.fromiter(map(len, ids), dtype=np.int32, count=len(ids))
+            uniq = np.fromiter((len(set(x.tolist())) for x in ids), dtype=np.int32, count=len(ids))
+            chars = np.fromiter(map(len, flat), dtype=np.int32, count=len(flat))
+            tokens = np.concatenate(ids) if ids else np.zeros(0, np.int32)
+    lens = lens[:S]
+    zero = np.zeros(S + 1, dtype=np.int64)
     np.cumsum(lens == 0, out=zero[1:])
     ok = (ns > 0) & (nt > 0) & (zero[start[1:]] == zero[start[:-1]])
     errors = {}
@@ -363,24 +411,25 @@ def pack_documents(vocab, pairs) -> PackedDocuments:
         if not ns[k] or not nt[k]:
             errors[k] = "both sentence sequences must be non-empty"
             continue
-        bad = int(start[k]) + int(np.flatnonzero(lens[start[k]: start[k + 1]] == 0)[0])
-        side, index = ("source", bad - start[k]) if bad - start[k] < ns[k] else ("target", bad - start[k] - ns[k])
-        errors[k] = f"{side} sentence {index}: untokenizable sentence: {flat[bad]!r}"
+        bad = int(np.flatnonzero(lens[start[k]: start[k + 1]] == 0)[0])
+        side, index = ("source", bad) if bad < ns[k] else ("target", bad - int(ns[k]))
+        text = pairs[k][0 if side == "source" else 1][index]
+        errors[k] = f"{side} sentence {index}: untokenizable sentence: {text!r}"
     keep = np.flatnonzero(ok)
     batch = None
     if keep.size:
         if keep.size == P:
-            tok, sl, su, sc = tokens, lens, uniq[: len(flat)], chars[: len(flat)]
+            tok, sl, su, sc = tokens, lens, uniq[:S], chars[:S]
             first = start[:-1]
         else:
             sent_keep = np.repeat(ok, ns + nt)
             tok = tokens[np.repeat(sent_keep, lens)]
-            sl, su, sc = lens[sent_keep], uniq[: len(flat)][sent_keep], chars[: len(flat)][sent_keep]
+            sl, su, sc = lens[sent_keep], uniq[:S][sent_keep], chars[:S][sent_keep]
             first = np.zeros(keep.size, dtype=np.int64)
             np.cumsum((ns + nt)[keep][:-1], out=first[1:])
         batch = PackedBatch.from_token_lengths(tok, sl, sc, first, ns[keep], first + ns[keep], nt[keep],
                                                sent_uniq=su)
-    return PackedDocuments(batch=batch, sentences=flat, start=start, n_src=ns, ok=ok, errors=errors)
+    return PackedDocuments(batch=batch, docs=pairs, start=start, n_src=ns, ok=ok, errors=errors)
 
 
 class BatchBuilder:

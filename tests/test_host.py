@@ -257,6 +257,7 @@ def test_native_tokenizer_in_place_list():
         assert pos == tokens.shape[0]
 
     check(sents)
+    check(["a b c d e f g"] * 3000 + ["x"])  # denser than one token per 5 characters: the retry
     for odd in ("na\u00efve x", S("subclass str")):
         batch = sents[:3000] + [odd] + sents[3000:6000]
         m = len(batch)
@@ -273,28 +274,47 @@ def test_build_rows_matches_python():
 
     _native_vocab()  # builds _pyhost too
     rng = np.random.default_rng(3)
-    sents = [f"sentence {k}" for k in range(500)]
     K = 40
-    n_src = rng.integers(1, 6, K)
-    n_tgt = rng.integers(1, 6, K)
-    start = np.concatenate([[0], np.cumsum(n_src + n_tgt)[:-1]]).astype(np.int64)
-    counts = np.minimum(n_src, n_tgt) - rng.integers(0, 2, K).clip(0, None)
-    counts = counts.clip(0, None).astype(np.int64)
+    docs = [(tuple(f"s{k}.{i}" for i in range(rng.integers(1, 6))), [f"t{k}.{j}" for j in range(rng.integers(1, 6))])
+            for k in range(K)]
+    pair = np.sort(rng.choice(K, 30, replace=False)).astype(np.int64)
+    counts = np.array([rng.integers(0, min(len(docs[k][0]), len(docs[k][1])) + 1) for k in pair], np.int64)
     m = np.empty(int(counts.sum()), dtype=N.MATCH_DTYPE)
     want, r = [], 0
-    for k in range(K):
-        for c in range(counts[k]):
-            i, j = rng.integers(0, n_src[k]), rng.integers(0, n_tgt[k])
+    for k, c in zip(pair.tolist(), counts.tolist()):
+        for _ in range(c):
+            i, j = rng.integers(0, len(docs[k][0])), rng.integers(0, len(docs[k][1]))
             m[r] = (rng.random(), i, j)
-            want.append((float(m[r]["score"]), sents[start[k] + i], sents[start[k] + n_src[k] + j]))
+            want.append((float(m[r]["score"]), docs[k][0][i], docs[k][1][j]))
             r += 1
-    got = _pyhost().build_rows(m, counts, start, start + n_src, sents)
+    got = _pyhost().build_rows(m, counts, pair, docs)
     assert got == want and all(g[1] is w[1] and g[2] is w[2] for g, w in zip(got, want))
-    assert _pyhost().build_rows(m[:0], np.zeros(K, np.int64), start, start + n_src, sents) == []
+    assert _pyhost().build_rows(m[:0], np.zeros(30, np.int64), pair, docs) == []
     with pytest.raises(ValueError):  # counts do not cover the matches
-        _pyhost().build_rows(m, counts + 1, start, start + n_src, sents)
-    with pytest.raises(IndexError):  # a sentence index past the list
-        _pyhost().build_rows(m, counts, start + 10_000, start + n_src, sents)
+        _pyhost().build_rows(m, counts + 1, pair, docs)
+    bad = m.copy()
+    bad["i"] += 10
+    with pytest.raises(IndexError):  # a sentence index past the pair
+        _pyhost().build_rows(bad, counts, pair, docs)
+    with pytest.raises(TypeError):  # a pair index past the list
+        _pyhost().build_rows(m, counts, pair + K, docs)
+
+
+def test_docs_view_matches_flat_view():
+    """_pyhost.docs_view over (source, target) pairs == str_view over the
+    flattened sentences; any other shape or a non-ASCII str -> False."""
+    from paper_1512_01641_b200.packing import _pyhost
+
+    _native_vocab()
+    docs = [(("a b", "c"), ["dd", "e f g"]), (["h"], ("i", "j", "k"))]
+    flat = [s for d in docs for side in d for s in side]
+    n = len(flat)
+    out = [np.empty(n, np.int64), np.empty(n, np.int64), np.empty(n + 1, np.int64)]
+    ref = [np.empty(n, np.int64), np.empty(n, np.int64), np.empty(n + 1, np.int64)]
+    assert _pyhost().docs_view(docs, *out) and _pyhost().str_view(flat, *ref)
+    assert all((a == b).all() for a, b in zip(out, ref))
+    for odd in ([(("a",), ("\u00e9",))], [(("a",),)], [("a", "b")], [(("a",), ("b",), ("c",))]):
+        assert not _pyhost().docs_view(odd, np.empty(4, np.int64), np.empty(4, np.int64), np.empty(5, np.int64))
 
 
 def test_utf8_offsets_edge_cases():

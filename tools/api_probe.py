@@ -2,6 +2,7 @@
 for several chunk sizes (align.CHUNK_PAIRS).
 
     python tools/api_probe.py [n_pairs] [chunk ...]
+    API_PROFILE=1 python tools/api_probe.py ...   # + cProfile of one call
 """
 import os
 import sys
@@ -43,6 +44,15 @@ def main():
         stages = " ".join(f"{k} {v * 1e3:.1f}" for k, v in st.items())
         print(f"chunk {ch}: {best:.3f} s = {n / best:.0f} pairs/s, {len(out.rows)} rows; stages ms: {stages}",
               flush=True)
+    if os.environ.get("API_PROFILE"):
+        import cProfile
+        import pstats
+
+        pr = cProfile.Profile()
+        pr.enable()
+        A.mine_corpus(model, lex, pairs, A.MiningConfig())
+        pr.disable()
+        pstats.Stats(pr).sort_stats("tottime").print_stats(18)
 
 
 if __name__ == "__main__":
