@@ -18,6 +18,14 @@
 // plus the |x| in [512, 1024) special case (scale*tmp then + scale, no
 // FMA there) and the tiny / huge / non-finite branches.  Compiles for the
 // host too (std::fma), so CPU tests can check it against libm directly.
+//
+// Attribution: the algorithm, its constants and its operation order are
+// those of the GNU C Library's exp (sysdeps/ieee754/dbl-64/e_exp.c,
+// e_exp_data.c, math_config.h; Copyright (C) 2018-2024 Free Software
+// Foundation, Inc., originally contributed by Szabolcs Nagy / Arm Ltd.),
+// licensed under the GNU Lesser General Public License v2.1 or later.
+// Reproducing that exact operation order is what makes the device result
+// bit-identical to the reference's math.exp.
 #pragma once
 
 #include <stdint.h>
