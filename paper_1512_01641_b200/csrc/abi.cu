@@ -1519,6 +1519,13 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   return BIMINE_OK;
 }
 
+#ifdef BIMINE_PROF_GLOBAL
+// profiling builds only: the band end times of the last nw_big_kernel launch
+extern "C" int bimine_debug_band_times(uint64_t *out, int n) {
+  return cudaMemcpyFromSymbol(out, g_prof_band, sizeof(uint64_t) * std::min(n, 4096)) == cudaSuccess ? 0 : -2;
+}
+#endif
+
 // ------------------------------------------------------------------------
 // test hook: the device exp
 // ------------------------------------------------------------------------

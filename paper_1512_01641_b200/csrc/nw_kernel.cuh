@@ -696,7 +696,10 @@ namespace bimine {
 #define BIMINE_BIG_W 8
 #endif
 constexpr int kBigW = BIMINE_BIG_W;  // warps per CTA of the band pipeline (one per SM sub-partition)
-constexpr int kRing = 128;  // boundary values buffered per ring
+#ifndef BIMINE_RING
+#define BIMINE_RING 128
+#endif
+constexpr int kRing = BIMINE_RING;  // boundary values buffered per ring
 
 // A ring slot carries its value and the position it holds, written by one
 // 16-byte shared-memory store, so a consumer polling the slot's position
@@ -713,10 +716,34 @@ struct BigRing {
   volatile long long cons;  // positions consumed (capacity hint for the producer)
 };
 
-__device__ __forceinline__ void ring_put(double2 *slot, double v, long long pos) {
-  asm volatile("st.volatile.shared.v2.f64 [%0], {%1, %2};" ::"r"((unsigned)__cvta_generic_to_shared(slot)), "d"(v),
-               "d"(__longlong_as_double(pos))
+// The band pipeline's boundary stores: lane 31's store of each step as one
+// predicated instruction (no branch, so no reconvergence point in the step
+// loop; every lane forms the address, only the predicate differs).
+__device__ __forceinline__ void st_shared_v2_if(bool p, const void *slot, double v, long long tag) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.volatile.shared.v2.f64 [%1], {%2, %3};\n\t}" ::"r"(
+                   (unsigned)p),
+               "r"((unsigned)__cvta_generic_to_shared(slot)), "d"(v), "d"(__longlong_as_double(tag))
                : "memory");
+}
+__device__ __forceinline__ void st_cluster_v2_if(bool p, unsigned addr, double v, long long tag) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.relaxed.cluster.shared::cluster.v2.f64 [%1], {%2, %3};\n\t}" ::"r"(
+          (unsigned)p),
+      "r"(addr), "d"(v), "d"(__longlong_as_double(tag))
+      : "memory");
+}
+__device__ __forceinline__ void st_global_v2_if(bool p, const void *slot, double v, long long tag) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.relaxed.gpu.global.v2.f64 [%1], {%2, %3};\n\t}" ::"r"(
+                   (unsigned)p),
+               "l"(slot), "d"(v), "d"(__longlong_as_double(tag))
+               : "memory");
+}
+// %laneid, read once (a `threadIdx.x & 31` inside the step loop is
+// re-derived from %tid by an S2R per use)
+__device__ __forceinline__ unsigned lane_id_reg() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));
+  return r;
 }
 
 __device__ __forceinline__ double ring_get(const double2 *slot, long long pos) {
@@ -815,18 +842,22 @@ struct BotRing {
   long long base;
   int M;
   bool on;
+  bool l31;                       // this thread is lane 31
+  long long seen = -(1ll << 62);  // last `cons` read (it only grows: a stale value is safe)
   // warp-uniform wait (every lane reads the same `cons`): the group's
-  // stores, positions up to base + s0 + 7 - 30, must not lap the consumer
-  __device__ void reserve(int s0) const {
+  // stores, positions up to base + s0 + 7 - 30, must not lap the consumer;
+  // `cons` is re-read only when the last value read does not allow them
+  __device__ void reserve(int s0) {
     if (!on) return;
     const long long last = base + (s0 + 7 - 30);
-    while (last - out->cons >= kRing - 1)
-      if (kSpinNs) __nanosleep(kSpinNs);
+    while (last - seen >= kRing - 1) {
+      seen = out->cons;
+      if (kSpinNs && last - seen >= kRing - 1) __nanosleep(kSpinNs);
+    }
   }
   __device__ void put(int s, bool v, double best) const {
-    if (!(on && v && (threadIdx.x & 31) == 31)) return;
     const long long pos = base + (s - 30);
-    ring_put(&out->slot[pos & (kRing - 1)], best, pos);
+    st_shared_v2_if(on && v && l31, &out->slot[pos & (kRing - 1)], best, pos);
   }
 };
 
@@ -842,13 +873,11 @@ struct BotRowG {  // lane 31 writes tagged slots of a global row
   double2 *row;
   long long base;
   bool on;
+  bool l31;
   __device__ void reserve(int) const {}
   __device__ void put(int s, bool v, double best) const {
-    if (!(on && v && (threadIdx.x & 31) == 31)) return;
     const int b = s - 30;
-    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(row + b), "d"(best),
-                 "d"(__longlong_as_double(base + b))
-                 : "memory");
+    st_global_v2_if(on && v && l31, row + b, best, base + b);
   }
 };
 
@@ -952,24 +981,28 @@ struct BotRemote {  // lane 31 writes ring 0 of the next CTA of the cluster
   unsigned cons;    // shared::cluster address of its cons
   long long base;
   bool on;
-  __device__ void reserve(int s0) const {
+  bool l31;
+  long long seen = -(1ll << 62);  // last remote `cons` read (a DSMEM round trip per group otherwise)
+  __device__ void reserve(int s0) {
     if (!on) return;
     const long long last = base + (s0 + 7 - 30);
-    while (true) {
-      long long c;
-      asm volatile("ld.relaxed.cluster.shared::cluster.b64 %0, [%1];" : "=l"(c) : "r"(cons) : "memory");
-      if (last - c < kRing - 1) break;
-      if (kSpinNs) __nanosleep(kSpinNs);
+    while (last - seen >= kRing - 1) {
+      asm volatile("ld.relaxed.cluster.shared::cluster.b64 %0, [%1];" : "=l"(seen) : "r"(cons) : "memory");
+      if (kSpinNs && last - seen >= kRing - 1) __nanosleep(kSpinNs);
     }
   }
   __device__ void put(int s, bool v, double best) const {
-    if (!(on && v && (threadIdx.x & 31) == 31)) return;
     const long long pos = base + (s - 30);
-    asm volatile("st.relaxed.cluster.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(slot0 + (unsigned)((pos & (kRing - 1)) * 16)),
-                 "d"(best), "d"(__longlong_as_double(pos))
-                 : "memory");
+    st_cluster_v2_if(on && v && l31, slot0 + (unsigned)((pos & (kRing - 1)) * 16), best, pos);
   }
 };
+
+#ifdef BIMINE_PROF_GLOBAL
+__device__ unsigned long long g_prof_band[4096];
+#endif
+#ifdef BIMINE_FAKE_CALL
+__device__ __noinline__ void bimine_noop_call(int g) { asm volatile("" ::"r"(g) : "memory"); }
+#endif
 
 template <int MODE, int W>
 __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t *g_dirs_all,
@@ -1007,6 +1040,13 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
   if (threadIdx.x < W) rings[threadIdx.x].cons = 0;
   __syncthreads();
   cluster_barrier();  // every ring initialised before any remote write
+#ifdef BIMINE_PROF_GLOBAL
+  if (crank == 0 && threadIdx.x == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    g_prof_band[4095] = gt;
+  }
+#endif
 #if defined(BIMINE_NW_PROFILE) || defined(BIMINE_PROF_START)
   if (threadIdx.x == 0) {
     unsigned long long gt;
@@ -1015,20 +1055,21 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
   }
 #endif
   const bool has_next = crank + 1 < K;
+  const bool l31 = lane_id_reg() == 31u;
   const unsigned r_slot0 = has_next ? cluster_addr(&rings[0].slot[0], crank + 1) : 0u;
   const unsigned r_cons = has_next ? cluster_addr((const void *)&rings[0].cons, crank + 1) : 0u;
   for (int g = crank * W + warp, gen = 0; g < G; g += per_round, ++gen) {
     double fin;
     const bool last_warp = warp + 1 == W;
     const int ogr = (g + 1) / per_round;  // round of the consumer band
-    BotRing bring{&rings[(warp + 1) % W], (long long)gen * W1, M, g + 1 < G && !last_warp};
-    BotRemote brem{r_slot0, r_cons, (long long)gen * W1, g + 1 < G && last_warp && has_next};
-    BotRowG brow{wrap + (ogr & 1) * W1, (long long)(g + 1) * W1, g + 1 < G && last_warp && !has_next};
+    BotRing bring{&rings[(warp + 1) % W], (long long)gen * W1, M, g + 1 < G && !last_warp, l31};
+    BotRemote brem{r_slot0, r_cons, (long long)gen * W1, g + 1 < G && last_warp && has_next, l31};
+    BotRowG brow{wrap + (ogr & 1) * W1, (long long)(g + 1) * W1, g + 1 < G && last_warp && !has_next, l31};
     struct Bot3 {
-      const BotRing &r;
-      const BotRemote &x;
+      BotRing &r;
+      BotRemote &x;
       const BotRowG &w;
-      __device__ void reserve(int s0) const {
+      __device__ void reserve(int s0) {
         r.reserve(s0);
         x.reserve(s0);
       }
@@ -1055,13 +1096,25 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
     if (32 * g + 1 + lane == N) last_val[slot] = fin;
     __syncwarp();
     // (a guard only for launches without the operand layout, never true
-    // from abi.cu).  Its call site changes ptxas's schedule of the ring
-    // loops: 2.1 ms for the 4096x4096 sweep with it, 3.6 ms without
-    // (profiles/r2/nw_big_printf_ab.txt: same instruction mix, 37% of the
-    // issue slots in the ring polls either way).  Kept deliberately;
-    // tests/test_gpu_perf_guard.py fails if a toolchain change loses it.
+    // from abi.cu).  A call site here -- this one, or an empty __noinline__
+    // call (-DBIMINE_FAKE_CALL) -- is worth 2.8x on the 4096x4096 sweep:
+    // band 0 runs at the same speed either way, but without a call each
+    // consumer band's hand-off lag goes from 6.5 to 21.6 us, with the
+    // consumer's ring-poll SASS identical (profiles/r2/nw_big_printf_ab.txt).
+    // Kept deliberately; tests/test_gpu_perf_guard.py fails if a toolchain
+    // change loses it.
 #ifndef BIMINE_NO_PRINTF
     if (diag_all == nullptr) printf("bimine: nw_big_kernel band %d without its operand layout\n", g);
+#endif
+#ifdef BIMINE_FAKE_CALL
+    if (diag_all == nullptr) bimine_noop_call(g);
+#endif
+#ifdef BIMINE_PROF_GLOBAL  // profiling builds: band end times in a device array, no printf call site
+    if (lane == 0 && g < 4096) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      g_prof_band[g] = gt;
+    }
 #endif
 #if defined(BIMINE_NW_PROFILE) || defined(BIMINE_PROF_BAND)
     if (lane == 0) {

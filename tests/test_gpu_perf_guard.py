@@ -1,8 +1,8 @@
 """Timing guard for the cluster NW sweep's codegen sensitivity.
 
 nw_big_kernel keeps an unreachable printf call site in its band loop: with
-it ptxas schedules the ring hand-offs so that the 4096x4096 NW (operand
-layout + sweep + traceback) takes ~3.6 ms, without it ~5 ms
+it the 4096x4096 NW (operand layout + sweep + traceback) takes ~2.9 ms,
+without it ~5.9 ms -- each band's hand-off lag triples
 (profiles/r2/nw_big_printf_ab.txt).  A toolchain change that loses the
 effect fails here instead of silently slowing C3.
 """
@@ -20,7 +20,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU containers
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIMIT_MS = 4.4
+LIMIT_MS = 4.0
 
 
 def test_c3_nw_sweep_keeps_its_schedule():
