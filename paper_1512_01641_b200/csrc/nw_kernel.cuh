@@ -1160,9 +1160,15 @@ __device__ void nw_big_traceback_one(const NwArgs &A, const uint32_t *g_dirs_all
   const double s_last = last_val[slot];
   if (MODE == kNwTable) return;
   // ---- traceback on warp 0: lane 0 walks, the warp stages 16 direction
-  // groups (128 steps) of the current band at a time
+  // groups (128 steps) of the current band at a time.  A staged cell holds
+  // the index step to the next cell of the path in the window's
+  // [lane][step] layout (rows of kTbRow bytes): 1 = left (b - 1), kTbRow + 1
+  // = up (a - 1: lane - 1, step - 1), kTbRow + 2 = diagonal -- so a step of
+  // the walk is one shared-memory byte load and one subtraction.
   if (warp == 0) {
-    __shared__ uint16_t win[16 * 32];
+    constexpr int kTbRow = 132;  // 128 steps + 4: lane rows start in distinct banks
+    constexpr uint32_t kDelLut = (1u << 16) | ((uint32_t)(kTbRow + 1) << 8) | (uint32_t)(kTbRow + 2);  // by d
+    __shared__ __align__(16) uint8_t win[32 * kTbRow];
     __shared__ int win_g, win_k0;
     int a = N, b = M;
     int64_t cnt = 0;
@@ -1173,6 +1179,23 @@ __device__ void nw_big_traceback_one(const NwArgs &A, const uint32_t *g_dirs_all
       win_k0 = 0;
     }
     __syncwarp();
+    // a lane's 16 direction words of the window -> its row of step bytes
+    auto stage = [&](const uint16_t *w16) {
+      uint32_t *row = reinterpret_cast<uint32_t *>(win + lane * kTbRow);
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t d = ((uint32_t)w16[t] >> (2 * (4 * h + u))) & 3u;
+            word |= ((kDelLut >> (8 * d)) & 0xFFu) << (8 * u);
+          }
+          row[2 * t + h] = word;
+        }
+      }
+    };
     // the next band's window, loaded into registers while lane 0 walks the
     // current one: the path enters band g-1 at a column no greater than
     // where it entered band g, so the window ending at that column covers
@@ -1186,8 +1209,7 @@ __device__ void nw_big_traceback_one(const NwArgs &A, const uint32_t *g_dirs_all
       const int g = (a - 1) >> 5, l = (a - 1) & 31, k = (b + l - 1) >> 3;
       if (!(g == win_g && k >= win_k0 && k < win_k0 + 16)) {
         if (g == pre_g && k >= pre_k0 && k < pre_k0 + 16) {
-#pragma unroll
-          for (int t = 0; t < 16; ++t) win[t * 32 + lane] = pre[t];
+          stage(pre);
           __syncwarp();
           if (lane == 0) {
             win_g = g;
@@ -1195,10 +1217,13 @@ __device__ void nw_big_traceback_one(const NwArgs &A, const uint32_t *g_dirs_all
           }
         } else {
           const int k0 = max(0, k - 15);
-          for (int x = lane; x < 16 * 32; x += 32) {
-            const int kk = k0 + (x >> 5);
-            win[x] = kk < G8 ? __ldcg(dirs + ((int64_t)g * G8 + kk) * 32 + (x & 31)) : (uint16_t)0;
+          uint16_t cur[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int kk = k0 + t;
+            cur[t] = kk < G8 ? __ldcg(dirs + ((int64_t)g * G8 + kk) * 32 + lane) : (uint16_t)0;
           }
+          stage(cur);
           __syncwarp();
           if (lane == 0) {
             win_g = g;
@@ -1217,43 +1242,48 @@ __device__ void nw_big_traceback_one(const NwArgs &A, const uint32_t *g_dirs_all
         }
       }
       if (lane == 0) {
-        // window bounds and base in registers: nothing but the direction
-        // load itself on the walk's dependency chain
-        const int wg = win_g, wk0 = win_k0;
-        const uint16_t *wb = win;
-        auto step = [&]() {
-          const int ll = (a - 1) & 31, ss = b + ll - 1;
-          const uint32_t d = ((uint32_t)wb[((ss >> 3) - wk0) * 32 + ll] >> (2 * (ss & 7))) & 3u;
-          if (MODE == kNwMine) {
-            if (d == 0u) {
-              outm[cnt].i = N - a;  // score filled below
-              outm[cnt].j = M - b;
-              ++cnt;
+        const int s_base = 8 * win_k0, arow = 32 * win_g + 1;  // window step 0; a = arow + lane
+        // the current cell as a window index; valid while the walk stays in
+        // the window: each step lowers the lane by <= 1 and the step by <= 2
+        int idx = ((a - 1) & 31) * kTbRow + (b + ((a - 1) & 31) - 1 - s_base);
+        while (true) {
+          const int ll = idx / kTbRow, ss = s_base + idx - ll * kTbRow;
+          a = arow + ll;
+          b = ss - ll + 1;
+          const int safe = min(min(ll, b - 1), (ss - s_base) >> 1);
+          auto emit = [&](int del, int ia, int ib) {
+            if (MODE == kNwMine) {
+              if (del == kTbRow + 2) {
+                outm[cnt].i = N - ia;  // score filled below
+                outm[cnt].j = M - ib;
+                ++cnt;
+              }
+            } else {
+              st[cnt++] = (uint8_t)(del == kTbRow + 2 ? 0 : del == kTbRow + 1 ? 1 : 2);
             }
-          } else {
-            st[cnt++] = (uint8_t)d;
+          };
+          if (safe <= 0) {  // the step may leave the window, the band or the table
+            const int del = win[idx];
+            emit(del, a, b);
+            a -= del != 1;
+            b -= del != kTbRow + 1;
+            break;
           }
-          a -= (d != 2u);
-          b -= (d != 1u);
-        };
-        while (a > 0 && b > 0) {
-          const int gg = (a - 1) >> 5, ll = (a - 1) & 31, ss = b + ll - 1, kk = ss >> 3;
-          if (gg != wg || kk < wk0 || kk >= wk0 + 16) break;
-          // steps that cannot leave the band, the window or the table: each
-          // step lowers a by <= 1 and s = b + l - 1 by <= 2, and b by <= 1
-          const int safe = min(min(ll, b - 1), (ss - 8 * wk0) >> 1);
-          if (safe <= 0) {
-            step();
-            continue;
+#pragma unroll 4
+          for (int t = 0; t < safe; ++t) {
+            const int del = win[idx];
+            if (MODE == kNwMine) {
+              if (del == kTbRow + 2) {  // a, b of this cell, off the walk's dependency chain
+                const int l2 = idx / kTbRow;
+                outm[cnt].i = N - (arow + l2);
+                outm[cnt].j = M - (s_base + idx - l2 * kTbRow - l2 + 1);
+                ++cnt;
+              }
+            } else {
+              st[cnt++] = (uint8_t)(del == kTbRow + 2 ? 0 : del == kTbRow + 1 ? 1 : 2);
+            }
+            idx -= del;
           }
-          int t = 0;
-          for (; t + 4 <= safe; t += 4) {
-            step();
-            step();
-            step();
-            step();
-          }
-          for (; t < safe; ++t) step();
         }
       }
       __syncwarp();
@@ -1272,28 +1302,45 @@ __device__ void nw_big_traceback_one(const NwArgs &A, const uint32_t *g_dirs_all
         A.n_steps[q] = (int32_t)cnt;
       }
     } else {
-      // gather the scores in parallel, keep those at or above the threshold
+      // gather the scores in parallel, keep those at or above the threshold:
+      // 8 batches of 32 matches per round, all their loads in flight before
+      // the in-order compaction (the scores are scattered over the whole
+      // N x M matrix: one round trip per batch made this half the traceback)
       const double thr = nw_threshold(A, setting);
       int64_t kept = 0;
-      for (int64_t base = 0; base < cnt; base += 32) {
-        const int64_t c = base + lane;
-        double v = 0.0;
-        int32_t i = 0, j = 0;
-        if (c < cnt) {
-          i = outm[c].i;
-          j = outm[c].j;
-          v = sim[(int64_t)i * M + j];
+      constexpr int kRounds = 8;
+      for (int64_t base = 0; base < cnt; base += 32 * kRounds) {
+        int32_t ii[kRounds], jj[kRounds];
+        double vv[kRounds];
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+          const int64_t c = base + 32 * r + lane;
+          ii[r] = 0;
+          jj[r] = 0;
+          if (c < cnt) {
+            ii[r] = outm[c].i;
+            jj[r] = outm[c].j;
+          }
         }
-        const bool keep = c < cnt && v >= thr;
-        const unsigned bal = __ballot_sync(kFull, keep);
-        __syncwarp();
-        if (keep) {
-          bimine_match &o = outm[kept + __popc(bal & ((1u << lane) - 1u))];
-          o.score = v;
-          o.i = i;
-          o.j = j;
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+          const int64_t c = base + 32 * r + lane;
+          vv[r] = c < cnt ? sim[(int64_t)ii[r] * M + jj[r]] : 0.0;
         }
-        kept += __popc(bal);
+        __syncwarp();  // every read of this round's entries before any write
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+          const int64_t c = base + 32 * r + lane;
+          const bool keep = c < cnt && vv[r] >= thr;
+          const unsigned bal = __ballot_sync(kFull, keep);
+          if (keep) {
+            bimine_match &o = outm[kept + __popc(bal & ((1u << lane) - 1u))];
+            o.score = vv[r];
+            o.i = ii[r];
+            o.j = jj[r];
+          }
+          kept += __popc(bal);
+        }
         __syncwarp();
       }
       if (lane == 0) A.counts[q] = (int32_t)kept;
