@@ -716,27 +716,22 @@ struct BigRing {
   volatile long long cons;  // positions consumed (capacity hint for the producer)
 };
 
-// The band pipeline's boundary stores: lane 31's store of each step as one
-// predicated instruction (no branch, so no reconvergence point in the step
-// loop; every lane forms the address, only the predicate differs).
-__device__ __forceinline__ void st_shared_v2_if(bool p, const void *slot, double v, long long tag) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.volatile.shared.v2.f64 [%1], {%2, %3};\n\t}" ::"r"(
-                   (unsigned)p),
-               "r"((unsigned)__cvta_generic_to_shared(slot)), "d"(v), "d"(__longlong_as_double(tag))
-               : "memory");
-}
-__device__ __forceinline__ void st_cluster_v2_if(bool p, unsigned addr, double v, long long tag) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.relaxed.cluster.shared::cluster.v2.f64 [%1], {%2, %3};\n\t}" ::"r"(
-          (unsigned)p),
-      "r"(addr), "d"(v), "d"(__longlong_as_double(tag))
-      : "memory");
-}
-__device__ __forceinline__ void st_global_v2_if(bool p, const void *slot, double v, long long tag) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.relaxed.gpu.global.v2.f64 [%1], {%2, %3};\n\t}" ::"r"(
+// The band pipeline's boundary store: lane 31's store of each step as one
+// predicated generic instruction (no branch, so no reconvergence point in
+// the step loop; every lane forms the address, only the predicate
+// differs).  Generic addressing reaches the CTA's own ring, the next CTA's
+// ring (a mapa'd address) and the global wrap row alike.
+__device__ __forceinline__ void st_generic_v2_if(bool p, const void *slot, double v, long long tag) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.relaxed.gpu.v2.f64 [%1], {%2, %3};\n\t}" ::"r"(
                    (unsigned)p),
                "l"(slot), "d"(v), "d"(__longlong_as_double(tag))
                : "memory");
+}
+// generic address of the same shared-memory object in cluster CTA `rank`
+__device__ __forceinline__ void *cluster_generic(const void *p, unsigned rank) {
+  void *r;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(p), "r"(rank));
+  return r;
 }
 // %laneid, read once (a `threadIdx.x & 31` inside the step loop is
 // re-derived from %tid by an S2R per use)
@@ -855,10 +850,6 @@ struct BotRing {
       if (kSpinNs && last - seen >= kRing - 1) __nanosleep(kSpinNs);
     }
   }
-  __device__ void put(int s, bool v, double best) const {
-    const long long pos = base + (s - 30);
-    st_shared_v2_if(on && v && l31, &out->slot[pos & (kRing - 1)], best, pos);
-  }
 };
 
 // Boundaries between bands of the same round (warp w-1 -> warp w, w >= 1)
@@ -875,10 +866,6 @@ struct BotRowG {  // lane 31 writes tagged slots of a global row
   bool on;
   bool l31;
   __device__ void reserve(int) const {}
-  __device__ void put(int s, bool v, double best) const {
-    const int b = s - 30;
-    st_global_v2_if(on && v && l31, row + b, best, base + b);
-  }
 };
 
 template <int W>
@@ -991,10 +978,6 @@ struct BotRemote {  // lane 31 writes ring 0 of the next CTA of the cluster
       if (kSpinNs && last - seen >= kRing - 1) __nanosleep(kSpinNs);
     }
   }
-  __device__ void put(int s, bool v, double best) const {
-    const long long pos = base + (s - 30);
-    st_cluster_v2_if(on && v && l31, slot0 + (unsigned)((pos & (kRing - 1)) * 16), best, pos);
-  }
 };
 
 #ifdef BIMINE_PROF_GLOBAL
@@ -1058,6 +1041,7 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
   const bool l31 = lane_id_reg() == 31u;
   const unsigned r_slot0 = has_next ? cluster_addr(&rings[0].slot[0], crank + 1) : 0u;
   const unsigned r_cons = has_next ? cluster_addr((const void *)&rings[0].cons, crank + 1) : 0u;
+  void *const r_gslot0 = has_next ? cluster_generic(&rings[0].slot[0], crank + 1) : nullptr;
   for (int g = crank * W + warp, gen = 0; g < G; g += per_round, ++gen) {
     double fin;
     const bool last_warp = warp + 1 == W;
@@ -1065,20 +1049,40 @@ __global__ void __launch_bounds__(W * 32) nw_big_kernel(const NwArgs A, uint32_t
     BotRing bring{&rings[(warp + 1) % W], (long long)gen * W1, M, g + 1 < G && !last_warp, l31};
     BotRemote brem{r_slot0, r_cons, (long long)gen * W1, g + 1 < G && last_warp && has_next, l31};
     BotRowG brow{wrap + (ogr & 1) * W1, (long long)(g + 1) * W1, g + 1 < G && last_warp && !has_next, l31};
+    // whichever of the three the band writes, one generic 16-byte store per
+    // step: slot (b + off) & mask of `to`, tag base + b (b = s - 30)
     struct Bot3 {
       BotRing &r;
       BotRemote &x;
-      const BotRowG &w;
+      char *to;
+      int off, mask;
+      long long base;
+      bool on, l31;
       __device__ void reserve(int s0) {
         r.reserve(s0);
         x.reserve(s0);
       }
       __device__ void put(int s_, bool v, double best) const {
-        r.put(s_, v, best);
-        x.put(s_, v, best);
-        w.put(s_, v, best);
+        const int b = s_ - 30;
+        st_generic_v2_if(on && v && l31, to + (int64_t)((b + off) & mask) * 16, best, base + b);
       }
-    } bot{bring, brem, brow};
+    };
+    Bot3 bot{bring, brem, nullptr, 0, -1, 0, false, l31};
+    if (bring.on) {
+      bot.to = (char *)&bring.out->slot[0];
+      bot.base = bring.base;
+    } else if (brem.on) {
+      bot.to = (char *)r_gslot0;
+      bot.base = brem.base;
+    } else if (brow.on) {
+      bot.to = (char *)brow.row;
+      bot.base = brow.base;
+    }
+    bot.on = bring.on || brem.on || brow.on;
+    if (!brow.on) {  // a ring: slots wrap
+      bot.off = (int)(bot.base & (kRing - 1));
+      bot.mask = kRing - 1;
+    }
     uint16_t *dband = dirs + (int64_t)g * G8 * 32;
     const double *dg = diag + g * dstride;
     if (g == 0) {
