@@ -118,9 +118,13 @@ void *pinned_scratch(size_t bytes) {
 // launches that read everything (long-sentence kernel, NW) wait for `all`.
 struct UploadGate {
   const int32_t *ready;  // grows as pieces land
-  const int32_t *need;   // per pair: the counter value its data need
+  const int32_t *need;   // per pair: the counter value its data need (null: the CTAs derive it)
   cudaEvent_t all;
   std::function<void()> before_all;  // host side: `all` is recorded once this returns
+  bool pair_launched = false;        // the pair kernel already runs (bimine_mine_host launches it early)
+  int64_t n_sentences = 0, n_tokens = 0;
+  int32_t n_pieces = 0;
+  const int64_t *piece_start = nullptr;
 };
 thread_local const UploadGate *tl_gate = nullptr;
 cudaError_t gate_wait_all(cudaStream_t st) {
@@ -606,6 +610,61 @@ extern "C" {
 
 namespace {
 
+// One launch of the pair kernel: the tiles of pairs larger than 64x64, then
+// one item per pair, over persistent CTAs.  gate: the upload gate of
+// bimine_mine_host (null: the data are in place).
+int launch_pair_kernel(const bimine_dict *dict, const double *model, const bimine_batch *b, const int64_t *tiles,
+                       int64_t n_tiles, int64_t n_cells, double *sim_dev, cudaStream_t st, double *features,
+                       const UploadGate *gate) {
+  if (b->n_pairs > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: more than 2^31-1 pairs per call");
+  PairArgs A;
+  memset(&A, 0, sizeof(A));
+  A.b = to_dev(*b);
+  A.d = DictDev{dict->n_rows, dict->row_ptr, dict->tgt, dict->prob, dict->rowdesc, dict->ent};
+  A.md = to_model(model);
+  int rc = term_tables(model, st, &A.T);
+  if (rc != BIMINE_OK) return rc;
+  A.sim = sim_dev;
+  // per-cell counters (L2 resident while a CTA works on them), then the
+  // persistent CTAs' work counter
+  const size_t aux_bytes = (sizeof(uint16_t) * std::max<int64_t>(n_cells, 1) + 15) & ~(size_t)15;
+  BIMINE_CUDA(cudaMallocAsync((void **)&A.aux, aux_bytes + 16, st));
+  A.next_item = (unsigned long long *)((char *)A.aux + aux_bytes);
+  BIMINE_CUDA(cudaMemsetAsync(A.next_item, 0, 8, st));
+  const size_t smem = kPairSmemBytes;
+  const bool packed = b->token_bytes == 3;
+  auto kern = features ? (packed ? pair_kernel<true, true> : pair_kernel<true, false>)
+                       : (packed ? pair_kernel<false, true> : pair_kernel<false, false>);
+  BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  A.tiles = n_tiles ? tiles : nullptr;
+  A.n_tiles = n_tiles;
+  A.features = features;
+  if (gate) {
+    A.ready = gate->ready;
+    A.need = gate->need;
+    A.n_sentences = gate->n_sentences;
+    A.n_tokens = gate->n_tokens;
+    A.n_pieces = gate->n_pieces;
+    A.piece_start = gate->piece_start;
+  }
+  const int64_t items = n_tiles + b->n_pairs;
+  static thread_local std::map<std::pair<int, const void *>, int> resident;  // (device, kernel) -> CTAs per SM
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int &per_sm = resident[{dev, (const void *)kern}];
+  if (per_sm == 0) {
+    BIMINE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPairThreads, smem));
+    per_sm = std::max(per_sm, 1);
+  }
+  const int64_t grid = std::min<int64_t>(items, (int64_t)num_sms() * per_sm);
+  kern<<<(unsigned)grid, kPairThreads, smem, st>>>(A);
+  const cudaError_t le = cudaGetLastError();
+  cudaFreeAsync(A.aux, st);
+  if (le != cudaSuccess) return fail(BIMINE_E_CUDA, std::string("pair_kernel: ") + cudaGetErrorString(le));
+  return BIMINE_OK;
+}
+
 int launch_scores(const bimine_dict *dict, const double *model, const bimine_batch *b, const bimine_plan *plan,
                   double *sim_dev, cudaStream_t st, double *features = nullptr) {
   if (!dict || !model || !b || !plan || !sim_dev) return fail(BIMINE_E_ARG, "bimine_score_batch: null argument");
@@ -620,38 +679,10 @@ int launch_scores(const bimine_dict *dict, const double *model, const bimine_bat
   const BatchDev bd = to_dev(*b);
   const DictDev dd = DictDev{dict->n_rows, dict->row_ptr, dict->tgt, dict->prob, dict->rowdesc, dict->ent};
   const Model md = to_model(model);
-  {
-    PairArgs A;
-    memset(&A, 0, sizeof(A));
-    A.b = bd;
-    A.d = dd;
-    A.md = md;
-    int rc = term_tables(model, st, &A.T);
+  if (!(tl_gate && tl_gate->pair_launched)) {
+    const int rc = launch_pair_kernel(dict, model, b, plan->n_tiles ? plan->work : nullptr, plan->n_tiles,
+                                      plan->n_cells, sim_dev, st, features, tl_gate);
     if (rc != BIMINE_OK) return rc;
-    A.sim = sim_dev;
-    // per-cell counters scratch (L2 resident while a CTA works on it)
-    const int64_t cells = plan->n_cells;
-    BIMINE_CUDA(cudaMallocAsync((void **)&A.aux, sizeof(uint16_t) * std::max<int64_t>(cells, 1), st));
-    const size_t smem = kPairSmemBytes;
-    const bool packed = b->token_bytes == 3;
-    auto kern = features ? (packed ? pair_kernel<true, true> : pair_kernel<true, false>)
-                         : (packed ? pair_kernel<false, true> : pair_kernel<false, false>);
-    BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    BIMINE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    // one launch: the tiles of pairs larger than 64x64, then one CTA per pair
-    A.tiles = plan->n_tiles ? plan->work : nullptr;
-    A.n_tiles = plan->n_tiles;
-    A.features = features;
-    if (tl_gate) {
-      A.ready = tl_gate->ready;
-      A.need = tl_gate->need;
-    }
-    const int64_t grid = plan->n_tiles + b->n_pairs;
-    if (grid > 0x7fffffffLL) return fail(BIMINE_E_LIMIT, "bimine_score_batch: too many CTAs");
-    kern<<<(unsigned)grid, kPairThreads, smem, st>>>(A);
-    const cudaError_t le = cudaGetLastError();
-    cudaFreeAsync(A.aux, st);
-    if (le != cudaSuccess) return fail(BIMINE_E_CUDA, std::string("pair_kernel: ") + cudaGetErrorString(le));
   }
   if (plan->n_long > 0) {
     BIMINE_CUDA(gate_wait_all(st));
@@ -1177,27 +1208,40 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     return v ? std::max<int64_t>(1, atoll(v)) : (int64_t)1 << 20;
   }();
   const int nt = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)max_chunks, T / min_tokens));
-  const int nc = (int)std::max<int64_t>(1, std::min<int64_t>(8, P));  // analysis threads
+  static const int max_analysis = [] {
+    const char *v = getenv("BIMINE_E2E_ANALYSIS_THREADS");
+    return v ? std::max(1, atoi(v)) : 8;
+  }();
+  const int nc = (int)std::max<int64_t>(1, std::min<int64_t>(max_analysis, P));  // analysis threads
   std::vector<int64_t> cut(nc + 1), tcut(nt + 1);
   for (int k = 0; k <= nc; ++k) cut[k] = P * k / nc;
   for (int j = 0; j <= nt; ++j) tcut[j] = T * j / nt;
   // pinned staging: slot offsets [P] | per-pair need [P] (int32) | ready values [nt + 1] | merged work
-  int64_t work_bound = 0;
-  for (int64_t p = 0; p < P; ++p)
-    work_bound += 3 + 3 * (int64_t)((h->pair_n[p] + kPairMax - 1) / kPairMax) * ((h->pair_m[p] + kPairMax - 1) / kPairMax);
-  const int64_t n_stage = P + (P + 1) / 2 + (nt + 2) / 2 + 1 + std::max<int64_t>(work_bound, 1);
+  int64_t work_bound = 0, n_tiles_pre = 0;  // (tiles: the 64x64 blocks of pairs larger than 64x64)
+  for (int64_t p = 0; p < P; ++p) {
+    const int32_t n = h->pair_n[p], m = h->pair_m[p];
+    const int64_t tl = (int64_t)((n + kPairMax - 1) / kPairMax) * ((m + kPairMax - 1) / kPairMax);
+    work_bound += 3 + 3 * tl;
+    if (n > kPairMax || m > kPairMax) n_tiles_pre += tl;
+  }
+  const int64_t n_stage = P + (P + 1) / 2 + (nt + 2) / 2 + 1 + std::max<int64_t>(work_bound, 1) +
+                          3 * std::max<int64_t>(n_tiles_pre, 0) + (nt + 1);
   int64_t *staging = (int64_t *)pinned_scratch(sizeof(int64_t) * n_stage);
   if (!staging) return fail(BIMINE_E_CUDA, "bimine_mine_host: pinned staging allocation failed");
   int64_t *out_off = staging;
   int32_t *need = (int32_t *)(staging + P);
   int32_t *ready_vals = need + P;
   int64_t *work = staging + P + (P + 1) / 2 + (nt + 2) / 2 + 1;
+  int64_t *tiles_pre = work + std::max<int64_t>(work_bound, 1);
+  int64_t *tcut_pinned = tiles_pre + 3 * n_tiles_pre;  // the piece boundaries, uploaded with the pair arrays
+  for (int j = 0; j <= nt; ++j) tcut_pinned[j] = tcut[j];
   for (int j = 0; j <= nt; ++j) ready_vals[j] = j + 1;
   // per pair (O(P)): match slots, cells
   int64_t cap = 0, cells = 0;
   for (int64_t p = 0; p < P; ++p) {
     const int32_t n = h->pair_n[p], m = h->pair_m[p];
     if (n < 1 || m < 1) return fail(BIMINE_E_ARG, "bimine_plan_batch: empty document");
+    if (h->pair_sim_off[p] < 0) return fail(BIMINE_E_ARG, "bimine_mine_host: negative pair_sim_off");
     out_off[p] = cap;
     cap += std::min(n, m);
     cells = std::max(cells, h->pair_sim_off[p] + (int64_t)n * m);
@@ -1227,7 +1271,8 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
                o_pm = carve(4 * P), o_psim = carve(8 * P), o_outoff = carve(8 * P), o_sim = carve(8 * cells),
                o_slots = carve(sizeof(bimine_match) * cap), o_counts = carve(4 * P), o_base = carve(8 * P),
                o_comp = carve(sizeof(bimine_match) * cap), o_total = carve(8),
-               o_work = carve(8 * std::max<int64_t>(work_bound, 1)), o_need = carve(4 * P), o_ready = carve(4);
+               o_work = carve(8 * std::max<int64_t>(work_bound, 1)), o_tiles = carve(8 * std::max<int64_t>(3 * n_tiles_pre, 1)), o_need = carve(4 * P), o_ready = carve(4),
+               o_tcut = carve(8 * (size_t)(nt + 1));
   // sent_tok_off is not uploaded: the copy stream rebuilds it from sent_len
   // (the usual packed layout); the analysis threads check that the caller's
   // offsets are exactly that, else they are uploaded on `st` before scoring
@@ -1282,6 +1327,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     H2D(o_slen, h->sent_len, 4 * S, pg_sent);
     H2D(o_suniq, h->sent_uniq, 4 * S, pg_sent);
     H2D(o_schar, h->sent_chars, 4 * S, pg_sent);
+    H2D(o_tcut, tcut_pinned, 8 * (size_t)(nt + 1), false);
     if (ue == cudaSuccess)
       ue = offsets_from_lengths((const int32_t *)(arena + o_slen), (int64_t *)(arena + o_soff), S, arena + o_scan,
                                 &scan_bytes, cs);
@@ -1319,6 +1365,58 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     return fail(code, msg);
   };
   if (e != cudaSuccess) return abort_with(BIMINE_E_CUDA, std::string("bimine_mine_host H2D: ") + cudaGetErrorString(e));
+  // ---- the score kernel goes now, before the host has looked at the
+  //      batch: its CTAs bounds-check their pairs and derive their upload
+  //      gates themselves (pair_kernel.cuh, self gate), and the analysis
+  //      below runs beside it.  The tiles of pairs larger than 64x64 come
+  //      from the shapes alone.  The launch follows the offsets scan on the
+  //      copy stream: waiting CTAs may fill every SM.
+  bimine_batch d;
+  d.n_pairs = P;
+  d.n_sentences = S;
+  d.n_tokens = T;
+  d.tokens = (const int32_t *)(arena + o_tok);
+  d.token_bytes = tb;
+  d.sent_tok_off = (const int64_t *)(arena + o_soff);
+  d.sent_len = (const int32_t *)(arena + o_slen);
+  d.sent_uniq = (const int32_t *)(arena + o_suniq);
+  d.sent_chars = (const int32_t *)(arena + o_schar);
+  d.pair_src = (const int64_t *)(arena + o_psrc);
+  d.pair_n = (const int32_t *)(arena + o_pn);
+  d.pair_tgt = (const int64_t *)(arena + o_ptgt);
+  d.pair_m = (const int32_t *)(arena + o_pm);
+  d.pair_sim_off = (const int64_t *)(arena + o_psim);
+  UploadGate gate{(const int32_t *)(arena + o_ready), nullptr, ev_all, join_uploader};
+  gate.n_sentences = S;
+  gate.n_tokens = T;
+  gate.n_pieces = nt;
+  gate.piece_start = (const int64_t *)(arena + o_tcut);
+  {
+    int64_t t = 0;
+    for (int64_t p = 0; p < P; ++p) {
+      const int32_t n = h->pair_n[p], m = h->pair_m[p];
+      if (n > kPairMax || m > kPairMax)
+        for (int32_t i0 = 0; i0 < n; i0 += kPairMax)
+          for (int32_t j0 = 0; j0 < m; j0 += kPairMax) {
+            tiles_pre[3 * t] = p;
+            tiles_pre[3 * t + 1] = i0;
+            tiles_pre[3 * t + 2] = j0;
+            ++t;
+          }
+    }
+    if (n_tiles_pre) e = cudaMemcpyAsync(arena + o_tiles, tiles_pre, 8 * 3 * n_tiles_pre, cudaMemcpyHostToDevice, st);
+    const cudaError_t e1 = phase1_done.get();  // the uploader has enqueued the offsets scan
+    e = e ? e : e1;
+    e = e ? e : cudaStreamWaitEvent(st, ev_scan, 0);
+    if (e != cudaSuccess) return abort_with(BIMINE_E_CUDA, std::string("bimine_mine_host: ") + cudaGetErrorString(e));
+    const int rc0 = launch_pair_kernel(dict, model, &d, (const int64_t *)(arena + o_tiles), n_tiles_pre, cells,
+                                       (double *)(arena + o_sim), st, nullptr, &gate);
+    if (rc0 != BIMINE_OK) {
+      const std::string msg = g_error;
+      return abort_with(rc0, msg);
+    }
+    gate.pair_launched = true;
+  }
   // ---- per chunk of pairs, on host threads: validity, each pair's counter
   //      value, the chunk's plan (a view: pair arrays from p0, sentence arrays whole)
   struct ChunkInfo {
@@ -1394,10 +1492,10 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     if (ci[k].rc != BIMINE_OK) return abort_with(ci[k].rc, ci[k].err);
   bool packed = true;
   for (int k = 0; k < nc; ++k) packed = packed && ci[k].packed;
-  e = phase1_done.get();  // the uploader has enqueued the offsets scan
-  e = e ? e : cudaStreamWaitEvent(st, ev_scan, 0);
-  if (!packed && e == cudaSuccess)  // the caller's own layout: overwrite the rebuilt offsets
+  if (!packed) {  // the caller's own layout: overwrite the rebuilt offsets and score again
     e = cudaMemcpyAsync(arena + o_soff, h->sent_tok_off, 8 * S, cudaMemcpyHostToDevice, st);
+    gate.pair_launched = false;
+  }
   if (e != cudaSuccess) return abort_with(BIMINE_E_CUDA, std::string("bimine_mine_host: ") + cudaGetErrorString(e));
 #ifdef BIMINE_E2E_PROFILE
   h_an = hclock() - h0;
@@ -1439,28 +1537,10 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     }
   }
   e = cudaMemcpyAsync(arena + o_work, work, 8 * plan.work_len, cudaMemcpyHostToDevice, st);
-  e = e ? e : cudaMemcpyAsync(arena + o_need, need, 4 * P, cudaMemcpyHostToDevice, st);
   int rc = BIMINE_OK;
   if (e == cudaSuccess) {
-    bimine_batch d;
-    d.n_pairs = P;
-    d.n_sentences = S;
-    d.n_tokens = T;
-    d.tokens = (const int32_t *)(arena + o_tok);
-    d.token_bytes = tb;
-    d.sent_tok_off = (const int64_t *)(arena + o_soff);
-    d.sent_len = (const int32_t *)(arena + o_slen);
-    d.sent_uniq = (const int32_t *)(arena + o_suniq);
-    d.sent_chars = (const int32_t *)(arena + o_schar);
-    d.pair_src = (const int64_t *)(arena + o_psrc);
-    d.pair_n = (const int32_t *)(arena + o_pn);
-    d.pair_tgt = (const int64_t *)(arena + o_ptgt);
-    d.pair_m = (const int32_t *)(arena + o_pm);
-    d.pair_sim_off = (const int64_t *)(arena + o_psim);
     plan.work = (const int64_t *)(arena + o_work);
     plan.work_host = work;
-    const UploadGate gate{(const int32_t *)(arena + o_ready), (const int32_t *)(arena + o_need), ev_all,
-                          join_uploader};
     tl_gate = &gate;
     rc = bimine_mine_batch(dict, model, &d, &plan, gap, threshold, mismatch, bonus, (double *)(arena + o_sim),
                            (const int64_t *)(arena + o_outoff), (bimine_match *)(arena + o_slots),

@@ -75,7 +75,26 @@ struct PairArgs {
   // *ready >= need[p] (the counter grows as pieces land); null: no wait
   const int32_t *ready;
   const int32_t *need;
+  unsigned long long *next_item;  // the persistent CTAs' work counter (zeroed before the launch)
+  // need == null with ready set: the CTA derives its counter value itself
+  // (bimine_mine_host launches before the host has looked at the batch):
+  // once the pair and sentence arrays are in (ready >= 1) it bounds-checks
+  // its pair against these sizes -- skipping it if out of range, the host
+  // reports the error -- and waits for the piece of its last token; token
+  // piece k covers [piece_start[k], piece_start[k + 1]), k < n_pieces
+  int64_t n_sentences, n_tokens;
+  int32_t n_pieces;
+  const int64_t *piece_start;
 };
+
+__device__ __forceinline__ void wait_ready(const int32_t *ready, int want) {
+  while (true) {
+    int r;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(r) : "l"(ready) : "memory");
+    if (r >= want) break;
+    __nanosleep(256);
+  }
+}
 
 constexpr int kSegItems = 96;   // dictionary entries examined per warp segment
 
@@ -90,6 +109,7 @@ struct PairSmem {
   int64_t src_off[64], tgt_off[64];
   int32_t src_len[64], src_uniq[64], src_chars[64];
   int32_t tgt_len[64], tgt_uniq[64], tgt_chars[64];
+  unsigned long long te_max;          // self-gated launch: the block's largest token end
   int32_t misc[8];                    // 0 dense-id counter, 1 chunk end, 2 D claims, 3 C claims
   uint8_t src_order[64];              // source sentences, longest first (phase D claim order)
   uint8_t covt[64 * 64];
@@ -203,38 +223,35 @@ __host__ __device__ inline bool pair_is_small(int n, int m, int max_len) {
   return n <= kPairMax && m <= kPairMax && max_len <= kPairMaxLen;
 }
 
+// One work item of the score kernel: items [0, n_tiles) are the 64x64
+// tiles of large pairs (first, so the long pairs start early), the rest one
+// pair each (pairs larger than 64x64 are skipped there: their tiles cover
+// them).  Every exit is CTA-uniform.
 // kFeatures: also write the six features per cell (bimine_features_batch);
 // kPacked: the batch's token ids are in the 24-bit form
 template <bool kFeatures, bool kPacked>
-__global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  PairSmem &S = *reinterpret_cast<PairSmem *>(smem_raw);
-  // CTAs [0, n_tiles) take the 64x64 tiles of large pairs (first, so the
-  // long pairs start early), the rest one pair each (pairs larger than
-  // 64x64 are skipped there: their tiles cover them)
+__device__ __forceinline__ void pair_item(const PairArgs &A, PairSmem &S, const int64_t item) {
   int64_t p;
   int i0 = 0, j0 = 0;
-  const bool is_tile = (int64_t)blockIdx.x < A.n_tiles;
+  const bool is_tile = item < A.n_tiles;
   if (is_tile) {
-    p = A.tiles[3 * (int64_t)blockIdx.x];
-    i0 = (int)A.tiles[3 * (int64_t)blockIdx.x + 1];
-    j0 = (int)A.tiles[3 * (int64_t)blockIdx.x + 2];
+    p = A.tiles[3 * item];
+    i0 = (int)A.tiles[3 * item + 1];
+    j0 = (int)A.tiles[3 * item + 2];
   } else {
-    p = (int64_t)blockIdx.x - A.n_tiles;
+    p = item - A.n_tiles;
   }
+  const bool self_gate = A.ready && !A.need;
   if (A.ready) {  // wait until the chunk holding this pair's data has landed
-    if (threadIdx.x == 0) {
-      const int want = A.need[p];
-      while (true) {
-        int r;
-        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(r) : "l"(A.ready) : "memory");
-        if (r >= want) break;
-        __nanosleep(256);
-      }
-    }
+    if (threadIdx.x == 0) wait_ready(A.ready, self_gate ? 1 : A.need[p]);
     __syncthreads();
   }
   const int Nfull = A.b.pair_n[p], Mfull = A.b.pair_m[p];
+  if (self_gate) {  // the pair's sentence ranges, before any of them is read
+    const int64_t ps = A.b.pair_src[p], pt = A.b.pair_tgt[p];
+    if (Nfull < 1 || Mfull < 1 || ps < 0 || pt < 0 || ps + Nfull > A.n_sentences || pt + Mfull > A.n_sentences)
+      return;
+  }
   if (!is_tile && (Nfull > kPairMax || Mfull > kPairMax)) return;
   // this CTA's block: source sentences [i0, i0 + N), target sentences [j0, j0 + M)
   const int N = min(kPairMax, Nfull - i0), M = min(kPairMax, Mfull - j0);
@@ -262,6 +279,30 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
     S.tgt_chars[j] = A.b.sent_chars[t_first + j];
   }
   __syncthreads();
+  if (self_gate) {  // every sentence non-empty and inside the tokens; the piece of the last token
+    int64_t te = 0;
+    bool bad = false;
+    if (tid < N || (tid >= 64 && tid - 64 < M)) {
+      const int64_t o = tid < N ? S.src_off[tid] : S.tgt_off[tid - 64];
+      const int l = tid < N ? S.src_len[tid] : S.tgt_len[tid - 64];
+      bad = l < 1 || o < 0 || o + l > A.n_tokens;
+      te = o + l;
+    }
+    if (__syncthreads_or(bad)) return;
+    // the block's largest end: warp maxima, then one shared maximum
+    for (int o = 16; o > 0; o >>= 1) te = max(te, (int64_t)__shfl_xor_sync(kFull, (long long)te, o));
+    if (tid == 0) S.te_max = 0ull;
+    __syncthreads();
+    if (lane == 0) atomicMax(&S.te_max, (unsigned long long)te);
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t x = (int64_t)S.te_max - 1;
+      int j = 0;  // the piece holding token x
+      while (j + 1 < A.n_pieces && A.piece_start[j + 1] <= x) ++j;
+      wait_ready(A.ready, j + 2);
+    }
+    __syncthreads();
+  }
   {  // the rule of pair_is_small: every sentence <= kPairMaxLen tokens
     const int l = tid < N ? S.src_len[tid] : (tid >= 64 && tid - 64 < M) ? S.tgt_len[tid - 64] : 0;
     if (__syncthreads_or(l > kPairMaxLen)) return;
@@ -695,6 +736,26 @@ __global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A)
       j -= M;
       ++i;
     }
+  }
+}
+
+// Persistent CTAs (as many as are resident at once) take the items in order
+// from a counter, so a CTA that finishes moves straight to the next item
+// whose data has landed (bimine_mine_host's gated uploads), with no wave of
+// newly dispatched CTAs waiting behind a piece still in flight.
+template <bool kFeatures, bool kPacked>
+__global__ void __launch_bounds__(kPairThreads, 4) pair_kernel(const PairArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PairSmem &S = *reinterpret_cast<PairSmem *>(smem_raw);
+  __shared__ int64_t s_item;
+  const int64_t n_items = A.n_tiles + A.b.n_pairs;
+  while (true) {
+    if (threadIdx.x == 0) s_item = (int64_t)atomicAdd(A.next_item, 1ull);
+    __syncthreads();
+    const int64_t item = s_item;
+    if (item >= n_items) break;
+    pair_item<kFeatures, kPacked>(A, S, item);
+    __syncthreads();  // the item's shared-memory state is dead before the next one starts
   }
 }
 
