@@ -252,10 +252,14 @@ int bimine_agreement_batch(const bimine_match *matches_dev,
  *   matches_host[capacity]      compacted matches in pair order
  *   capacity >= sum over pairs of min(N, M)
  *   sim_host (optional, may be NULL): the score matrices.
- * Host buffers are read while the call runs (page-locked ones let the
- * uploads overlap the scoring).  sent_tok_off is rebuilt on the device as
- * the exclusive sum of sent_len and uploaded only when the caller's
- * offsets differ from that packed layout. */
+ * Host buffers are read while the call runs; pageable ones are staged
+ * through page-locked memory by the library.  The scoring starts before
+ * the call has validated the batch and overlaps the uploads (each score
+ * CTA bounds-checks its pair and waits for its data); an invalid batch is
+ * still reported with the usual error and no results.  sent_tok_off is
+ * rebuilt on the device as the exclusive sum of sent_len; when the
+ * caller's offsets differ from that packed layout they are uploaded and
+ * the scores computed again. */
 int bimine_mine_host(const bimine_dict *dict, const double *model,
                      const bimine_batch *batch_host, double gap,
                      double threshold, double mismatch, double bonus,
