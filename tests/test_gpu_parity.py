@@ -462,6 +462,44 @@ def test_mine_host_unpacked_sentence_offsets(layout):
     assert bits_equal(got[2], want[2])
 
 
+@pytest.mark.parametrize("fault", ["src_past_end", "tgt_negative", "empty_sentence", "tokens_past_end",
+                                   "negative_sim_off"])
+def test_mine_host_rejects_invalid_batches(fault):
+    """bimine_mine_host launches the score kernel before it has validated
+    the batch (each CTA bounds-checks its own pair): an invalid batch still
+    gets the host's error, nothing is read or written out of range (the
+    device stays usable), and the next valid call mines as before."""
+    import dataclasses
+
+    from paper_1512_01641_b200._native import BimineError
+
+    corpus = synth.make_config(2, n_pairs=64)
+    d = corpus.dictionary
+    model = model_vector(H.synth_model())
+    dd = E.LexiconContext(vocab=None, coo=(d.src, d.tgt, d.prob), devices={}).on(E.current_device())
+    b = corpus.batch
+    want = E.mine_host(dd, model, b, 2.0, 0.5, -1.0, 1.0, want_sim=True)
+    f = {k: np.array(getattr(b, k), copy=True) for k in ("pair_src", "pair_tgt", "sent_len", "pair_sim_off")}
+    k = 37  # a pair in the middle
+    if fault == "src_past_end":
+        f["pair_src"][k] = b.n_sentences - 1
+    elif fault == "tgt_negative":
+        f["pair_tgt"][k] = -5
+    elif fault == "empty_sentence":
+        f["sent_len"][int(b.pair_tgt[k]) + 1] = 0
+    elif fault == "tokens_past_end":
+        f["sent_len"][b.n_sentences - 1] += 1000  # the last sentence runs past the token array
+    else:
+        f["pair_sim_off"][k] = -1
+    bad = dataclasses.replace(b, **f)
+    with pytest.raises(BimineError):
+        E.mine_host(dd, model, bad, 2.0, 0.5, -1.0, 1.0, want_sim=True)
+    got = E.mine_host(dd, model, b, 2.0, 0.5, -1.0, 1.0, want_sim=True)
+    assert np.array_equal(got[0], want[0])
+    assert np.array_equal(got[1].view(np.uint8), want[1].view(np.uint8))
+    assert bits_equal(got[2], want[2])
+
+
 @pytest.mark.parametrize("chunks", ["3", "7"])
 def test_mine_host_chunked_uploads(chunks):
     """bimine_mine_host with the batch uploaded in chunks (the score kernel
