@@ -463,7 +463,7 @@ def pinned_batch(R, batch):
     for f in ("tokens", "sent_tok_off", "sent_len", "sent_uniq", "sent_chars", "pair_src", "pair_n",
               "pair_tgt", "pair_m", "pair_sim_off"):
         pinned[f] = R.torch.from_numpy(np.ascontiguousarray(getattr(batch, f))).pin_memory().numpy()
-    return PackedBatch(**pinned, token_bytes=batch.token_bytes)
+    return PackedBatch(**pinned, token_bytes=batch.token_bytes, sent_bytes=batch.sent_bytes)
 
 
 def time_e2e(R, dd, model, batch, steps, warmup, stream, gap, thr, mism, bonus):
@@ -583,9 +583,11 @@ def run_gpu(args):
     e2e_pg = e2e_32 = 0.0
     h2d_32 = 0
     if not args.no_e2e:
-        # the headline e2e uploads the compact wire form (24-bit ids) when the
-        # vocabulary allows it; int32 ids and pageable inputs beside it
+        # the headline e2e uploads the compact wire form (24-bit ids, uint16
+        # sentence arrays) when the values allow it; int32 arrays and
+        # pageable inputs beside it
         wire = batch.with_24bit_tokens() if int(batch.tokens.max(initial=0)) < (1 << 24) else batch
+        wire = wire.with_narrow_sentences()
         e2e_s, e2e_steps, h2d, d2h = time_e2e(R, dd, model, wire, K, args.warmup, stream, gap, thr, mism, bonus)
         if wire is not batch:
             e2e_32, _, h2d_32, _ = time_e2e(R, dd, model, batch, K, args.warmup, stream, gap, thr, mism, bonus)
@@ -611,13 +613,14 @@ def run_gpu(args):
             "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h,
             "steps": e2e_steps,
-            "path": "bimine_mine_host (C ABI): pinned host inputs (token ids in the 24-bit wire form, "
-                    "bimine_batch.token_bytes = 3), results copied into reused page-locked host output buffers"
+            "path": "bimine_mine_host (C ABI): pinned host inputs in the compact wire form (24-bit token ids, "
+                    "bimine_batch.token_bytes = 3; uint16 sentence lengths / distinct counts / characters, "
+                    "sent_bytes = 2), results copied into reused page-locked host output buffers"
                     + ("; per rank: the shared base sentences + its pair descriptors" if strong else ""),
         }
         if e2e_32:
             e2e["int32_tokens"] = {"value": pairs_all * e2e_steps / max(cols[9]), "h2d_bytes_per_step": h2d_32,
-                                   "path": "the same call with int32 token ids"}
+                                   "path": "the same call with int32 token ids and int32 sentence arrays"}
         if e2e_pg:
             e2e["pageable_inputs"] = {"value": pairs_all * e2e_steps / max(cols[8]),
                                       "path": "bimine_mine_host on the generator's pageable numpy arrays (staged "

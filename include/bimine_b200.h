@@ -75,6 +75,11 @@ typedef struct bimine_batch {
   const int64_t *pair_sim_off; /* [n_pairs] offset of the row-major N x M block   */
   int32_t token_bytes;         /* 4 (or 0): int32 ids; 3: packed 24-bit ids (the
                                   upload of bimine_mine_host shrinks by a quarter) */
+  int32_t sent_bytes;          /* 4 (or 0): sent_len / sent_uniq / sent_chars are
+                                  int32; 2: uint16 (every value < 65536).  The
+                                  narrow form is accepted by bimine_mine_host
+                                  only (its sentence upload halves); the other
+                                  entry points refuse it with BIMINE_E_ARG      */
 } bimine_batch;
 
 /* Bilingual dictionary in CSR form over source ids (Lexicon,

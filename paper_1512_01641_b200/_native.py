@@ -55,6 +55,7 @@ class CBatch(ctypes.Structure):
         ("pair_m", _vp),
         ("pair_sim_off", _vp),
         ("token_bytes", ctypes.c_int32),
+        ("sent_bytes", ctypes.c_int32),
     ]
 
 
@@ -175,6 +176,7 @@ def batch_struct_host(b) -> CBatch:
         b.tokens.ctypes.data, b.sent_tok_off.ctypes.data, b.sent_len.ctypes.data, b.sent_uniq.ctypes.data,
         b.sent_chars.ctypes.data, b.pair_src.ctypes.data, b.pair_n.ctypes.data, b.pair_tgt.ctypes.data,
         b.pair_m.ctypes.data, b.pair_sim_off.ctypes.data, getattr(b, "token_bytes", 4),
+        getattr(b, "sent_bytes", 4),
     )
 
 
@@ -184,5 +186,5 @@ def batch_struct_device(t: dict, n_pairs: int, n_sentences: int, n_tokens: int, 
         n_pairs, n_sentences, n_tokens,
         t["tokens"].data_ptr(), t["sent_tok_off"].data_ptr(), t["sent_len"].data_ptr(), t["sent_uniq"].data_ptr(),
         t["sent_chars"].data_ptr(), t["pair_src"].data_ptr(), t["pair_n"].data_ptr(), t["pair_tgt"].data_ptr(),
-        t["pair_m"].data_ptr(), t["pair_sim_off"].data_ptr(), token_bytes,
+        t["pair_m"].data_ptr(), t["pair_sim_off"].data_ptr(), token_bytes, 4,
     )

@@ -148,6 +148,9 @@ bool is_pageable(const void *p) {
   return a.type == cudaMemoryTypeUnregistered;
 }
 
+const char *const kNarrowOnlyHost =
+    "uint16 sentence arrays (bimine_batch.sent_bytes = 2) are accepted by bimine_mine_host only";
+
 // memcpy into page-locked staging with streaming (non-temporal) stores: the
 // destination is only read again by the DMA engine, so its lines need not
 // be fetched first (a cached store reads each line before writing it; glibc
@@ -389,6 +392,69 @@ struct bimine_dict {
   DictEntry *ent = nullptr;     //                      {p, t} per entry
 };
 
+// bimine_plan_batch over sentence arrays of either width (T = int32_t, or
+// uint16_t for bimine_mine_host's narrow form)
+template <class T>
+int plan_batch_t(const bimine_batch *b, const T *sent_len, const T *sent_uniq, int64_t *work, int64_t work_cap,
+                 bimine_plan *plan) {
+  bimine_plan P;
+  memset(&P, 0, sizeof(P));
+  // maxima over the sentences the pairs reference (a view of a larger batch
+  // plans in time proportional to its own pairs)
+  std::vector<int64_t> longs, larges;
+  int64_t t = 0;
+  for (int64_t p = 0; p < b->n_pairs; ++p)
+    P.n_cells = std::max(P.n_cells, b->pair_sim_off[p] + (int64_t)b->pair_n[p] * b->pair_m[p]);
+  for (int64_t p = 0; p < b->n_pairs; ++p) {
+    const int32_t n = b->pair_n[p], m = b->pair_m[p];
+    if (n < 1 || m < 1) return fail(BIMINE_E_ARG, "bimine_plan_batch: empty document");
+    P.max_n = std::max(P.max_n, n);
+    P.max_m = std::max(P.max_m, m);
+    int32_t ml = 0, mu = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      ml = std::max(ml, (int32_t)sent_len[b->pair_src[p] + i]);
+      mu = std::max(mu, (int32_t)sent_uniq[b->pair_src[p] + i]);
+    }
+    for (int32_t j = 0; j < m; ++j) {
+      ml = std::max(ml, (int32_t)sent_len[b->pair_tgt[p] + j]);
+      mu = std::max(mu, (int32_t)sent_uniq[b->pair_tgt[p] + j]);
+    }
+    P.max_len = std::max(P.max_len, ml);
+    P.max_uniq = std::max(P.max_uniq, mu);
+    if (n > kPairMax || m > kPairMax) larges.push_back(p);  // NW: cluster kernel
+    if (ml > kPairMaxLen) {
+      longs.push_back(p);
+      P.long_max_n = std::max(P.long_max_n, n);
+      P.long_max_m = std::max(P.long_max_m, m);
+    } else if (n > kPairMax || m > kPairMax) {
+      for (int32_t i0 = 0; i0 < n; i0 += kPairMax)
+        for (int32_t j0 = 0; j0 < m; j0 += kPairMax) {
+          if (3 * t + 3 <= work_cap) {
+            work[3 * t] = p;
+            work[3 * t + 1] = i0;
+            work[3 * t + 2] = j0;
+          }
+          ++t;
+        }
+    }
+  }
+  P.n_tiles = t;
+  P.n_long = (int64_t)longs.size();
+  P.n_large = (int64_t)larges.size();
+  P.work_len = 3 * P.n_tiles + P.n_long + 3 * P.n_large;
+  *plan = P;
+  if (P.work_len > work_cap) return fail(BIMINE_E_ARG, "bimine_plan_batch: work_cap < plan->work_len");
+  for (int64_t k = 0; k < P.n_long; ++k) work[3 * P.n_tiles + k] = longs[k];
+  int64_t *lw = work + 3 * P.n_tiles + P.n_long;
+  for (int64_t k = 0; k < P.n_large; ++k) {
+    lw[k] = larges[k];
+    lw[P.n_large + 2 * k] = b->pair_n[larges[k]];
+    lw[P.n_large + 2 * k + 1] = b->pair_m[larges[k]];
+  }
+  return BIMINE_OK;
+}
+
+
 extern "C" {
 
 const char *bimine_last_error(void) { return g_error.c_str(); }
@@ -504,61 +570,8 @@ int64_t bimine_dict_entries(const bimine_dict *d) { return d ? d->n_entries : -1
 
 int bimine_plan_batch(const bimine_batch *b, int64_t *work, int64_t work_cap, bimine_plan *plan) {
   if (!b || !plan || (work_cap > 0 && !work)) return fail(BIMINE_E_ARG, "bimine_plan_batch: null argument");
-  bimine_plan P;
-  memset(&P, 0, sizeof(P));
-  // maxima over the sentences the pairs reference (a view of a larger batch
-  // plans in time proportional to its own pairs)
-  std::vector<int64_t> longs, larges;
-  int64_t t = 0;
-  for (int64_t p = 0; p < b->n_pairs; ++p)
-    P.n_cells = std::max(P.n_cells, b->pair_sim_off[p] + (int64_t)b->pair_n[p] * b->pair_m[p]);
-  for (int64_t p = 0; p < b->n_pairs; ++p) {
-    const int32_t n = b->pair_n[p], m = b->pair_m[p];
-    if (n < 1 || m < 1) return fail(BIMINE_E_ARG, "bimine_plan_batch: empty document");
-    P.max_n = std::max(P.max_n, n);
-    P.max_m = std::max(P.max_m, m);
-    int32_t ml = 0, mu = 0;
-    for (int32_t i = 0; i < n; ++i) {
-      ml = std::max(ml, b->sent_len[b->pair_src[p] + i]);
-      mu = std::max(mu, b->sent_uniq[b->pair_src[p] + i]);
-    }
-    for (int32_t j = 0; j < m; ++j) {
-      ml = std::max(ml, b->sent_len[b->pair_tgt[p] + j]);
-      mu = std::max(mu, b->sent_uniq[b->pair_tgt[p] + j]);
-    }
-    P.max_len = std::max(P.max_len, ml);
-    P.max_uniq = std::max(P.max_uniq, mu);
-    if (n > kPairMax || m > kPairMax) larges.push_back(p);  // NW: cluster kernel
-    if (ml > kPairMaxLen) {
-      longs.push_back(p);
-      P.long_max_n = std::max(P.long_max_n, n);
-      P.long_max_m = std::max(P.long_max_m, m);
-    } else if (n > kPairMax || m > kPairMax) {
-      for (int32_t i0 = 0; i0 < n; i0 += kPairMax)
-        for (int32_t j0 = 0; j0 < m; j0 += kPairMax) {
-          if (3 * t + 3 <= work_cap) {
-            work[3 * t] = p;
-            work[3 * t + 1] = i0;
-            work[3 * t + 2] = j0;
-          }
-          ++t;
-        }
-    }
-  }
-  P.n_tiles = t;
-  P.n_long = (int64_t)longs.size();
-  P.n_large = (int64_t)larges.size();
-  P.work_len = 3 * P.n_tiles + P.n_long + 3 * P.n_large;
-  *plan = P;
-  if (P.work_len > work_cap) return fail(BIMINE_E_ARG, "bimine_plan_batch: work_cap < plan->work_len");
-  for (int64_t k = 0; k < P.n_long; ++k) work[3 * P.n_tiles + k] = longs[k];
-  int64_t *lw = work + 3 * P.n_tiles + P.n_long;
-  for (int64_t k = 0; k < P.n_large; ++k) {
-    lw[k] = larges[k];
-    lw[P.n_large + 2 * k] = b->pair_n[larges[k]];
-    lw[P.n_large + 2 * k + 1] = b->pair_m[larges[k]];
-  }
-  return BIMINE_OK;
+  if (b->sent_bytes == 2) return fail(BIMINE_E_ARG, kNarrowOnlyHost);
+  return plan_batch_t<int32_t>(b, b->sent_len, b->sent_uniq, work, work_cap, plan);
 }
 
 }  // extern "C"
@@ -609,6 +622,16 @@ extern "C" {
 }  // extern "C"
 
 namespace {
+
+// uint16 sentence arrays (bimine_mine_host's narrow upload) -> the int32
+// arrays every kernel reads: src holds len | uniq | chars, n each
+__global__ void widen_u16_kernel(const uint16_t *__restrict__ src, int64_t n, int32_t *__restrict__ len,
+                                 int32_t *__restrict__ uniq, int32_t *__restrict__ chars) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < 3 * n; k += (int64_t)gridDim.x * blockDim.x) {
+    int32_t *dst = k < n ? len : k < 2 * n ? uniq : chars;
+    dst[k - (k < n ? 0 : k < 2 * n ? n : 2 * n)] = (int32_t)src[k];
+  }
+}
 
 // One launch of the pair kernel: the tiles of pairs larger than 64x64, then
 // one item per pair, over persistent CTAs.  gate: the upload gate of
@@ -668,6 +691,7 @@ int launch_pair_kernel(const bimine_dict *dict, const double *model, const bimin
 int launch_scores(const bimine_dict *dict, const double *model, const bimine_batch *b, const bimine_plan *plan,
                   double *sim_dev, cudaStream_t st, double *features = nullptr) {
   if (!dict || !model || !b || !plan || !sim_dev) return fail(BIMINE_E_ARG, "bimine_score_batch: null argument");
+  if (b->sent_bytes == 2) return fail(BIMINE_E_ARG, kNarrowOnlyHost);
   if (b->n_pairs == 0) return BIMINE_OK;
   if (plan->max_n < 1 || plan->max_m < 1 || plan->max_uniq < 1 || plan->max_len < 1)
     return fail(BIMINE_E_ARG, "bimine_score_batch: empty document or sentence");
@@ -1163,7 +1187,7 @@ cudaError_t preload_kernels(cudaStream_t st) {
       (const void *)nw_big_kernel<kNwTable, kBigW>, (const void *)nw_big_traceback_kernel<kNwMine>,
       (const void *)nw_big_traceback_kernel<kNwSteps>, (const void *)nw_big_traceback_kernel<kNwTable>,
       (const void *)nw_diag_kernel, (const void *)uniform_offsets_kernel, (const void *)scan_counts_kernel,
-      (const void *)gather_matches_kernel, (const void *)agree_kernel};
+      (const void *)gather_matches_kernel, (const void *)agree_kernel, (const void *)widen_u16_kernel};
   cudaFuncAttributes fa;
   for (const void *f : fns) {
     const cudaError_t e = cudaFuncGetAttributes(&fa, f);  // loads the kernel
@@ -1190,6 +1214,9 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   const int64_t P = h->n_pairs, S = h->n_sentences, T = h->n_tokens;
   *total_host = 0;
   if (P == 0) return BIMINE_OK;
+  if (h->sent_bytes != 0 && h->sent_bytes != 2 && h->sent_bytes != 4)
+    return fail(BIMINE_E_ARG, "bimine_mine_host: sent_bytes must be 2 or 4");
+  const bool narrow = h->sent_bytes == 2;  // uint16 sentence arrays: half the upload, widened on the device
   pool_setup();
   cudaStream_t st = as_stream(stream);
   BIMINE_CUDA(preload_kernels(st));
@@ -1276,6 +1303,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   // sent_tok_off is not uploaded: the copy stream rebuilds it from sent_len
   // (the usual packed layout); the analysis threads check that the caller's
   // offsets are exactly that, else they are uploaded on `st` before scoring
+  const size_t o_s16 = carve(narrow ? 6 * (size_t)S : 1);  // the narrow arrays as uploaded: len | uniq | chars
   size_t scan_bytes = 0;
   BIMINE_CUDA(offsets_from_lengths(nullptr, nullptr, S, nullptr, &scan_bytes, st));
   const size_t o_scan = carve(std::max<size_t>(scan_bytes, 1));
@@ -1324,9 +1352,21 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     H2D(o_pm, h->pair_m, 4 * P, pg_pairs);
     H2D(o_psim, h->pair_sim_off, 8 * P, pg_pairs);
     H2D(o_outoff, out_off, 8 * P, false);
-    H2D(o_slen, h->sent_len, 4 * S, pg_sent);
-    H2D(o_suniq, h->sent_uniq, 4 * S, pg_sent);
-    H2D(o_schar, h->sent_chars, 4 * S, pg_sent);
+    if (narrow) {
+      H2D(o_s16, h->sent_len, 2 * S, pg_sent);
+      H2D(o_s16 + 2 * S, h->sent_uniq, 2 * S, pg_sent);
+      H2D(o_s16 + 4 * S, h->sent_chars, 2 * S, pg_sent);
+      if (ue == cudaSuccess && S > 0) {
+        widen_u16_kernel<<<(unsigned)std::min<int64_t>((3 * S + 255) / 256, 4096), 256, 0, cs>>>(
+            (const uint16_t *)(arena + o_s16), S, (int32_t *)(arena + o_slen), (int32_t *)(arena + o_suniq),
+            (int32_t *)(arena + o_schar));
+        ue = cudaGetLastError();
+      }
+    } else {
+      H2D(o_slen, h->sent_len, 4 * S, pg_sent);
+      H2D(o_suniq, h->sent_uniq, 4 * S, pg_sent);
+      H2D(o_schar, h->sent_chars, 4 * S, pg_sent);
+    }
     H2D(o_tcut, tcut_pinned, 8 * (size_t)(nt + 1), false);
     if (ue == cudaSuccess)
       ue = offsets_from_lengths((const int32_t *)(arena + o_slen), (int64_t *)(arena + o_soff), S, arena + o_scan,
@@ -1386,6 +1426,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   d.pair_tgt = (const int64_t *)(arena + o_ptgt);
   d.pair_m = (const int32_t *)(arena + o_pm);
   d.pair_sim_off = (const int64_t *)(arena + o_psim);
+  d.sent_bytes = 4;  // (widened on the device)
   UploadGate gate{(const int32_t *)(arena + o_ready), nullptr, ev_all, join_uploader};
   gate.n_sentences = S;
   gate.n_tokens = T;
@@ -1427,14 +1468,16 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     bool packed = true;  // sentences [S k / nc, S (k+1) / nc) are at the rebuilt offsets
   };
   std::vector<ChunkInfo> ci(nc);
+  // the host's own reads of the sentence arrays, in whichever width they are
+  const uint16_t *const n_len = (const uint16_t *)h->sent_len, *const n_uniq = (const uint16_t *)h->sent_uniq;
+  auto sent_len_at = [&](int64_t x) -> int32_t { return narrow ? (int32_t)n_len[x] : h->sent_len[x]; };
   auto analyse = [&](int k) {
     ChunkInfo &c = ci[k];
     {
       const int64_t s0 = S * k / nc, s1 = S * (k + 1) / nc;
       const int64_t *so = h->sent_tok_off;
-      const int32_t *sl = h->sent_len;
       bool ok = s0 > 0 || S == 0 || so[0] == 0;
-      for (int64_t x = s0; ok && x + 1 < s1 + (s1 < S ? 1 : 0); ++x) ok = so[x + 1] == so[x] + sl[x];
+      for (int64_t x = s0; ok && x + 1 < s1 + (s1 < S ? 1 : 0); ++x) ok = so[x + 1] == so[x] + sent_len_at(x);
       c.packed = ok;
     }
     const int64_t p0 = cut[k], p1 = cut[k + 1];
@@ -1452,7 +1495,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
           return;
         }
         for (int32_t q = 0; q < cnt; ++q) {
-          const int32_t len = h->sent_len[s0 + q];
+          const int32_t len = sent_len_at(s0 + q);
           if (len < 1) {
             c.rc = BIMINE_E_ARG;
             c.err = "bimine_mine_host: empty sentence";
@@ -1479,7 +1522,8 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     hv.pair_m = h->pair_m + p0;
     hv.pair_sim_off = h->pair_sim_off + p0;
     c.work.resize(std::max<int64_t>(wcap, 1));
-    c.rc = bimine_plan_batch(&hv, c.work.data(), wcap, &c.plan);
+    c.rc = narrow ? plan_batch_t<uint16_t>(&hv, n_len, n_uniq, c.work.data(), wcap, &c.plan)
+                  : plan_batch_t<int32_t>(&hv, h->sent_len, h->sent_uniq, c.work.data(), wcap, &c.plan);
     if (c.rc != BIMINE_OK) c.err = g_error;  // this thread's message
   };
   {

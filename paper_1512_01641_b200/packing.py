@@ -213,6 +213,7 @@ class PackedBatch:
     pair_m: np.ndarray  # int32 [P]
     pair_sim_off: np.ndarray  # int64 [P]
     token_bytes: int = 4  # 3: the compact wire form of the ids (with_24bit_tokens)
+    sent_bytes: int = 4  # 2: sent_len / sent_uniq / sent_chars as uint16 (with_narrow_sentences)
 
     @property
     def n_pairs(self) -> int:
@@ -229,6 +230,19 @@ class PackedBatch:
             raise ValueError("token ids outside [0, 2^24) need the int32 form")
         packed = np.ascontiguousarray(t.view(np.uint8).reshape(-1, 4)[:, :3]).reshape(-1)
         return dataclasses.replace(self, tokens=packed, token_bytes=3)
+
+    def with_narrow_sentences(self) -> "PackedBatch":
+        """The same batch with sent_len, sent_uniq and sent_chars as uint16
+        (every value below 2^16; otherwise the batch is returned as is):
+        the form whose sentence arrays bimine_mine_host uploads in half the
+        time.  For bimine_mine_host only; other consumers want int32."""
+        if self.sent_bytes == 2:
+            return self
+        arrs = (self.sent_len, self.sent_uniq, self.sent_chars)
+        if any(a.size and (int(a.min()) < 0 or int(a.max()) >= 1 << 16) for a in arrs):
+            return self
+        narrow = [np.ascontiguousarray(a, dtype=np.uint16) for a in arrs]
+        return dataclasses.replace(self, sent_len=narrow[0], sent_uniq=narrow[1], sent_chars=narrow[2], sent_bytes=2)
 
     def int32_tokens(self) -> np.ndarray:
         """The ids as int32 whatever the stored form."""

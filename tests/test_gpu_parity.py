@@ -500,6 +500,34 @@ def test_mine_host_rejects_invalid_batches(fault):
     assert bits_equal(got[2], want[2])
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+def test_mine_host_narrow_wire_form(pinned):
+    """bimine_mine_host with the compact wire form (24-bit token ids, uint16
+    sentence arrays widened on the device) mines bit for bit what the int32
+    form mines, from pinned and from pageable host arrays."""
+    import torch
+
+    from paper_1512_01641_b200.packing import PackedBatch
+
+    corpus = synth.make_config(2, n_pairs=300)
+    d = corpus.dictionary
+    model = model_vector(H.synth_model())
+    dd = E.LexiconContext(vocab=None, coo=(d.src, d.tgt, d.prob), devices={}).on(E.current_device())
+    b = corpus.batch
+    want = E.mine_host(dd, model, b, 2.0, 0.5, -1.0, 1.0, want_sim=True)
+    wire = b.with_24bit_tokens().with_narrow_sentences()
+    assert wire.sent_bytes == 2 and wire.token_bytes == 3
+    if pinned:
+        arrs = {f: torch.from_numpy(np.ascontiguousarray(getattr(wire, f))).pin_memory().numpy()
+                for f in ("tokens", "sent_tok_off", "sent_len", "sent_uniq", "sent_chars", "pair_src", "pair_n",
+                          "pair_tgt", "pair_m", "pair_sim_off")}
+        wire = PackedBatch(**arrs, token_bytes=3, sent_bytes=2)
+    got = E.mine_host(dd, model, wire, 2.0, 0.5, -1.0, 1.0, want_sim=True)
+    assert np.array_equal(got[0], want[0])
+    assert np.array_equal(got[1].view(np.uint8), want[1].view(np.uint8))
+    assert bits_equal(got[2], want[2])
+
+
 @pytest.mark.parametrize("chunks", ["3", "7"])
 def test_mine_host_chunked_uploads(chunks):
     """bimine_mine_host with the batch uploaded in chunks (the score kernel

@@ -317,6 +317,29 @@ def test_docs_view_matches_flat_view():
         assert not _pyhost().docs_view(odd, np.empty(4, np.int64), np.empty(4, np.int64), np.empty(5, np.int64))
 
 
+def test_narrow_sentence_form():
+    """PackedBatch.with_narrow_sentences: uint16 copies of the three sentence
+    arrays with bimine_batch.sent_bytes = 2 (values unchanged); a batch with
+    a value of 2^16 or more stays int32; the entry points other than
+    bimine_mine_host refuse the narrow form (bimine_plan_batch here)."""
+    from paper_1512_01641_b200 import _native as N
+    from paper_1512_01641_b200 import engine as E
+
+    _native_vocab()
+    b = synth.make_config(2, n_pairs=30).batch
+    nb = b.with_narrow_sentences()
+    assert nb.sent_bytes == 2 and nb.with_narrow_sentences() is nb
+    for f in ("sent_len", "sent_uniq", "sent_chars"):
+        assert getattr(nb, f).dtype == np.uint16
+        assert np.array_equal(getattr(nb, f).astype(np.int64), getattr(b, f).astype(np.int64))
+    assert N.batch_struct_host(nb).sent_bytes == 2 and N.batch_struct_host(b).sent_bytes == 4
+    wide = dataclasses.replace(b, sent_chars=b.sent_chars.copy())
+    wide.sent_chars[3] = 70000
+    assert wide.with_narrow_sentences() is wide
+    with pytest.raises(N.BimineError, match="sent_bytes = 2"):
+        E.plan_batch(nb)
+
+
 def test_utf8_offsets_edge_cases():
     """The UTF-8 packing behind bimine_tokenize_batch: bytes back to back and
     byte offsets, for ASCII, non-ASCII, empty strings, NULs and lone

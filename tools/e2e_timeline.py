@@ -1,6 +1,7 @@
 """bimine_mine_host's host/device timeline on C2 (run against a build with
 -DBIMINE_E2E_PROFILE, e.g. BIMINE_LIB=scratch_so/e2eprof.so): prints the
-library's per-call timeline line for a few calls, 24-bit and int32 ids.
+library's per-call timeline line for a few calls: the compact wire form
+(24-bit ids, uint16 sentence arrays), 24-bit ids only, int32.
 
     BIMINE_LIB=scratch_so/e2eprof.so python tools/e2e_timeline.py
 """
@@ -24,7 +25,8 @@ class _R:
 
 R = _R()
 R.torch = torch
-for name, b in (("24-bit", corpus.batch.with_24bit_tokens()), ("int32", corpus.batch)):
+for name, b in (("wire", corpus.batch.with_24bit_tokens().with_narrow_sentences()),
+                ("24-bit", corpus.batch.with_24bit_tokens()), ("int32", corpus.batch)):
     pb = bench.pinned_batch(R, b)
     out = {}
     for k in range(5):
