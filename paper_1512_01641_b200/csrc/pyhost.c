@@ -11,11 +11,13 @@
  *       caller then encodes the sentences to one UTF-8 buffer instead.  The
  *       caller keeps the list alive while the pointers are used.
  *
- *   docs_view(docs, ptrs, lens, prefix) -> bool
+ *   docs_view(docs, ptrs, lens, prefix, start) -> bool
  *       The same over a list of document pairs (source sentences, target
  *       sentences), each a tuple or list, each side a tuple or list of str:
  *       pair by pair, source then target sentences -- no flat list of
- *       10^6 sentences to build and free.  False also for any other shape.
+ *       10^6 sentences to build and free; pair d's first sentence is
+ *       start[d] (start[n_docs] = the total).  Ranges of pairs on up to 16
+ *       threads.  False also for any other shape or counts.
  *
  *   build_rows(matches, counts, pair, docs) -> list
  *       The mining rows (score, source sentence, target sentence) of
@@ -25,6 +27,7 @@
  */
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -92,10 +95,52 @@ static PyObject *str_view(PyObject *self, PyObject *args) {
   return PyBool_FromLong(ok);
 }
 
+/* docs_view's work on docs [d0, d1): sentence s of doc d is written at
+   start[d] + s.  Reads object memory only (no Python API calls), so the
+   ranges run on plain threads while the caller holds the list. */
+struct DocsRange {
+  PyObject **docs;
+  const int64_t *start;
+  Py_ssize_t d0, d1, cap;
+  int64_t *P, *L;
+  int ok;
+};
+
+static void *docs_range(void *arg) {
+  struct DocsRange *r = (struct DocsRange *)arg;
+  for (Py_ssize_t d = r->d0; r->ok && d < r->d1; ++d) {
+    Py_ssize_t two, s = r->start[d];
+    PyObject **side = seq_items(r->docs[d], &two);
+    if (!side || two != 2) {
+      r->ok = 0;
+      break;
+    }
+    for (int h = 0; r->ok && h < 2; ++h) {
+      Py_ssize_t m;
+      PyObject **it = seq_items(side[h], &m);
+      if (!it) {
+        r->ok = 0;
+        break;
+      }
+      for (Py_ssize_t k = 0; k < m; ++k, ++s) {
+        PyObject *o = it[k];
+        if (s >= r->start[d + 1] || s >= r->cap || !PyUnicode_CheckExact(o) || !PyUnicode_IS_COMPACT_ASCII(o)) {
+          r->ok = 0;
+          break;
+        }
+        r->P[s] = (int64_t)(intptr_t)PyUnicode_DATA(o);
+        r->L[s] = (int64_t)PyUnicode_GET_LENGTH(o);
+      }
+    }
+    if (r->ok && s != r->start[d + 1]) r->ok = 0;  /* the caller's counts disagree with the docs */
+  }
+  return NULL;
+}
+
 static PyObject *docs_view(PyObject *self, PyObject *args) {
-  PyObject *docs, *po, *lo, *xo;
-  if (!PyArg_ParseTuple(args, "O!OOO", &PyList_Type, &docs, &po, &lo, &xo)) return NULL;
-  Py_buffer bp, bl, bx;
+  PyObject *docs, *po, *lo, *xo, *so;
+  if (!PyArg_ParseTuple(args, "O!OOOO", &PyList_Type, &docs, &po, &lo, &xo, &so)) return NULL;
+  Py_buffer bp, bl, bx, bs;
   if (get_buf(po, &bp, 1, 8, "ptrs") < 0) return NULL;
   if (get_buf(lo, &bl, 1, 8, "lens") < 0) {
     PyBuffer_Release(&bp);
@@ -106,41 +151,51 @@ static PyObject *docs_view(PyObject *self, PyObject *args) {
     PyBuffer_Release(&bl);
     return NULL;
   }
-  const Py_ssize_t cap = bp.len / 8 < bl.len / 8 ? bp.len / 8 : bl.len / 8;
-  int64_t *P = (int64_t *)bp.buf, *L = (int64_t *)bl.buf, *X = (int64_t *)bx.buf;
-  Py_ssize_t s = 0;
-  int ok = bx.len >= 8;
-  if (ok) X[0] = 0;
+  if (get_buf(so, &bs, 0, 8, "start") < 0) {
+    PyBuffer_Release(&bp);
+    PyBuffer_Release(&bl);
+    PyBuffer_Release(&bx);
+    return NULL;
+  }
   const Py_ssize_t nd = PyList_GET_SIZE(docs);
-  for (Py_ssize_t d = 0; ok && d < nd; ++d) {
-    Py_ssize_t two;
-    PyObject **side = seq_items(PyList_GET_ITEM(docs, d), &two);
-    if (!side || two != 2) {
-      ok = 0;
-      break;
+  const int64_t *start = (const int64_t *)bs.buf;
+  int64_t *P = (int64_t *)bp.buf, *L = (int64_t *)bl.buf, *X = (int64_t *)bx.buf;
+  const Py_ssize_t cap = bp.len / 8 < bl.len / 8 ? bp.len / 8 : bl.len / 8;
+  int ok = bs.len / 8 == nd + 1 && start[0] == 0 && bx.len / 8 >= start[nd] + 1 && start[nd] <= cap;
+  if (ok && nd > 0) {
+    /* up to 16 ranges of >= 256 documents each */
+    int nt = (int)(nd / 256);
+    if (nt < 1) nt = 1;
+    if (nt > 16) nt = 16;
+    struct DocsRange r[16];
+    pthread_t th[16];
+    int started[16] = {0};
+    for (int t = 0; t < nt; ++t) {
+      r[t].docs = ((PyListObject *)docs)->ob_item;
+      r[t].start = start;
+      r[t].d0 = nd * t / nt;
+      r[t].d1 = nd * (t + 1) / nt;
+      r[t].cap = cap;
+      r[t].P = P;
+      r[t].L = L;
+      r[t].ok = 1;
     }
-    for (int h = 0; ok && h < 2; ++h) {
-      Py_ssize_t m;
-      PyObject **it = seq_items(side[h], &m);
-      if (!it) {
-        ok = 0;
-        break;
-      }
-      for (Py_ssize_t k = 0; k < m; ++k, ++s) {
-        PyObject *o = it[k];
-        if (s >= cap || 8 * (s + 2) > bx.len || !PyUnicode_CheckExact(o) || !PyUnicode_IS_COMPACT_ASCII(o)) {
-          ok = 0;
-          break;
-        }
-        P[s] = (int64_t)(intptr_t)PyUnicode_DATA(o);
-        L[s] = (int64_t)PyUnicode_GET_LENGTH(o);
-        X[s + 1] = X[s] + L[s];
-      }
+    for (int t = 1; t < nt; ++t) started[t] = pthread_create(&th[t], NULL, docs_range, &r[t]) == 0;
+    docs_range(&r[0]);
+    for (int t = 1; t < nt; ++t) {
+      if (started[t]) pthread_join(th[t], NULL);
+      else docs_range(&r[t]);
     }
+    for (int t = 0; t < nt; ++t) ok = ok && r[t].ok;
+  }
+  if (ok) {
+    X[0] = 0;
+    for (int64_t s = 0; s < start[nd]; ++s) X[s + 1] = X[s] + L[s];
   }
   PyBuffer_Release(&bp);
   PyBuffer_Release(&bl);
   PyBuffer_Release(&bx);
+  PyBuffer_Release(&bs);
   return PyBool_FromLong(ok);
 }
 

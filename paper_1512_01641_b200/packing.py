@@ -140,15 +140,16 @@ class NativeVocabulary:
         N.check(rc)
         return tokens[: int(nt[0])], lens[:n], uniq[:n], chars[:n]
 
-    def tokenize_docs(self, docs, n: int):
+    def tokenize_docs(self, docs, n: int, start: np.ndarray):
         """tokenize() of the n sentences of `docs`, a list of (source
-        sentences, target sentences), pair by pair, source first -- read in
+        sentences, target sentences), pair by pair, source first (pair d's
+        first sentence is start[d], start[-1] == n) -- read in
         place, without a flat list; None unless every pair is a tuple or
         list of two tuples or lists of compact ASCII str (the caller then
         flattens them for tokenize())."""
         ptrs, blen, prefix = (np.empty(max(n, 1), dtype=np.int64), np.empty(max(n, 1), dtype=np.int64),
                               np.empty(n + 1, dtype=np.int64))
-        if not (n and type(docs) is list and _pyhost().docs_view(docs, ptrs, blen, prefix)):
+        if not (n and type(docs) is list and _pyhost().docs_view(docs, ptrs, blen, prefix, start)):
             return None
         return self._in_place(n, ptrs, blen, prefix)
 
@@ -401,7 +402,7 @@ def pack_documents(vocab, pairs) -> PackedDocuments:
     start = np.zeros(P + 1, dtype=np.int64)
     np.cumsum(ns + nt, out=start[1:])
     S = int(start[P])
-    res = vocab.tokenize_docs(pairs, S) if getattr(vocab, "native", False) else None
+    res = vocab.tokenize_docs(pairs, S, start) if getattr(vocab, "native", False) else None
     if res is not None:
         tokens, lens, uniq, chars = res
     else:

@@ -311,10 +311,22 @@ def test_docs_view_matches_flat_view():
     n = len(flat)
     out = [np.empty(n, np.int64), np.empty(n, np.int64), np.empty(n + 1, np.int64)]
     ref = [np.empty(n, np.int64), np.empty(n, np.int64), np.empty(n + 1, np.int64)]
-    assert _pyhost().docs_view(docs, *out) and _pyhost().str_view(flat, *ref)
+    start = np.array([0, 4, 8], np.int64)
+    assert _pyhost().docs_view(docs, *out, start) and _pyhost().str_view(flat, *ref)
     assert all((a == b).all() for a, b in zip(out, ref))
+    many = docs * 3000  # several thread ranges
+    fm = [s for d in many for side in d for s in side]
+    st = np.arange(0, 4 * len(many) + 1, 4, dtype=np.int64)
+    o2 = [np.empty(len(fm), np.int64), np.empty(len(fm), np.int64), np.empty(len(fm) + 1, np.int64)]
+    r2 = [np.empty(len(fm), np.int64), np.empty(len(fm), np.int64), np.empty(len(fm) + 1, np.int64)]
+    assert _pyhost().docs_view(many, *o2, st) and _pyhost().str_view(fm, *r2)
+    assert all((a == b).all() for a, b in zip(o2, r2))
+    bad_counts = st.copy()
+    bad_counts[5] += 1
+    assert not _pyhost().docs_view(many, *o2, bad_counts)
     for odd in ([(("a",), ("\u00e9",))], [(("a",),)], [("a", "b")], [(("a",), ("b",), ("c",))]):
-        assert not _pyhost().docs_view(odd, np.empty(4, np.int64), np.empty(4, np.int64), np.empty(5, np.int64))
+        assert not _pyhost().docs_view(odd, np.empty(4, np.int64), np.empty(4, np.int64), np.empty(5, np.int64),
+                                       np.array([0, 2], np.int64))
 
 
 def test_narrow_sentence_form():
