@@ -230,6 +230,7 @@ static PyObject *build_rows(PyObject *self, PyObject *args) {
     if (!out) goto fail_all;
     Py_ssize_t r = 0;
     for (Py_ssize_t k = 0; k < K; ++k) {
+      if (k + 2 < K && pq[k + 2] >= 0 && pq[k + 2] < nd) __builtin_prefetch(PyList_GET_ITEM(docs, pq[k + 2]));
       if (!cnt[k]) continue;
       Py_ssize_t two = 0, ns = 0, nt = 0;
       PyObject **side = pq[k] >= 0 && pq[k] < nd ? seq_items(PyList_GET_ITEM(docs, pq[k]), &two) : NULL;
@@ -246,6 +247,15 @@ static PyObject *build_rows(PyObject *self, PyObject *args) {
         memcpy(&score, m + 16 * r, 8);
         memcpy(&i, m + 16 * r + 8, 4);
         memcpy(&j, m + 16 * r + 12, 4);
+        if (c + 8 < cnt[k]) {  /* the str objects a few rows ahead: their refcounts are the misses here */
+          int32_t ia, ja;
+          memcpy(&ia, m + 16 * (r + 8) + 8, 4);
+          memcpy(&ja, m + 16 * (r + 8) + 12, 4);
+          if (ia >= 0 && ia < ns && ja >= 0 && ja < nt) {
+            __builtin_prefetch(src[ia], 1);
+            __builtin_prefetch(tgt[ja], 1);
+          }
+        }
         if (i < 0 || j < 0 || i >= ns || j >= nt) {
           PyErr_Format(PyExc_IndexError, "build_rows: match %zd = (%d, %d) outside a %zd x %zd pair", r, i, j, ns, nt);
           Py_DECREF(out);
