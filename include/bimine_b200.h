@@ -264,7 +264,8 @@ int bimine_agreement_batch(const bimine_match *matches_dev,
  * still reported with the usual error and no results.  sent_tok_off is
  * rebuilt on the device as the exclusive sum of sent_len; when the
  * caller's offsets differ from that packed layout they are uploaded and
- * the scores computed again. */
+ * the scores computed again.  Calls on one device run one at a time (other
+ * threads' calls wait inside). */
 int bimine_mine_host(const bimine_dict *dict, const double *model,
                      const bimine_batch *batch_host, double gap,
                      double threshold, double mismatch, double bonus,

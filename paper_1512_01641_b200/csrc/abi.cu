@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <map>
+#include <memory>
 #include <cstring>
 #include <condition_variable>
 #include <functional>
@@ -1164,6 +1165,17 @@ int bimine_nw_fill_wavefront(double *dp, const double *sim, int64_t n, int64_t m
 // end to end from host buffers
 // ------------------------------------------------------------------------
 
+std::mutex &mine_host_mutex() {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<std::mutex>> per_dev;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  std::unique_ptr<std::mutex> &m = per_dev[dev];
+  if (!m) m.reset(new std::mutex());
+  return *m;
+}
+
 // Under lazy module loading (CUDA_MODULE_LOADING=LAZY, the CUDA 12 default)
 // a kernel is loaded at its first launch, and that load can wait for the
 // device to go idle.  bimine_mine_host's score kernel waits on copies still
@@ -1220,6 +1232,10 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   pool_setup();
   cudaStream_t st = as_stream(stream);
   BIMINE_CUDA(preload_kernels(st));
+  // One call per device at a time: the calls share the device's copy
+  // stream, and a call's score CTAs (persistent, possibly on every SM) wait
+  // for uploads that must not queue behind another call's scan kernel.
+  std::unique_lock<std::mutex> call_lock(mine_host_mutex());
   // Uploads start at once on a copy stream: pair and sentence arrays, then
   // the tokens in `nt` equal pieces, a device counter bumped after each
   // (1 = pairs + sentences, 1 + j = token pieces 0..j-1).  Meanwhile host

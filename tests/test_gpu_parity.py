@@ -528,6 +528,33 @@ def test_mine_host_narrow_wire_form(pinned):
     assert bits_equal(got[2], want[2])
 
 
+def test_mine_host_concurrent_calls_one_device():
+    """bimine_mine_host from several host threads on one device at once
+    (pageable inputs: the staged upload path) gives every caller its own
+    results -- calls on one device are serialised inside the library, so
+    one call's waiting score CTAs never hold the SMs another call's upload
+    pipeline needs."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    d_list = []
+    for seed in range(4):
+        c = synth.make_config(2, seed_base=20261018 + 7 * seed, n_pairs=120 + 40 * seed)
+        d_list.append(c)
+    # one dictionary for all (the first corpus's), every batch mined with it
+    d = d_list[0].dictionary
+    model = model_vector(H.synth_model())
+    dd = E.LexiconContext(vocab=None, coo=(d.src, d.tgt, d.prob), devices={}).on(E.current_device())
+    batches = [c.batch if k % 2 else c.batch.with_24bit_tokens().with_narrow_sentences() for k, c in enumerate(d_list)]
+    want = [E.mine_host(dd, model, b, 2.0, 0.5, -1.0, 1.0, want_sim=True) for b in batches]
+    with ThreadPoolExecutor(4) as ex:
+        got = list(ex.map(lambda b: E.mine_host(dd, model, b, 2.0, 0.5, -1.0, 1.0, want_sim=True), batches * 2))
+    for k, g in enumerate(got):
+        w = want[k % 4]
+        assert np.array_equal(g[0], w[0])
+        assert np.array_equal(g[1].view(np.uint8), w[1].view(np.uint8))
+        assert bits_equal(g[2], w[2])
+
+
 @pytest.mark.parametrize("chunks", ["3", "7"])
 def test_mine_host_chunked_uploads(chunks):
     """bimine_mine_host with the batch uploaded in chunks (the score kernel
