@@ -1238,10 +1238,11 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   std::unique_lock<std::mutex> call_lock(mine_host_mutex());
   // Uploads start at once on a copy stream: pair and sentence arrays, then
   // the tokens in `nt` equal pieces, a device counter bumped after each
-  // (1 = pairs + sentences, 1 + j = token pieces 0..j-1).  Meanwhile host
-  // threads check and plan the batch in chunks of pairs and record each
-  // pair's counter value; the score kernel's CTA for a pair starts once the
-  // counter reaches it.
+  // (1 = pairs + sentences, 1 + j = token pieces 0..j-1).  The score kernel
+  // is launched right behind them; each of its CTAs derives the counter
+  // value its pair needs (pair_kernel.cuh, self gate).  Meanwhile host
+  // threads check and plan the batch in chunks of pairs; the rest of the
+  // path follows the plan.
   static const int max_chunks = [] {
     const char *v = getenv("BIMINE_E2E_CHUNKS");
     return v ? std::max(1, atoi(v)) : 16;
@@ -1259,7 +1260,8 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   std::vector<int64_t> cut(nc + 1), tcut(nt + 1);
   for (int k = 0; k <= nc; ++k) cut[k] = P * k / nc;
   for (int j = 0; j <= nt; ++j) tcut[j] = T * j / nt;
-  // pinned staging: slot offsets [P] | per-pair need [P] (int32) | ready values [nt + 1] | merged work
+  // pinned staging: slot offsets [P] | counter values [nt + 1] (int32) | merged work | tiles | piece
+  // boundaries
   int64_t work_bound = 0, n_tiles_pre = 0;  // (tiles: the 64x64 blocks of pairs larger than 64x64)
   for (int64_t p = 0; p < P; ++p) {
     const int32_t n = h->pair_n[p], m = h->pair_m[p];
@@ -1267,14 +1269,13 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     work_bound += 3 + 3 * tl;
     if (n > kPairMax || m > kPairMax) n_tiles_pre += tl;
   }
-  const int64_t n_stage = P + (P + 1) / 2 + (nt + 2) / 2 + 1 + std::max<int64_t>(work_bound, 1) +
+  const int64_t n_stage = P + (nt + 2) / 2 + 1 + std::max<int64_t>(work_bound, 1) +
                           3 * std::max<int64_t>(n_tiles_pre, 0) + (nt + 1);
   int64_t *staging = (int64_t *)pinned_scratch(sizeof(int64_t) * n_stage);
   if (!staging) return fail(BIMINE_E_CUDA, "bimine_mine_host: pinned staging allocation failed");
   int64_t *out_off = staging;
-  int32_t *need = (int32_t *)(staging + P);
-  int32_t *ready_vals = need + P;
-  int64_t *work = staging + P + (P + 1) / 2 + (nt + 2) / 2 + 1;
+  int32_t *ready_vals = (int32_t *)(staging + P);
+  int64_t *work = staging + P + (nt + 2) / 2 + 1;
   int64_t *tiles_pre = work + std::max<int64_t>(work_bound, 1);
   int64_t *tcut_pinned = tiles_pre + 3 * n_tiles_pre;  // the piece boundaries, uploaded with the pair arrays
   for (int j = 0; j <= nt; ++j) tcut_pinned[j] = tcut[j];
@@ -1314,7 +1315,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
                o_pm = carve(4 * P), o_psim = carve(8 * P), o_outoff = carve(8 * P), o_sim = carve(8 * cells),
                o_slots = carve(sizeof(bimine_match) * cap), o_counts = carve(4 * P), o_base = carve(8 * P),
                o_comp = carve(sizeof(bimine_match) * cap), o_total = carve(8),
-               o_work = carve(8 * std::max<int64_t>(work_bound, 1)), o_tiles = carve(8 * std::max<int64_t>(3 * n_tiles_pre, 1)), o_need = carve(4 * P), o_ready = carve(4),
+               o_work = carve(8 * std::max<int64_t>(work_bound, 1)), o_tiles = carve(8 * std::max<int64_t>(3 * n_tiles_pre, 1)), o_ready = carve(4),
                o_tcut = carve(8 * (size_t)(nt + 1));
   // sent_tok_off is not uploaded: the copy stream rebuilds it from sent_len
   // (the usual packed layout); the analysis threads check that the caller's
@@ -1525,10 +1526,6 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
         c.err = "bimine_mine_host: token range out of bounds";
         return;
       }
-      int j = (int)std::min<int64_t>(nt - 1, (te - 1) * nt / T);  // piece of the last token read
-      while (j > 0 && tcut[j] > te - 1) --j;
-      while (j + 1 < nt && tcut[j + 1] <= te - 1) ++j;
-      need[p] = j + 2;
     }
     bimine_batch hv = *h;
     hv.n_pairs = p1 - p0;
