@@ -5,8 +5,9 @@ pairs on both sides of the 64-sentence tile boundary, target documents
 with more distinct tokens than one shared-memory chunk, sentences up to 300
 tokens (past the 255-token limit of pair_kernel), dictionaries with
 duplicate and zero-probability entries and tokens without any row, and
-random mining settings.  Score matrices must be bit-identical, and match
-counts and mined (score, i, j) triples equal.
+random mining settings, sent in the int32 or the compact wire form.  Score
+matrices must be bit-identical, and match counts and mined (score, i, j)
+triples equal.
 """
 
 import numpy as np
@@ -63,7 +64,8 @@ def batches(draw):
     prob[rng.random(n_entries) < 0.05] = 0.0  # dropped like read_lexicon + the p > 0 rule
     gap = draw(st.sampled_from([0.0, 0.5, 1.3, 2.0, 3.7]))
     thr = draw(st.sampled_from([0.0, 0.3, 0.5, 0.9, 1.0]))
-    return batch, (src, tgt, prob), gap, thr
+    wire = draw(st.booleans())  # bimine_mine_host's compact wire form (24-bit ids, uint16 sentence arrays)
+    return batch, (src, tgt, prob), gap, thr, wire
 
 
 @settings(max_examples=60, deadline=None, derandomize=True, suppress_health_check=list(HealthCheck))
@@ -72,13 +74,14 @@ def test_random_batches_match_oracle(case):
     from paper_1512_01641_b200 import engine as E
     from paper_1512_01641_b200.classifier import model_vector
 
-    batch, (src, tgt, prob), gap, thr = case
+    batch, (src, tgt, prob), gap, thr, wire = case
     model = model_vector(H.synth_model())
     od = oracle.OracleDict(src, tgt, prob)
     want_sim = oracle.score_batch(od, model, batch)
     want_counts, want_rows = oracle.mine_batch(od, model, batch, gap=gap, threshold=thr)
     dd = E.LexiconContext(vocab=None, coo=(src, tgt, prob), devices={}).on(E.current_device())
-    counts, matches, sim = E.mine_host(dd, model, batch, gap, thr, -1.0, 1.0, want_sim=True)
+    sent = batch.with_24bit_tokens().with_narrow_sentences() if wire else batch
+    counts, matches, sim = E.mine_host(dd, model, sent, gap, thr, -1.0, 1.0, want_sim=True)
     assert np.array_equal(sim.view(np.uint64), want_sim.view(np.uint64))
     assert np.array_equal(counts, want_counts)
     flat = np.concatenate(want_rows) if want_rows else np.zeros(0, dtype=matches.dtype)
