@@ -104,16 +104,19 @@ struct PinnedScratch {
   }
 };
 thread_local PinnedScratch tl_pinned;
-void *pinned_scratch(size_t bytes) {
-  if (tl_pinned.n < bytes) {
-    if (tl_pinned.p) cudaFreeHost(tl_pinned.p);
-    tl_pinned.p = nullptr;
-    tl_pinned.n = 0;
-    if (cudaMallocHost(&tl_pinned.p, bytes) != cudaSuccess) return nullptr;
-    tl_pinned.n = bytes;
+void *pinned_grow(PinnedScratch &b, size_t bytes) {
+  if (b.n < bytes) {
+    if (b.p) cudaFreeHost(b.p);
+    b.p = nullptr;
+    b.n = 0;
+    if (cudaMallocHost(&b.p, bytes) != cudaSuccess) return nullptr;
+    b.n = bytes;
   }
-  return tl_pinned.p;
+  return b.p;
 }
+void *pinned_scratch(size_t bytes) { return pinned_grow(tl_pinned, bytes); }
+// a small batch's whole upload, laid out like the device arena's front
+thread_local PinnedScratch tl_mirror;
 
 // Upload gate of bimine_mine_host: the score kernel waits per chunk; the
 // launches that read everything (long-sentence kernel, NW) wait for `all`.
@@ -1310,17 +1313,20 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   if (h->token_bytes != 0 && h->token_bytes != 3 && h->token_bytes != 4)
     return fail(BIMINE_E_ARG, "bimine_mine_host: token_bytes must be 3 or 4");
   const int tb = h->token_bytes == 3 ? 3 : 4;  // bytes per token id on the wire and on the device
-  const size_t o_tok = carve((size_t)tb * T + 4), o_soff = carve(8 * S), o_slen = carve(4 * S), o_suniq = carve(4 * S),
-               o_schar = carve(4 * S), o_psrc = carve(8 * P), o_pn = carve(4 * P), o_ptgt = carve(8 * P),
-               o_pm = carve(4 * P), o_psim = carve(8 * P), o_outoff = carve(8 * P), o_sim = carve(8 * cells),
-               o_slots = carve(sizeof(bimine_match) * cap), o_counts = carve(4 * P), o_base = carve(8 * P),
-               o_comp = carve(sizeof(bimine_match) * cap), o_total = carve(8),
-               o_work = carve(8 * std::max<int64_t>(work_bound, 1)), o_tiles = carve(8 * std::max<int64_t>(3 * n_tiles_pre, 1)), o_ready = carve(4),
-               o_tcut = carve(8 * (size_t)(nt + 1));
+  // the uploaded arrays first (one contiguous front, so a small batch goes
+  // up in one transfer), then the device-only buffers
+  const size_t o_tok = carve((size_t)tb * T + 4), o_slen = carve(4 * S), o_suniq = carve(4 * S),
+               o_schar = carve(4 * S), o_s16 = carve(narrow ? 6 * (size_t)S : 1), o_psrc = carve(8 * P),
+               o_pn = carve(4 * P), o_ptgt = carve(8 * P), o_pm = carve(4 * P), o_psim = carve(8 * P),
+               o_outoff = carve(8 * P), o_tcut = carve(8 * (size_t)(nt + 1));
+  const size_t up_end = off;  // end of the uploaded front
+  const size_t o_soff = carve(8 * S), o_sim = carve(8 * cells), o_slots = carve(sizeof(bimine_match) * cap),
+               o_counts = carve(4 * P), o_base = carve(8 * P), o_comp = carve(sizeof(bimine_match) * cap),
+               o_total = carve(8), o_work = carve(8 * std::max<int64_t>(work_bound, 1)),
+               o_tiles = carve(8 * std::max<int64_t>(3 * n_tiles_pre, 1)), o_ready = carve(4);
   // sent_tok_off is not uploaded: the copy stream rebuilds it from sent_len
   // (the usual packed layout); the analysis threads check that the caller's
   // offsets are exactly that, else they are uploaded on `st` before scoring
-  const size_t o_s16 = carve(narrow ? 6 * (size_t)S : 1);  // the narrow arrays as uploaded: len | uniq | chars
   size_t scan_bytes = 0;
   BIMINE_CUDA(offsets_from_lengths(nullptr, nullptr, S, nullptr, &scan_bytes, st));
   const size_t o_scan = carve(std::max<size_t>(scan_bytes, 1));
@@ -1356,6 +1362,12 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   std::promise<cudaError_t> phase1;  // sentence arrays, offsets scan and ev_scan enqueued
   std::future<cudaError_t> phase1_done = phase1.get_future();
   cudaError_t up_err = cudaSuccess;
+  // A small batch goes up in ONE transfer: its arrays are copied on the
+  // host into a page-locked mirror of the arena's front (each transfer of
+  // the general path costs ~5-10 us of setup: a one-pair call waited ~70
+  // us for a dozen of them before the score kernel could start)
+  constexpr size_t kSmallUpload = 512 << 10;
+  char *mirror = up_end <= kSmallUpload ? (char *)pinned_grow(tl_mirror, up_end) : nullptr;
   auto upload = [&, dev_id, e0 = e]() {
     cudaSetDevice(dev_id);
     Stager sg(cs, dev_id);
@@ -1363,6 +1375,44 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     auto H2D = [&](size_t o, const void *src, size_t bytes, bool pg) {
       if (ue == cudaSuccess && bytes) ue = sg.copy(arena + o, src, bytes, pg);
     };
+    if (mirror) {
+      auto put = [&](size_t o, const void *src, size_t bytes) {
+        if (bytes) memcpy(mirror + o, src, bytes);
+      };
+      put(o_tok, h->tokens, (size_t)tb * T);
+      if (narrow) {
+        put(o_s16, h->sent_len, 2 * S);
+        put(o_s16 + 2 * S, h->sent_uniq, 2 * S);
+        put(o_s16 + 4 * S, h->sent_chars, 2 * S);
+      } else {
+        put(o_slen, h->sent_len, 4 * S);
+        put(o_suniq, h->sent_uniq, 4 * S);
+        put(o_schar, h->sent_chars, 4 * S);
+      }
+      put(o_psrc, h->pair_src, 8 * P);
+      put(o_pn, h->pair_n, 4 * P);
+      put(o_ptgt, h->pair_tgt, 8 * P);
+      put(o_pm, h->pair_m, 4 * P);
+      put(o_psim, h->pair_sim_off, 8 * P);
+      put(o_outoff, out_off, 8 * P);
+      put(o_tcut, tcut_pinned, 8 * (size_t)(nt + 1));
+      if (ue == cudaSuccess) ue = cudaMemcpyAsync(arena, mirror, up_end, cudaMemcpyHostToDevice, cs);
+      if (narrow && ue == cudaSuccess && S > 0) {
+        widen_u16_kernel<<<(unsigned)std::min<int64_t>((3 * S + 255) / 256, 4096), 256, 0, cs>>>(
+            (const uint16_t *)(arena + o_s16), S, (int32_t *)(arena + o_slen), (int32_t *)(arena + o_suniq),
+            (int32_t *)(arena + o_schar));
+        ue = cudaGetLastError();
+      }
+      if (ue == cudaSuccess)
+        ue = offsets_from_lengths((const int32_t *)(arena + o_slen), (int64_t *)(arena + o_soff), S,
+                                  arena + o_scan, &scan_bytes, cs);
+      ue = ue ? ue : cudaEventRecord(ev_scan, cs);
+      H2D(o_ready, &ready_vals[nt], 4, false);  // nt + 1: everything is in place
+      phase1.set_value(ue);
+      ue = ue ? ue : cudaEventRecord(ev_all, cs);
+      up_err = ue;
+      return;
+    }
     H2D(o_psrc, h->pair_src, 8 * P, pg_pairs);
     H2D(o_pn, h->pair_n, 4 * P, pg_pairs);
     H2D(o_ptgt, h->pair_tgt, 8 * P, pg_pairs);
@@ -1401,7 +1451,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
     up_err = ue ? ue : de;
   };
   std::thread uploader;
-  if (staged) {
+  if (staged && !mirror) {
     uploader = std::thread(upload);
   } else {
     upload();
