@@ -122,7 +122,6 @@ thread_local PinnedScratch tl_mirror;
 // launches that read everything (long-sentence kernel, NW) wait for `all`.
 struct UploadGate {
   const int32_t *ready;  // grows as pieces land
-  const int32_t *need;   // per pair: the counter value its data need (null: the CTAs derive it)
   cudaEvent_t all;
   std::function<void()> before_all;  // host side: `all` is recorded once this returns
   bool pair_launched = false;        // the pair kernel already runs (bimine_mine_host launches it early)
@@ -669,7 +668,6 @@ int launch_pair_kernel(const bimine_dict *dict, const double *model, const bimin
   A.features = features;
   if (gate) {
     A.ready = gate->ready;
-    A.need = gate->need;
     A.n_sentences = gate->n_sentences;
     A.n_tokens = gate->n_tokens;
     A.n_pieces = gate->n_pieces;
@@ -1494,7 +1492,7 @@ int bimine_mine_host(const bimine_dict *dict, const double *model, const bimine_
   d.pair_m = (const int32_t *)(arena + o_pm);
   d.pair_sim_off = (const int64_t *)(arena + o_psim);
   d.sent_bytes = 4;  // (widened on the device)
-  UploadGate gate{(const int32_t *)(arena + o_ready), nullptr, ev_all, join_uploader};
+  UploadGate gate{(const int32_t *)(arena + o_ready), ev_all, join_uploader};
   gate.n_sentences = S;
   gate.n_tokens = T;
   gate.n_pieces = nt;

@@ -71,17 +71,15 @@ struct PairArgs {
   // features mode (extract_features, classifier.py:62-112): the six
   // features of every cell at features[6 * (pair_sim_off + i * M + j) + k]
   double *features;
-  // upload gate (bimine_mine_host): pair p's data are on the device once
-  // *ready >= need[p] (the counter grows as pieces land); null: no wait
-  const int32_t *ready;
-  const int32_t *need;
   unsigned long long *next_item;  // the persistent CTAs' work counter (zeroed before the launch)
-  // need == null with ready set: the CTA derives its counter value itself
-  // (bimine_mine_host launches before the host has looked at the batch):
+  // upload gate (bimine_mine_host; null: the data are in place): a counter
+  // that grows as upload pieces land.  bimine_mine_host launches before the
+  // host has looked at the batch, so each CTA derives the value it needs:
   // once the pair and sentence arrays are in (ready >= 1) it bounds-checks
   // its pair against these sizes -- skipping it if out of range, the host
   // reports the error -- and waits for the piece of its last token; token
   // piece k covers [piece_start[k], piece_start[k + 1]), k < n_pieces
+  const int32_t *ready;
   int64_t n_sentences, n_tokens;
   int32_t n_pieces;
   const int64_t *piece_start;
@@ -241,9 +239,9 @@ __device__ __forceinline__ void pair_item(const PairArgs &A, PairSmem &S, const 
   } else {
     p = item - A.n_tiles;
   }
-  const bool self_gate = A.ready && !A.need;
-  if (A.ready) {  // wait until the chunk holding this pair's data has landed
-    if (threadIdx.x == 0) wait_ready(A.ready, self_gate ? 1 : A.need[p]);
+  const bool self_gate = A.ready != nullptr;
+  if (self_gate) {  // the pair and sentence arrays first
+    if (threadIdx.x == 0) wait_ready(A.ready, 1);
     __syncthreads();
   }
   const int Nfull = A.b.pair_n[p], Mfull = A.b.pair_m[p];
