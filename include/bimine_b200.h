@@ -273,6 +273,12 @@ int bimine_mine_host(const bimine_dict *dict, const double *model,
                      int64_t capacity, int64_t *total_host, double *sim_host,
                      void *stream);
 
+/* Host memcpy of `bytes` from src to dst over the library's copy threads
+ * (BIMINE_STAGE_THREADS helpers + the caller) with streaming stores -- the
+ * copy bimine_mine_host stages pageable inputs with; for a caller that
+ * fills its own page-locked staging (the tuning sweep's re-uploads). */
+int bimine_host_copy(void *dst, const void *src, int64_t bytes);
+
 /* ---- host tokenizer and joint vocabulary (text.py:97-104) ---------------
  * A vocabulary maps token strings (UTF-8 bytes) to dense int32 ids; one
  * vocabulary holds the dictionary's strings and every sentence token, so

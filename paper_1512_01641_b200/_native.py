@@ -128,6 +128,7 @@ SIGNATURES = {
     "bimine_vocab_word": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_char_p), _i64p]),
     "bimine_tokenize_batch": (ctypes.c_int, [_vp, ctypes.c_char_p, _i64p, ctypes.c_int64, _i32p, ctypes.c_int64,
                                              _i64p, _i32p, _i32p, _i32p]),
+    "bimine_host_copy": (ctypes.c_int, [_vp, _vp, ctypes.c_int64]),
     "bimine_tokenize_ptrs": (ctypes.c_int, [_vp, _vp, _i64p, ctypes.c_int64, _i64p, _i32p, ctypes.c_int64, _i64p,
                                             _i32p, _i32p, _i32p]),
 }

@@ -1711,6 +1711,12 @@ extern "C" int bimine_debug_band_times(uint64_t *out, int n) {
 }
 #endif
 
+int bimine_host_copy(void *dst, const void *src, int64_t bytes) {
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(BIMINE_E_ARG, "bimine_host_copy: bad arguments");
+  if (bytes) MemcpyPool::get().copy(dst, src, (size_t)bytes);
+  return BIMINE_OK;
+}
+
 // ------------------------------------------------------------------------
 // test hook: the device exp
 // ------------------------------------------------------------------------

@@ -419,15 +419,20 @@ class DeviceTuner:
             self.t_gap.copy_(self.torch.from_numpy(self.trials[1]))
 
     def upload(self, batch: PackedBatch) -> None:
-        """The batch's arrays into the staging, then non-blocking H2D copies
-        on the tuner's stream (same shapes as the tuner's batch)."""
+        """The batch's arrays into the staging (the library's threaded
+        streaming copy), then non-blocking H2D copies on the tuner's stream
+        (same shapes as the tuner's batch)."""
         torch = self.torch
+        L = N.load()
         with torch.cuda.stream(self.stream):
             for f in _FIELDS:
-                a = getattr(batch, f)
+                a = np.ascontiguousarray(getattr(batch, f))
                 h = self.host[f]
                 if a.shape[0]:
-                    h[: a.shape[0]].numpy()[:] = a
+                    hv = h[: a.shape[0]].numpy()
+                    if a.dtype != hv.dtype:
+                        a = a.astype(hv.dtype)
+                    N.check(L.bimine_host_copy(hv.ctypes.data, a.ctypes.data, a.nbytes))
                     self.db.t[f][: a.shape[0]].copy_(h[: a.shape[0]], non_blocking=True)
 
     def run_device(self, events=None) -> None:
