@@ -178,6 +178,38 @@ def synth_fixtures(model, lexicon_c2):
     run(c2, lexicon_c2, list(range(12)), "synth_c2")
 
 
+def extreme_fixture():
+    """Reference score matrices and mined rows with dictionary
+    probabilities of every float class (tests/helpers.py
+    extreme_probabilities): subnormal, tied, > 1, dropped (zero, negative,
+    NaN), overflowing and infinite values."""
+    import dataclasses
+
+    sys.path.insert(0, os.path.dirname(HERE))
+    import helpers as H
+    from bimine.classifier import load_model
+
+    model = load_model(os.path.join(HERE, "synth_model.json"))
+    sims, out = {}, {}
+    for variant in H.EXTREME_VARIANTS:
+        for cname, corpus, pairs in H.extreme_corpora():
+            d = corpus.dictionary
+            d = dataclasses.replace(d, prob=H.extreme_probabilities(d.prob, variant))
+            lexicon = Lexicon(d.table())
+            for p in pairs:
+                src, tgt = corpus.pair_sentences(p)
+                sim = build_score_matrix(model, lexicon, src, tgt)
+                key = f"{variant}_{cname}_{p}"
+                sims[key] = sim
+                al = nw_align(sim, MiningConfig())
+                out[key] = {"steps": step_codes(al), "score": float(al.score).hex(),
+                            "indices": [[float(s).hex(), i, j] for s, i, j in filter_by_threshold(sim, al, 0.5)]}
+                print(key, sim.shape, "distinct scores", len(np.unique(sim)), "matches", len(out[key]["indices"]))
+    np.savez_compressed(os.path.join(HERE, "extreme_sims.npz"), **sims)
+    with open(os.path.join(HERE, "extreme.json"), "w") as fh:
+        json.dump(out, fh)
+
+
 def nw_fixture():
     """Reference nw_align outputs on the reference tests' own instance
     families (test_align.py:38-43,68-115; test_acceptance.py:56-110)."""
@@ -451,7 +483,7 @@ def cli_fixture():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["toy", "synth", "nw", "exp", "tune", "cli", "lexicon", "features"]
+    which = sys.argv[1:] or ["toy", "synth", "extreme", "nw", "exp", "tune", "cli", "lexicon", "features"]
     if "cli" in which:
         cli_fixture()
     if "lexicon" in which:
@@ -465,6 +497,8 @@ if __name__ == "__main__":
         synth_fixtures(model, lex)
     if "nw" in which:
         nw_fixture()
+    if "extreme" in which:
+        extreme_fixture()
     if "exp" in which:
         exp_fixture()
     if "tune" in which:

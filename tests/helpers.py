@@ -129,3 +129,45 @@ def codes_of(steps) -> np.ndarray:
 
 def match_triples(rows):
     return [(float(s), int(i), int(j)) for s, i, j in rows]
+
+
+# Dictionary probabilities of every float class the reference's lexicon
+# reader admits (lexicon.py:165-178 keeps any float(field)); the p > 0 rules
+# (classifier.py:58,78) drop zero, negative and NaN entries.  The same
+# recipe makes the golden fixture (make_golden.py extreme_fixture) and
+# drives the CPU and GPU parity tests against it.
+EXTREME_VARIANTS = ("fine", "huge", "inf")
+
+
+def extreme_probabilities(prob: np.ndarray, variant: str, seed: int = 1512) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    u = rng.random(prob.size)
+    full = rng.random(prob.size)  # full-precision values in [0, 1)
+    pick = rng.integers(0, 3, size=prob.size)
+    p = prob.astype(np.float64).copy()
+    classes = [
+        (0.00, 0.10, full),
+        (0.10, 0.14, np.array([5e-324, 1e-310, 2.225073858507201e-308])[pick]),  # subnormal
+        (0.14, 0.17, np.array([1e-300, 2.2250738585072014e-308, 1e-30])[pick]),  # tiny normal
+        (0.17, 0.27, np.full(prob.size, 0.25)),  # ties
+        (0.27, 0.31, np.array([1.0, 3.5, 1e10])[pick]),  # >= 1
+        (0.31, 0.35, np.array([0.0, -0.5, np.nan])[pick]),  # dropped
+    ]
+    if variant == "huge":  # sums overflow to +inf
+        classes.append((0.35, 0.356, np.array([1e308, 1.5e308, 1.7976931348623157e308])[pick]))
+    elif variant == "inf":
+        classes.append((0.35, 0.352, np.full(prob.size, np.inf)))
+    elif variant != "fine":
+        raise ValueError(variant)
+    for lo, hi, v in classes:
+        sel = (u >= lo) & (u < hi)
+        p[sel] = v[sel]
+    return p
+
+
+def extreme_corpora():
+    """(name, corpus, pairs) the extreme-probability fixture covers: C1's
+    200 x 220 pair (tiled score path) and three C2 pairs (pair_kernel)."""
+    from paper_1512_01641_b200 import synth
+
+    return [("c1", synth.make_config(1), [0]), ("c2", synth.make_config(2, n_pairs=3), [0, 1, 2])]

@@ -4,7 +4,8 @@ hypothesis draws small vocabularies (many repeated and shared tokens),
 pairs on both sides of the 64-sentence tile boundary, target documents
 with more distinct tokens than one shared-memory chunk, sentences up to 300
 tokens (past the 255-token limit of pair_kernel), dictionaries with
-duplicate and zero-probability entries and tokens without any row, and
+duplicate and zero-probability entries and tokens without any row,
+probabilities of every float class (subnormal, > 1, NaN, overflowing, inf), and
 random mining settings, sent in the int32 or the compact wire form.  Score
 matrices must be bit-identical, and match counts and mined (score, i, j)
 triples equal.
@@ -62,6 +63,9 @@ def batches(draw):
     tgt = rng.integers(0, vocab, size=n_entries).astype(np.int32)
     prob = np.round(rng.random(n_entries), 6)
     prob[rng.random(n_entries) < 0.05] = 0.0  # dropped like read_lexicon + the p > 0 rule
+    extreme = draw(st.sampled_from([None, None, "fine", "huge", "inf"]))
+    if extreme:  # every float class read_lexicon admits (tests/helpers.py)
+        prob = H.extreme_probabilities(prob, extreme, seed=int(rng.integers(0, 2**31)))
     gap = draw(st.sampled_from([0.0, 0.5, 1.3, 2.0, 3.7]))
     thr = draw(st.sampled_from([0.0, 0.3, 0.5, 0.9, 1.0]))
     wire = draw(st.booleans())  # bimine_mine_host's compact wire form (24-bit ids, uint16 sentence arrays)

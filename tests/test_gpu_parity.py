@@ -271,6 +271,36 @@ def test_synthetic_fixtures_bit_exact():
             assert got == want
 
 
+@pytest.mark.parametrize("wire", [False, True])
+def test_extreme_probabilities_bit_exact(wire):
+    """Dictionary probabilities of every float class (subnormal, tied, > 1,
+    dropped zero/negative/NaN, sums overflowing to inf, +inf) through
+    bimine_mine_host, int32 and compact wire form: score matrices and mined
+    rows equal the reference's (extreme.json, made by make_golden.py)."""
+    model = model_vector(H.synth_model())
+    fx = H.load_json("extreme.json")
+    sims = H.load_npz("extreme_sims.npz")
+    for variant in H.EXTREME_VARIANTS:
+        for cname, corpus, pairs in H.extreme_corpora():
+            d = corpus.dictionary
+            coo = (d.src, d.tgt, H.extreme_probabilities(d.prob, variant))
+            dd = E.LexiconContext(vocab=None, coo=coo, devices={}).on(E.current_device())
+            sub = corpus.batch.select(pairs)
+            if wire:
+                sub = sub.with_24bit_tokens().with_narrow_sentences()
+            counts, matches, sim = E.mine_host(dd, model, sub, 2.0, 0.5, -1.0, 1.0, want_sim=True)
+            pos = 0
+            for k, p in enumerate(pairs):
+                key = f"{variant}_{cname}_{p}"
+                ref = sims[key]
+                n, m = ref.shape
+                assert bits_equal(sim[sub.pair_sim_off[k] : sub.pair_sim_off[k] + n * m].reshape(n, m), ref), key
+                want = [(float.fromhex(s), i, j) for s, i, j in fx[key]["indices"]]
+                got = [(float(r["score"]), int(r["i"]), int(r["j"])) for r in matches[pos : pos + counts[k]]]
+                pos += counts[k]
+                assert got == want, key
+
+
 def test_synthetic_c2_batch_vs_oracle():
     _synth_check(synth.make_config(2, n_pairs=400))
 

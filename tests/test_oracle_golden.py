@@ -125,3 +125,27 @@ def test_libm_exp_matches_golden():
     z = H.load_npz("exp_golden.npz")
     y = oracle.exp_array(z["x"])
     assert np.array_equal(y.view(np.uint64), z["y"].view(np.uint64))
+
+
+def test_extreme_probabilities_bit_exact():
+    """Dictionary probabilities of every float class (subnormal, tied, > 1,
+    dropped zero/negative/NaN, sums overflowing to inf, +inf): the oracle's
+    score matrices and mined rows equal the reference's (extreme.json)."""
+    model = model_vector(H.synth_model())
+    fx = H.load_json("extreme.json")
+    sims = H.load_npz("extreme_sims.npz")
+    for variant in H.EXTREME_VARIANTS:
+        for cname, corpus, pairs in H.extreme_corpora():
+            d = corpus.dictionary
+            od = oracle.OracleDict(d.src, d.tgt, H.extreme_probabilities(d.prob, variant))
+            sub = corpus.batch.select(pairs)
+            sim = oracle.score_batch(od, model, sub)
+            counts, per_pair = oracle.mine_batch(od, model, sub)
+            for k, p in enumerate(pairs):
+                key = f"{variant}_{cname}_{p}"
+                ref = sims[key]
+                n, m = ref.shape
+                got = sim[sub.pair_sim_off[k] : sub.pair_sim_off[k] + n * m].reshape(n, m)
+                assert np.array_equal(got.view(np.uint64), ref.view(np.uint64)), key
+                want = [(float.fromhex(s), i, j) for s, i, j in fx[key]["indices"]]
+                assert [(float(r["score"]), int(r["i"]), int(r["j"])) for r in per_pair[k]] == want, key
