@@ -558,6 +558,28 @@ def test_mine_host_narrow_wire_form(pinned):
     assert bits_equal(got[2], want[2])
 
 
+def test_mine_host_deterministic_across_calls():
+    """Reruns are byte-identical (the reference's acceptance criterion 9,
+    test_acceptance.py:279-326): 4,000 C2 pairs (~10M tokens, so the
+    upload runs in several gated token pieces and the persistent score CTAs
+    claim pairs in whatever order they land) mined eight times, alternating
+    the int32 and the compact wire form."""
+    corpus = synth.make_config(2, n_pairs=4_000)
+    d = corpus.dictionary
+    model = model_vector(H.synth_model())
+    dd = E.LexiconContext(vocab=None, coo=(d.src, d.tgt, d.prob), devices={}).on(E.current_device())
+    b = corpus.batch
+    assert b.n_tokens > 8 << 20
+    wire = b.with_24bit_tokens().with_narrow_sentences()
+    first = E.mine_host(dd, model, b, 2.0, 0.5, -1.0, 1.0, want_sim=True)
+    assert int(first[0].sum()) > 0
+    for k in range(8):
+        got = E.mine_host(dd, model, wire if k % 2 else b, 2.0, 0.5, -1.0, 1.0, want_sim=True)
+        assert np.array_equal(got[0], first[0]), k
+        assert np.array_equal(got[1].view(np.uint8), first[1].view(np.uint8)), k
+        assert bits_equal(got[2], first[2]), k
+
+
 def test_mine_host_concurrent_calls_one_device():
     """bimine_mine_host from several host threads on one device at once
     (pageable inputs: the staged upload path) gives every caller its own
